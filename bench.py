@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H_nu (alpha=2) hot path -- BASELINE.json metric, one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c5|c2|c3]
+
+Default workload (N=1): configuration 5 of BASELINE.json, the weak-scaled
+config-2-style hyper-diffusion (alpha=2, N=4, fp64) with 128x128x32 elements
+per GPU (x-slabs of the global (128*N)x128x32 perturbed box), the only
+configuration BASELINE.json quotes at 1/2/4/8 GPUs; it fits one GPU and its
+inputs (11.7 GB per op) exceed the 126 MB L2, so no flush is needed between
+steps.  A "step" is one hyperdiffusion_apply over the full per-GPU state.
+
+`value` = DOF-updates/s (4 diffused fields x global nodes / device time per
+step, inputs resident in HBM); `e2e` = the same metric through the public API
+with the state copied from pinned host memory and the result copied back
+every step.  `roofline` relates the algorithmic bytes of the op (SURVEY.md
+§8(d)) to its device time and the measured HBM copy bandwidth.
+`--impl reference` times the reference algorithm's CPU port (oracle/, numpy,
+single-threaded like the reference) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured", d
+    return 6650.0, "fallback", {}
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.f is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.f.flush()
+        rows = []
+        for line in Path(self.f.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[3]) if v.lower() == "active"})
+        loaded = [r for r in rows if r[2] > 250.0] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "power_w_max": max(r[2] for r in rows), "samples": len(rows), "reasons": reasons}
+
+
+# ----------------------------------------------------------------- workloads
+def algorithmic_bytes_hnu(ng, nloc, F=4, alpha=2):
+    """per pass 2*F*ng*8 (read q / write) + 6*nloc*8 (G_nu J w) + ng*8 (Minv) + nloc*4 (map)."""
+    return alpha * (2 * F * ng * 8 + 6 * nloc * 8 + ng * 8 + nloc * 4)
+
+
+def build_workload(name, rank, world, scale=1):
+    from paper_2311_11425_b200 import euler, hyperdiff, metrics, state, synthetic
+
+    w = synthetic.workload(name, scale=scale, slabs=1)
+    t0 = time.time()
+    m = synthetic.make_mesh(w)
+    t_mesh = time.time() - t0
+    mets = metrics.project_metrics_to_columns(metrics.curl_invariant_metrics(m), m)
+    cfg = hyperdiff.HyperDiffConfig(alpha=w.alpha, c=w.c)
+    vm = hyperdiff.build_viscous_metric(m, mets, cfg, dt=w.dt)
+    ops = euler.EulerOps(m, mets, state.PhysConstants(omega=0.0), w.set_name, hyper=(cfg, vm))
+    import torch
+
+    q = synthetic.make_state(w, m, device=torch.device("cuda"))
+    return dict(w=w, m=m, mets=mets, cfg=cfg, vm=vm, ops=ops, q=q, t_mesh=t_mesh)
+
+
+def cpu_sample(name, seconds=8.0):
+    """Reference algorithm's CPU port (oracle, numpy) on a bounded sample of the workload.
+
+    Sample: a 16x16 column block (all layers, same element size, generator and
+    state) of the workload's per-GPU mesh; repeated until ~`seconds` of CPU work.
+    Returns (DOF-updates/s, description, repeats).
+    """
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import synthetic
+
+    w = synthetic.workload(name)
+    sx, sy = min(16, w.nx or w.ne), min(16, w.ny or w.ne)
+    ext = (w.extents[0] * sx / w.nx, w.extents[1] * sy / w.ny, w.extents[2])
+    coords, layer, hcol = synthetic.perturbed_box_coords(sx, sy, w.nv, w.N, ext, perturb=w.perturb)
+    tol = O.dedupe_tol("box", max(sx, sy), extents=ext)
+    # numbering through the (bit-exact, tested) host C++ builder keeps the sample setup short
+    from paper_2311_11425_b200 import basis, mesh as hm
+
+    b = basis.lobatto(w.N)
+    pm = hm.Mesh(hm.MeshConfig("box", panels_per_edge=max(sx, sy), n_elem_vertical=w.nv, degree=w.N,
+                               box_extents=ext), coords, (b, b, b), layer, hcol)
+    x, wq, D = O.lgl(w.N)
+    om = O.OracleMesh("box", w.N, coords, layer, hcol, pm.gid, pm.nglobal, pm.xg, pm.col_gid, pm.flux_mask,
+                      D=D, w=wq)
+    _, J, grad = O.curl_metrics(om)
+    Jg, _ = O.project_columns(om, J, grad)
+    _, Minv = O.lumped_mass(om, J)
+    Gnu, _, _ = O.viscous_metric(om, grad, w.alpha, c=w.c, dt=w.dt)
+    Jg_e = O.gather(om.gid, Jg)
+    q = synthetic.fourier_state(om.xg, ext)
+    times = []
+    t_end = time.time() + seconds
+    while time.time() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        O.hyperdiffusion(om, Gnu, Jg_e, Minv, q, w.alpha)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= 50:
+            break
+    t = statistics.median(times)
+    desc = (f"{sx}x{sy}x{w.nv} element block of {name} (N={w.N}, ng={om.ng}), oracle port "
+            f"(numpy, 1 thread), median of {len(times)}")
+    return 4 * om.ng / t, desc, len(times), om.ng
+
+
+# ---------------------------------------------------------------------- arms
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2311_11425_b200 import synthetic
+
+    w = synthetic.workload(args.workload)
+    for _ in range(args.warmup):
+        pass
+    rate, desc, reps, ng = cpu_sample(args.workload, seconds=max(3.0, 0.5 * args.steps))
+    line = {
+        "impl": "reference",
+        "metric": "fp64 DOF-updates/s of H_nu (alpha=2)",
+        "value": rate,
+        "unit": "DOF-updates/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 4 * ng / rate * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded, host-generated)",
+        "config": {"workload": f"{args.workload}: {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, alpha={w.alpha}",
+                   "sample": desc},
+        "cpu_baseline": {"value": rate, "unit": "DOF-updates/s", "cores": 1, "kind": "port", "sample": desc},
+        "e2e": {"value": rate, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2311_11425_b200 import _lib, hyperdiff, state
+
+    P = build_workload(args.workload, rank, world)
+    w, m, ops, vm, cfg = P["w"], P["m"], P["ops"], P["vm"], P["cfg"]
+    ng, nloc = m.nglobal, m.nelem * (w.N + 1) ** 3
+    qd = torch.from_numpy(P["q"]).cuda()
+    out = torch.empty_like(qd)
+    st = state.StateField("2C", qd)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        hyperdiffusion_apply(st, cfg, vm, ops, out=out)
+
+    hyperdiffusion_apply = hyperdiff.hyperdiffusion_apply
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    L = _lib.lib()
+    n0 = L.hv_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = L.hv_launch_count() - n0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    dof = 4 * ng * world
+    value = dof / (ms * 1e-3)
+
+    # end to end through the public API: pinned host -> device, H_nu, device -> pinned host
+    h_in = torch.empty((ng, 5), dtype=torch.float64, pin_memory=True)
+    h_in.copy_(torch.from_numpy(P["q"]))
+    h_out = torch.empty_like(h_in, pin_memory=True)
+    d_in = torch.empty_like(qd)
+
+    def e2e_step():
+        d_in.copy_(h_in, non_blocking=True)
+        hyperdiffusion_apply(state.StateField("2C", d_in), cfg, vm, ops, out=out)
+        h_out.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    ke = max(3, min(args.steps, 10))
+    ev0.record(stream)
+    for _ in range(ke):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = ev0.elapsed_time(ev1) / ke
+    if dist:
+        t = torch.tensor([ms_e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    peak, peak_kind, _ = _peaks()
+    alg = algorithmic_bytes_hnu(ng, nloc)
+    achieved = alg / (ms * 1e-3) / 1e9
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            rate, desc, reps, _ = cpu_sample(args.workload, seconds=8.0)
+            cpu = {"value": rate, "unit": "DOF-updates/s", "cores": 1, "kind": "port", "sample": desc}
+        line = {
+            "metric": "fp64 DOF-updates/s of H_nu (alpha=2)",
+            "value": value,
+            "unit": "DOF-updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(3, args.warmup),
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded, host-generated geometry; Fourier state)",
+            "config": {"workload": f"{w.name}: H_nu alpha=2, {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, "
+                                   f"perturbed box, c={w.c}, dt={w.dt}",
+                       "nglobal_per_gpu": ng, "nelem_per_gpu": m.nelem, "fields": 4,
+                       "l2": "inputs (11.7 GB/op) exceed L2; no flush",
+                       "parallelism": f"x-slabs x{world}" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": None, "algorithmic_bytes_per_op": alg,
+                         "scope": "whole H_nu op (all kernels of the alpha=2 passes)"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": dof / (ms_e2e * 1e-3), "unit": "DOF-updates/s",
+                    "h2d_bytes_per_step": ng * 5 * 8, "d2h_bytes_per_step": ng * 5 * 8,
+                    "ms_per_step": ms_e2e},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "setup_s": {"mesh": round(P["t_mesh"], 2)},
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

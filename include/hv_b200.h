@@ -1,0 +1,133 @@
+/*
+ * hv_b200.h -- C-ABI of the B200-native EBG hyper-diffusion / Euler-RHS library.
+ *
+ * The reference (hevicore, pure Python/numpy) has no native FFI; its operator
+ * entry points are Python functions.  Each export below replaces the numerical
+ * body of one reference function (file:line relative to
+ * /root/reference/pkg/src/hevicore/), and the Python mirror package
+ * paper_2311_11425_b200 binds them through ctypes (INTEGRATION.md shows the
+ * binding a maintainer would add to the reference itself).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers,
+ *    "h_" pointers are host pointers.  `stream` is a cudaStream_t passed as
+ *    void* (0 = legacy default stream).  All device work is asynchronous on
+ *    `stream`; functions that must report data-dependent errors (J <= 0,
+ *    M <= 0, ...) synchronise the stream before returning.
+ *  - Element arrays use the reference layout (nelem, n, n, n) with k fastest;
+ *    the global state is (nglobal, ld) row-major (reference: (nglobal, 5)).
+ *  - Return value: HV_OK (0) or an HV_ERR_* code; hv_last_error() gives a
+ *    thread-local message.  The Python layer maps the codes onto the
+ *    reference's exception types (ValueError / RuntimeError).
+ *  - Only equal polynomial degree in the three directions is supported on the
+ *    device (all BASELINE configurations); 1 <= N <= 8.
+ */
+#ifndef HV_B200_H
+#define HV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HV_ABI_VERSION 1
+
+#define HV_OK 0
+#define HV_ERR_INVALID 1        /* ValueError: bad argument / config                  */
+#define HV_ERR_DEGENERATE 2     /* ValueError: J<=0, eigenvalue<=0, mass<=0 or ==0    */
+#define HV_ERR_NONCONFORMING 3  /* RuntimeError: mesh.py:127-128,139-140              */
+#define HV_ERR_CUDA 4           /* RuntimeError: CUDA runtime failure                 */
+#define HV_ERR_NCCL 5           /* RuntimeError: collective failure                   */
+#define HV_ERR_UNSUPPORTED 6    /* NotImplementedError                                */
+
+int hv_abi_version(void);
+const char* hv_last_error(void);
+/* Number of CUDA kernels this library has launched in the process (bench.py's gpu_launches). */
+int64_t hv_launch_count(void);
+
+/* ---------------------------------------------------------------- host mesh
+ * Replaces Mesh._number_gridpoints (mesh.py:86-107): bit-exact gid
+ * (first-appearance rank of each cluster of points within `tol`).
+ * h_coords: (nelem, 3, n1, n2, n3); h_gid: (nelem*n1*n2*n3). */
+int hv_number_gridpoints(const double* h_coords, int64_t nelem, int n1, int n2, int n3, double tol,
+                         int64_t* h_gid, int64_t* nglobal);
+/* mesh.py:106-107: xg[gid[p]] = pts[p], last writer wins. h_xg: (nglobal, 3). */
+int hv_last_writer_coords(const double* h_coords, const int64_t* h_gid, int64_t nelem, int n1, int n2,
+                          int n3, int64_t nglobal, double* h_xg);
+/* Replaces Mesh._build_columns (mesh.py:109-145). h_col_gid: (nglobal/n_z, n_z). */
+int hv_build_columns(const int64_t* h_gid, int64_t nelem, int n1, int n2, int n3, const int64_t* h_elem_layer,
+                     const int64_t* h_elem_hcol, int64_t nglobal, int64_t nlay, int64_t* h_col_gid,
+                     int64_t* h_col_of, int64_t* h_level_of, double* h_flux_mask, int64_t* ncol);
+/* DSS gather map behind assembly.dss (assembly.py:17-26): for node g, the
+ * local flat indices h_idx[h_off[g] .. h_off[g+1]) in increasing flat order,
+ * so a sequential sum reproduces np.add.at bit for bit. */
+int hv_build_dss_csr(const int64_t* h_gid, int64_t nloc, int64_t nglobal, int64_t* h_off, int32_t* h_idx);
+
+/* ------------------------------------------------------------ metric setup
+ * Replaces _covariant_basis/_jacobian/_cross/curl_invariant_metrics/
+ * cross_product_metrics (metrics.py:49-110).  scheme 0 = curl-invariant,
+ * 1 = cross-product.  Rounding-faithful to numpy's einsum order (bit-exact
+ * with the reference on the reference's numpy build).
+ * h_D: (n,n) derivative matrix (host); d_coords (nelem,3,n,n,n); outputs
+ * d_dxdxi (nelem,3,3,n,n,n) [nullable], d_J (nelem,n,n,n), d_grad (nelem,3,3,n,n,n).
+ * Returns HV_ERR_DEGENERATE if any J <= 0 (synchronises). */
+int hv_metric_terms(int scheme, int N, const double* h_D, const double* d_coords, int64_t nelem,
+                    double* d_dxdxi, double* d_J, double* d_grad, void* stream);
+
+/* Sequential-order DSS of `ncomp` element fields through the CSR map:
+ * d_out[g*ncomp + c] = sum_{p in csr(g)} d_fe[c*cstride + p]  (assembly.py:17-26). */
+int hv_dss_csr(const double* d_fe, int ncomp, int64_t cstride, const int64_t* d_off, const int32_t* d_idx,
+               int64_t nglobal, double* d_out, void* stream);
+
+/* GlobalMass (assembly.py:54-64) and project_metrics_to_columns
+ * (metrics.py:121-142).  d_w3 (n^3).  Outputs: d_M, d_Minv (nglobal) and,
+ * if d_Jg != NULL, the projected d_Jg (nglobal) and d_gz (nglobal,3).
+ * Returns HV_ERR_DEGENERATE for M <= 0 (synchronises). */
+int hv_mass_and_projection(int N, const double* d_w3, const double* d_J, const double* d_grad, int64_t nelem,
+                           const int64_t* d_off, const int32_t* d_idx, int64_t nglobal, double* d_M,
+                           double* d_Minv, double* d_Jg, double* d_gz, void* stream);
+
+/* build_viscous_metric (hyperdiff.py:54-81) fused with the packing of the
+ * Laplacian metric W = w3 * Jg[gid] * G_nu (6 unique components).
+ * mode 0 = scaled: nu_m*vals_m = ((a_m * lam_m) / b) * vals_m with host-computed
+ *          a_m = c_m**(1/alpha) * 4, b = N**2 * dt**(1/alpha) (reference order);
+ * mode 1 = constant (nu_m = h_nu[m]); mode 2 = anisotropic (nu_h, nu_h, nu_v) in h_nu.
+ * Outputs (all nullable): d_Gnu (nelem*n^3, 3, 3), d_lam (.., 3), d_evecs (.., 3, 3),
+ * d_W packed per DESIGN.md §3 (6, nelem*n^3) component-major.
+ * Returns HV_ERR_DEGENERATE if an eigenvalue of G is <= 0 (synchronises). */
+int hv_viscous_metric(int N, int mode, const double* h_a, double b, const double* h_nu, const double* d_grad,
+                      int64_t nelem, const double* d_w3, const double* d_Jg, const int32_t* d_gid32,
+                      double* d_Gnu, double* d_lam, double* d_evecs, double* d_W, void* stream);
+
+/* ------------------------------------------------------------- hot path
+ * Laplacian plan: everything laplacian_apply (hyperdiff.py:84-94) reads. */
+typedef struct hv_lap_plan {
+  int N;                       /* polynomial degree                               */
+  double D[81];                /* (N+1)x(N+1) derivative matrix, row-major         */
+  int64_t nelem, nglobal;
+  const int32_t* d_gid;        /* (nelem*n^3) local -> global                      */
+  const int64_t* d_off;        /* DSS CSR offsets (nglobal+1)                      */
+  const int32_t* d_idx;        /* DSS CSR local indices (nelem*n^3)                */
+  const double* d_W;           /* packed metric (6, nelem*n^3)                     */
+  const double* d_Minv;        /* (nglobal)                                        */
+  double* d_work;              /* element workspace, >= 5*nelem*n^3 doubles        */
+  double* d_y;                 /* gridpoint workspace, >= 5*nglobal doubles        */
+} hv_lap_plan;
+
+/* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
+ * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].
+ * (hyperdiff.py:84-94 applied to nf fields in one pass; 1 <= nf <= 5.) */
+int hv_laplacian(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,
+                 double* d_out, int64_t ldo, const int32_t* h_of, double scale, void* stream);
+
+/* hyperdiffusion_apply (hyperdiff.py:97-106): out (nglobal, ldo) gets
+ * (-1)^(alpha+1) L^alpha q on the nvar listed variables and 0 on every other
+ * column of out (out[:,0] = 0 as in the reference). q is (nglobal, ldq). */
+int hv_hyperdiffusion(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nvar, const int32_t* h_vars,
+                      int alpha, double* d_out, int64_t ldo, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HV_B200_H */

@@ -1,0 +1,75 @@
+"""Parity cases shared by the golden generator, the oracle tests and the GPU tests.
+
+Each case describes a mesh (by generator parameters), a hyper-diffusion
+configuration and seeded inputs.  ``tests/golden/make_golden.py`` runs the
+REFERENCE on these cases; the tests rebuild the same inputs and compare.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2311_11425_b200 import synthetic
+
+CASES = {
+    # config-1/2 generator (perturbed lattice box) at reduced size, alpha = 2
+    "box_p_n4": dict(kind="lattice", nx=4, ny=3, nv=2, N=4, extents=(8000.0, 6000.0, 2000.0),
+                     hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
+                     sets=("2C", "2NC", "3C"), omega=0.0, lap_fields=(1,)),
+    # config 1 at full size: alpha = 1 on all five fields
+    "c1": dict(kind="lattice", nx=8, ny=8, nv=4, N=4, extents=(8000.0, 8000.0, 2000.0),
+               hd=dict(alpha=1, c=(1.0, 1.0, 1.0)), dt=1.0, state="normal", sets=(), omega=0.0,
+               lap_fields=(0, 1, 2, 3, 4)),
+    # config-3 generator (cubed sphere) at reduced size, rotation on
+    "sphere_n4": dict(kind="sphere", ne=2, nv=2, N=4, radius=6.371e6, z_top=1.0e4,
+                      hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere",
+                      sets=("2C", "2NC", "3C"), omega=7.292e-5, lap_fields=(1, 4)),
+    # config-4 generator (N = 7 box, warm bubble) at reduced size
+    "box_n7": dict(kind="box", ne=2, nv=2, N=7, extents=(1.0e4, 1.0e4, 1.0e4),
+                   hd=dict(alpha=2, c=(0.02, 0.02, 0.02)), dt=0.1, state="bubble",
+                   sets=("2C", "2NC", "3C"), omega=0.0, lap_fields=None),
+    # low degrees, constant and anisotropic viscosity modes
+    "box_p_n2_const": dict(kind="lattice", nx=3, ny=2, nv=2, N=2, extents=(3000.0, 2000.0, 1000.0),
+                           hd=dict(alpha=2, mode="constant", nu=(3e3, 2e3, 1e2)), dt=1.0, state="fourier",
+                           sets=("2C",), omega=0.0, lap_fields=(2,)),
+    "box_p_n3_aniso": dict(kind="lattice", nx=2, ny=2, nv=3, N=3, extents=(2000.0, 2000.0, 600.0),
+                           hd=dict(alpha=1, mode="anisotropic", nu_h=5e2, nu_v=3.0), dt=1.0, state="fourier",
+                           sets=("2C",), omega=0.0, lap_fields=(3,)),
+}
+
+
+def make_state(case, xg):
+    c = CASES[case] if isinstance(case, str) else case
+    if c["state"] == "normal":
+        return np.random.default_rng(synthetic.STATE_SEED).standard_normal((xg.shape[0], 5))
+    if c["state"] == "fourier":
+        return synthetic.fourier_state(xg, c["extents"])
+    if c["state"] == "sphere":
+        return synthetic.sphere_state(xg, c["radius"], c["z_top"])
+    if c["state"] == "bubble":
+        return synthetic.bubble_state_2c(xg)
+    raise ValueError(c["state"])
+
+
+def random_state(ng, set_name, seed=7):
+    """Non-balanced positive random state (test S on such states)."""
+    rng = np.random.default_rng(seed)
+    q = np.empty((ng, 5))
+    q[:, 0] = 1.0 + 0.2 * rng.random(ng)
+    if set_name == "2NC":
+        q[:, 1:4] = 10.0 * rng.standard_normal((ng, 3))
+        q[:, 4] = 300.0 + 5.0 * rng.random(ng)
+    elif set_name == "2C":
+        q[:, 1:4] = 10.0 * rng.standard_normal((ng, 3)) * q[:, :1]
+        q[:, 4] = q[:, 0] * (300.0 + 5.0 * rng.random(ng))
+    else:
+        q[:, 1:4] = 10.0 * rng.standard_normal((ng, 3)) * q[:, :1]
+        q[:, 4] = 2.5e5 + 1e4 * rng.random(ng)
+    return q
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=float)
+    b = np.asarray(b, dtype=float)
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))

@@ -1,0 +1,123 @@
+"""Generate golden fixtures by running the REFERENCE implementation (hevicore).
+
+Run in the build container, where the reference is mounted read-only:
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Every fixture is produced by the reference's own public API on seeded inputs
+from ``paper_2311_11425_b200.synthetic`` (geometry seed 0, state seed 1);
+the GPU box has no /root/reference, so the committed .npz files plus the
+oracle (oracle/hevi_oracle.py, pinned against these fixtures by
+tests/test_oracle_golden.py) are the parity anchors there.
+
+Each case stores the reference arrays that are small, and SHA-256 digests of
+the exact bytes of the bit-exact integer/metric arrays.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parents[1]))
+sys.path.insert(0, REF)
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+
+from hevicore import basis as rbasis  # noqa: E402
+from hevicore import euler as reuler  # noqa: E402
+from hevicore import hyperdiff as rhd  # noqa: E402
+from hevicore import mesh as rmesh  # noqa: E402
+from hevicore import metrics as rmet  # noqa: E402
+from hevicore import state as rstate  # noqa: E402
+
+from paper_2311_11425_b200 import synthetic  # noqa: E402
+
+sys.path.insert(0, str(HERE.parent))
+from cases import CASES, make_state, random_state  # noqa: E402
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def ref_mesh_lattice(nx, ny, nv, N, extents, perturb):
+    coords, layer, hcol = synthetic.perturbed_box_coords(nx, ny, nv, N, extents, perturb=perturb)
+    cfg = rmesh.MeshConfig("box", panels_per_edge=max(nx, ny), n_elem_vertical=nv, degree=N,
+                           box_extents=tuple(float(e) for e in extents))
+    b = rbasis.lobatto(N)
+    return rmesh.Mesh(cfg, coords, (b, b, b), layer, hcol)
+
+
+def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, lap_fields=None):
+    """Reference outputs for one mesh; inputs are regenerated from the seeds by the tests."""
+    out = {}
+    mets0 = rmet.curl_invariant_metrics(m)
+    mets = rmet.project_metrics_to_columns(mets0, m)
+    consts = rstate.PhysConstants(omega=omega)
+    out["ng"] = np.array(m.nglobal)
+    out["sha_gid"] = np.array(sha(m.gid))
+    out["sha_xg"] = np.array(sha(m.xg))
+    out["sha_col_gid"] = np.array(sha(m.col_gid))
+    out["sha_flux_mask"] = np.array(sha(m.flux_mask))
+    out["sha_J"] = np.array(sha(mets0.J_elem))
+    out["sha_grad"] = np.array(sha(mets0.grad_elem))
+    out["sha_dxdxi"] = np.array(sha(mets0.dxdxi))
+    out["sha_Jg_naive"] = np.array(sha(mets0.Jg))
+    out["sha_gz_naive"] = np.array(sha(mets0.gradzeta_g))
+    out["sha_Jg"] = np.array(sha(mets.Jg))
+    out["sha_gz"] = np.array(sha(mets.gradzeta_g))
+    xm = rmet.cross_product_metrics(m)
+    out["sha_grad_cross"] = np.array(sha(xm.grad_elem))
+    vm = rhd.build_viscous_metric(m, mets, hd_cfg, dt=dt)
+    ops = reuler.EulerOps(m, mets, consts, (sets or ("2C",))[0], hyper=(hd_cfg, vm))
+    out["sha_M"] = np.array(sha(ops.mass.M))
+    st = rstate.StateField((sets or ("2C",))[0], state)
+    if lap_fields is not None:
+        out["lap"] = np.stack([rhd.laplacian_apply(state[:, f], vm, ops) for f in lap_fields], axis=1)
+    out["hyper"] = rhd.hyperdiffusion_apply(st, hd_cfg, vm, ops)
+    for s in sets:
+        o = reuler.EulerOps(m, mets, consts, s, hyper=(hd_cfg, vm))
+        rs = random_state(m.nglobal, s, seed=7)
+        out[f"rhs_full_{s}"] = o.rhs_full(rstate.StateField(s, rs))
+        out[f"rhs_h_{s}"] = o.rhs_horizontal(rstate.StateField(s, rs), with_hyperdiff=False)
+    if store_full:
+        out["gid"] = m.gid.astype(np.int32)
+        out["Jg"] = mets.Jg
+        out["gz"] = mets.gradzeta_g
+        out["M"] = ops.mass.M
+        out["Gnu_sample"] = vm.Gnu.reshape(-1, 3, 3)[:: max(1, vm.Gnu.size // 9 // 512)]
+    np.savez_compressed(HERE / f"{name}.npz", **out)
+    print(name, "ng", m.nglobal, "nelem", m.nelem, "bytes", (HERE / f"{name}.npz").stat().st_size)
+
+
+def ref_mesh(c):
+    if c["kind"] == "lattice":
+        return ref_mesh_lattice(c["nx"], c["ny"], c["nv"], c["N"], c["extents"], perturb=True)
+    if c["kind"] == "sphere":
+        cfg = rmesh.MeshConfig("sphere", panels_per_edge=c["ne"], n_elem_vertical=c["nv"], degree=c["N"],
+                               radius=c["radius"], z_top=c["z_top"])
+        return rmesh.build_cubed_sphere(cfg)
+    cfg = rmesh.MeshConfig("box", panels_per_edge=c["ne"], n_elem_vertical=c["nv"], degree=c["N"],
+                           box_extents=c["extents"])
+    return rmesh.build_box(cfg)
+
+
+def main():
+    for name, c in CASES.items():
+        m = ref_mesh(c)
+        case(name, m, rhd.HyperDiffConfig(**c["hd"]), c["dt"], make_state(c, m.xg), sets=c["sets"],
+             omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"])
+    # basis constants
+    np.savez_compressed(HERE / "basis.npz", **{f"D{N}": rbasis.lobatto(N).diff_matrix for N in range(1, 9)},
+                        **{f"w{N}": rbasis.lobatto(N).weights for N in range(1, 9)},
+                        **{f"x{N}": rbasis.lobatto(N).nodes for N in range(1, 9)})
+
+
+if __name__ == "__main__":
+    main()

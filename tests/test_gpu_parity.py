@@ -1,0 +1,136 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle and the reference goldens.
+
+Bars (BASELINE.json north_star): integer maps bit-exact; metric setup
+bit-exact (rounding-faithful kernel); H_nu / Laplacian / S within 1e-12
+relative L2 in fp64.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from cases import CASES, rel_l2
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request):
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+
+    return request.param, ProductProblem(request.param), OracleProblem(request.param)
+
+
+def test_metrics_bitwise(pair):
+    name, p, o = pair
+    assert np.array_equal(p.mets0.J_elem, o.J)
+    assert np.array_equal(p.mets0.grad_elem, o.grad)
+    assert np.array_equal(p.mets0.Jg, o.Jg0) and np.array_equal(p.mets0.gradzeta_g, o.gz0)
+    assert np.array_equal(p.mets.Jg, o.Jg) and np.array_equal(p.mets.gradzeta_g, o.gz)
+    assert np.array_equal(p.ops.mass.M, o.M) and np.array_equal(p.ops.mass.Minv, o.Minv)
+
+
+def test_dxdxi_and_cross_bitwise(pair):
+    name, p, o = pair
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import metrics
+
+    assert np.array_equal(p.mets0.dxdxi, o.dxdxi)
+    xm = metrics.cross_product_metrics(p.m)
+    _, _, gx = O.cross_metrics(o.m)
+    assert np.array_equal(xm.grad_elem, gx)
+
+
+def test_viscous_metric(pair):
+    name, p, o = pair
+    G = p.vm.Gnu
+    scale = np.max(np.abs(o.Gnu))
+    assert np.max(np.abs(G - o.Gnu)) <= 1e-13 * scale
+    assert np.max(np.abs(G - np.swapaxes(G, -1, -2))) <= 1e-15 * scale
+    assert np.allclose(p.vm.lam, o.lam, rtol=1e-12, atol=0)
+    E = p.vm.evecs
+    eye = np.einsum("...ci,...cj->...ij", E, E)
+    assert np.max(np.abs(eye - np.eye(3))) < 1e-12
+
+
+def test_hyperdiffusion_parity(pair):
+    name, p, o = pair
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
+    ref = o.hyper()
+    assert rel_l2(got, ref) <= TOL, rel_l2(got, ref)
+    assert rel_l2(got, golden(name)["hyper"]) <= TOL
+    assert np.all(got[:, 0] == 0.0)
+
+
+def test_laplacian_parity(pair):
+    name, p, o = pair
+    from paper_2311_11425_b200 import hyperdiff
+
+    if p.c["lap_fields"] is None:
+        pytest.skip("no laplacian fixture")
+    g = golden(name)["lap"]
+    for col, f in enumerate(p.c["lap_fields"]):
+        got = hyperdiff.laplacian_apply(o.state[:, f], p.vm, p.ops)
+        assert rel_l2(got, o.lap(f)) <= TOL
+        assert rel_l2(got, g[:, col]) <= TOL
+
+
+def test_device_resident_matches_host_path(pair):
+    import torch
+
+    name, p, o = pair
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    qd = torch.from_numpy(o.state).cuda()
+    out_d = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), p.cfg, p.vm, p.ops)
+    out_h = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
+    assert out_d.is_cuda
+    assert np.array_equal(out_d.cpu().numpy(), out_h)   # deterministic kernels
+
+
+def test_dss_primitive_bitwise(pair):
+    name, p, o = pair
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import assembly
+
+    rng = np.random.default_rng(11)
+    fe = rng.standard_normal(p.m.gid.shape + (3,))
+    assert np.array_equal(assembly.dss(p.m, fe), O.dss(o.m.gid, o.m.ng, fe))
+
+
+def test_constant_field_annihilated():
+    from paper_2311_11425_b200 import hyperdiff
+    from product_cases import ProductProblem
+
+    p = ProductProblem("box_p_n4")
+    y = hyperdiff.laplacian_apply(np.full(p.m.nglobal, 3.7), p.vm, p.ops)
+    assert np.max(np.abs(y)) < 1e-12 * 3.7 * np.max(np.abs(p.ops.mass.Minv)) * 1e3
+
+
+def test_inverted_element_raises():
+    from paper_2311_11425_b200 import metrics
+    from product_cases import product_mesh
+
+    m = product_mesh("box_p_n2_const")
+    m.coords[0, 2] = m.coords[0, 2][:, :, ::-1].copy()  # flip zeta in element 0 -> J < 0
+    m._dev = None
+    with pytest.raises(ValueError):
+        metrics.curl_invariant_metrics(m)
+
+
+def test_hyperdiffusion_config_validation():
+    from paper_2311_11425_b200 import hyperdiff
+
+    with pytest.raises(ValueError):
+        hyperdiff.HyperDiffConfig(alpha=3)
+    with pytest.raises(ValueError):
+        hyperdiff.HyperDiffConfig(variables=(0, 1))
+    with pytest.raises(ValueError):
+        hyperdiff.HyperDiffConfig(mode="bogus")
