@@ -113,7 +113,26 @@ typedef struct hv_lap_plan {
   const double* d_Minv;        /* (nglobal)                                        */
   double* d_work;              /* element workspace, >= 5*nelem*n^3 doubles        */
   double* d_y;                 /* gridpoint workspace, >= 5*nglobal doubles        */
+  /* optional tile-sweep plan (tiles.py); d_gt == NULL selects the
+   * element-parallel path */
+  int TX, TY, nlay, n_z;
+  int64_t ntiles, nslot;
+  const int32_t* d_gt;         /* (ntiles, nlay, TX*N+1, TY*N+1, N+1) tile node gids */
+  const int32_t* d_code;       /* (ntiles, TX*N+1, TY*N+1) -1 or partial row         */
+  const int32_t* d_tmeta;      /* (ntiles, 2) active tile extent                     */
+  const int32_t* d_slot_col;   /* (nslot) shared column ids                           */
+  const int32_t* d_slot_row0;  /* (nslot) first partial row                           */
+  const int32_t* d_slot_nc;    /* (nslot) owning tiles per shared column              */
+  const int32_t* d_col_gid;    /* (ncol, n_z) int32 column gids                       */
+  const double* d_Wt;          /* tiled packed metric                                 */
+  double* d_part;              /* partial rows (rows, n_z, 5)                         */
 } hv_lap_plan;
+
+/* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
+ * Wt[t][l][c][k][e][i*n+j] using d_elem (ntiles, nlay, TX*TY),
+ * -1 for the absent elements of ragged tiles. */
+int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem, const double* d_W,
+                        int64_t nloc, double* d_Wt, void* stream);
 
 /* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
  * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].

@@ -42,6 +42,21 @@ class LapPlan(C.Structure):
         ("d_Minv", _P),
         ("d_work", _P),
         ("d_y", _P),
+        ("TX", C.c_int),
+        ("TY", C.c_int),
+        ("nlay", C.c_int),
+        ("n_z", C.c_int),
+        ("ntiles", _I64),
+        ("nslot", _I64),
+        ("d_gt", _P),
+        ("d_code", _P),
+        ("d_tmeta", _P),
+        ("d_slot_col", _P),
+        ("d_slot_row0", _P),
+        ("d_slot_nc", _P),
+        ("d_col_gid", _P),
+        ("d_Wt", _P),
+        ("d_part", _P),
     ]
 
 
@@ -59,6 +74,7 @@ _SIGS = {
     "hv_mass_and_projection": (C.c_int, [C.c_int, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "hv_viscous_metric": (C.c_int, [C.c_int, C.c_int, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
+    "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, _P, _P]),
     "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, _P]),
     # test hook (host build of the metric arithmetic); never used by the product path
     "hv_debug_metric_terms_host": (C.c_int, [C.c_int, C.c_int, _P, _P, _I64, _P, _P, _P]),

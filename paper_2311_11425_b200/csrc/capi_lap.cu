@@ -5,6 +5,7 @@
 
 #include "hv_common.h"
 #include "lap_common.cuh"
+#include "lap_tile.cuh"
 
 namespace {
 
@@ -24,7 +25,35 @@ int check_plan(const hv_lap_plan* P) {
   return HV_OK;
 }
 
+// Run one Laplacian pass with the best available kernel for this plan.
+int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
+             int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st) {
+  if (P->d_gt && hv::tile_supported(P->N, P->TX, P->TY, nf)) {
+    hv::TileArgs A{};
+    A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
+    A.ntiles = P->ntiles; A.nslot = P->nslot;
+    A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
+    A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
+    A.Wt = P->d_Wt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
+    A.zero_mask = zero_mask; A.scale = scale; A.out = out; A.part = P->d_part;
+    return hv::laplacian_tile(A, P->N, nf, P->D, st);
+  }
+  if (zero_mask) {
+    const int64_t tot = P->nglobal * ldo;
+    zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, P->nglobal, ldo, ~zero_mask);
+    HV_LAUNCH_CHECK();
+  }
+  return hv::laplacian_v1(P, q, ldq, nf, qf, out, ldo, of, scale, st);
+}
+
 }  // namespace
+
+extern "C" int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem,
+                                   const double* d_W, int64_t nloc, double* d_Wt, void* stream) {
+  if (N < 1 || N > 8 || TX < 1 || TY < 1 || ntiles <= 0 || nlay <= 0 || !d_elem || !d_W || !d_Wt)
+    HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_metric: bad arguments");
+  return hv::tile_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
+}
 
 extern "C" int hv_laplacian(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,
                             double* d_out, int64_t ldo, const int32_t* h_of, double scale, void* stream) {
@@ -39,7 +68,7 @@ extern "C" int hv_laplacian(const hv_lap_plan* P, const double* d_q, int64_t ldq
     qf.f[f] = h_qf[f];
     of.f[f] = h_of[f];
   }
-  return hv::laplacian_v1(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, (cudaStream_t)stream);
+  return lap_pass(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, 0u, (cudaStream_t)stream);
 }
 
 extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar,
@@ -59,13 +88,16 @@ extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_
     yf.f[v] = v;
     keep |= 1u << h_vars[v];
   }
-  const int64_t tot = P->nglobal * ldo;
-  zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_out, P->nglobal, ldo, nvar ? keep : 0u);
-  HV_LAUNCH_CHECK();
-  if (nvar == 0) return HV_OK;
+  const unsigned zmask = ((ldo >= 32) ? 0xffffffffu : ((1u << ldo) - 1u)) & ~keep;
+  if (nvar == 0) {
+    const int64_t tot = P->nglobal * ldo;
+    zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_out, P->nglobal, ldo, 0u);
+    HV_LAUNCH_CHECK();
+    return HV_OK;
+  }
   const double sign = (alpha % 2 == 1) ? 1.0 : -1.0;  // (-1)^(alpha+1)
-  if (alpha == 1) return hv::laplacian_v1(P, d_q, ldq, nvar, qf, d_out, ldo, of, sign, st);
-  rc = hv::laplacian_v1(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, st);
+  if (alpha == 1) return lap_pass(P, d_q, ldq, nvar, qf, d_out, ldo, of, sign, zmask, st);
+  rc = lap_pass(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, 0u, st);
   if (rc) return rc;
-  return hv::laplacian_v1(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, st);
+  return lap_pass(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st);
 }

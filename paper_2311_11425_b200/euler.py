@@ -7,11 +7,13 @@ run in ``libhv_b200.so``.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
 from .assembly import GlobalMass, weights3
-from .device import torch_mod
+from .device import to_dev, torch_mod
 
 __all__ = ["EulerOps"]
 
@@ -50,6 +52,26 @@ class EulerOps:
                           torch.empty(5 * dev.nglobal, dtype=torch.float64, device="cuda"))
         return self._work
 
+    def _tile_arrays(self):
+        """Device copy of the tile plan (tiles.py), or None for meshes it does not fit."""
+        if "tiles" not in self._h:
+            from .tiles import build_tile_plan, tile_shape
+
+            dev = self.mesh.device()
+            tp = None
+            if os.environ.get("HV_DISABLE_TILES", "0") != "1" and dev.N <= 7:
+                tp = build_tile_plan(self.mesh, *tile_shape(dev.N))
+            if tp is None:
+                self._h["tiles"] = None
+            else:
+                torch = torch_mod()
+                d = {k: to_dev(getattr(tp, k)) for k in ("gt", "code", "tmeta", "slot_col", "slot_row0", "slot_nc")}
+                d["elem"] = to_dev(tp.elem.reshape(tp.ntiles, tp.nlay, -1).astype(np.int32))
+                d["col_gid"] = to_dev(self.mesh.col_gid.astype(np.int32))
+                d["part"] = torch.empty(max(1, tp.npart) * tp.n_z * 5, dtype=torch.float64, device="cuda")
+                self._h["tiles"] = (tp, d)
+        return self._h["tiles"]
+
     def lap_plan(self, viscous):
         """hv_lap_plan for this (viscous metric, operator set) pair."""
         key = id(viscous)
@@ -72,7 +94,23 @@ class EulerOps:
             p.d_Minv = self.mass.d_Minv.data_ptr()
             p.d_work = work.data_ptr()
             p.d_y = y.data_ptr()
-            self._plans[key] = (p, viscous, W)
+            keep = [viscous, W]
+            ta = self._tile_arrays()
+            if ta is not None:
+                torch = torch_mod()
+                tp, d = ta
+                Wt = torch.empty(tp.ntiles * tp.nlay * 6 * n * tp.NE * n * n, dtype=torch.float64, device="cuda")
+                _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
+                                                          d["elem"].data_ptr(), W.data_ptr(), dev.nloc,
+                                                          Wt.data_ptr(), _lib.stream_handle()))
+                p.TX, p.TY, p.nlay, p.n_z = tp.TX, tp.TY, tp.nlay, tp.n_z
+                p.ntiles, p.nslot = tp.ntiles, tp.nslot
+                p.d_gt, p.d_code, p.d_tmeta = d["gt"].data_ptr(), d["code"].data_ptr(), d["tmeta"].data_ptr()
+                p.d_slot_col, p.d_slot_row0 = d["slot_col"].data_ptr(), d["slot_row0"].data_ptr()
+                p.d_slot_nc, p.d_col_gid = d["slot_nc"].data_ptr(), d["col_gid"].data_ptr()
+                p.d_Wt, p.d_part = Wt.data_ptr(), d["part"].data_ptr()
+                keep.append(Wt)
+            self._plans[key] = (p, keep)
         return self._plans[key][0]
 
     # ------------------------------------------------------------ operators
