@@ -42,19 +42,63 @@ struct TileCfg {
   static constexpr int NODES = U * V * n;
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
-  static constexpr int NCOL = (TX > 1 ? 2 : 1) * (TY > 1 ? 2 : 1);
-  static constexpr size_t SMEM = sizeof(double) * (SQ + 2 * SE);
+  static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
+  static constexpr int PQ = (SQ + NT - 1) / NT;          // gather items per thread
+  static constexpr int PM = (NODES + NT - 1) / NT;       // node items per thread
+  // shared memory carve-up (doubles): q | W | a | b | Minv[2] ; ints: gid[2] ; mbarrier
+  static constexpr int OFF_W = SQ;
+  static constexpr int OFF_A = OFF_W + WL;
+  static constexpr int OFF_B = OFF_A + SE;
+  static constexpr int OFF_M = OFF_B + SE;
+  static constexpr int OFF_G = OFF_M + 2 * NODES;         // in doubles; ints packed 2 per double
+  static constexpr int OFF_BAR = OFF_G + NODES;           // 2*NODES ints == NODES doubles
+  static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
 };
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// one elected thread: expect `bytes` on the barrier and start the bulk copy global -> shared
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+
 template <int n, int TX, int TY, int F>
-__global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
+__global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY, F>::NT <= 512 ? 2 : 1))
     lap_tile_kernel(hv::DTab<n> Dt, TileArgs A) {
   using C = TileCfg<n, TX, TY, F>;
-  constexpr int N = C::N, U = C::U, V = C::V, NE = C::NE, NN = C::NN;
-  extern __shared__ double sm[];
-  double* s_q = sm;            // [U][V][n][F] gathered q, later the tile accumulator
-  double* s_a = sm + C::SQ;    // [NE][n][n][n][F] xi scratch (dq0 -> f0 -> weak0)
-  double* s_b = s_a + C::SE;   // [NE][n][n][n][F] eta scratch (dq1 -> f1 -> weak1)
+  constexpr int N = C::N, V = C::V, NE = C::NE, NN = C::NN, U = C::U;
+  extern __shared__ __align__(16) double sm[];
+  double* s_q = sm;                 // [U][V][n][F] gathered q of the current layer
+  double* s_w = sm + C::OFF_W;      // [6][n][NE][NN] packed metric of the current layer (TMA)
+  double* s_a = sm + C::OFF_A;      // [NE][n][n][n][F] xi scratch / element accumulator
+  double* s_b = sm + C::OFF_B;      // [NE][n][n][n][F] eta scratch
+  double* s_mi = sm + C::OFF_M;     // [2][NODES] Minv of the tile nodes
+  int* s_g = reinterpret_cast<int*>(sm + C::OFF_G);   // [2][NODES] gids of the tile nodes
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   const int tid = threadIdx.x;
   const int f = tid % F;
   const int line = tid / F;
@@ -65,23 +109,57 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
   const int64_t t = blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
   const bool act = (px < tx) && (py < ty);
-  const int color = (TX > 1 ? (px & 1) * (TY > 1 ? 2 : 1) : 0) + (TY > 1 ? (py & 1) : 0);
+  const int nlay = A.nlay;
   const int32_t* code_t = A.code + t * (U * V);
-  // element-private scratch index of (e, a, b, c, f)
-  auto eidx = [&](int a, int b, int c) { return (((e * n + a) * n + b) * n + c) * F + f; };
-  // tile node index of (u, v, k, f)
+  const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::NODES;
+  const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
+  auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
   auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
+
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  // prologue: layer 0 gather (direct), its gids / Minv, W(0) by TMA; gids of layer 1 in registers
+  for (int s = 0; s < C::PM; ++s) {
+    const int node = tid + s * C::NT;
+    if (node < C::NODES) {
+      const int g = gt_t[node];
+      s_g[node] = g;
+      s_mi[node] = (g >= 0) ? A.Minv[g] : 0.0;
+    }
+  }
+  for (int s = 0; s < C::PQ; ++s) {
+    const int idx = tid + s * C::NT;
+    if (idx < C::SQ) {
+      const int g = gt_t[idx / F];
+      s_q[idx] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[idx % F]] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) tma_load_1d(s_w, Wt_t, C::WL * sizeof(double), bar);
+  int gq[C::PQ], gm[C::PM];   // gids of the next layer's gather items
+  for (int s = 0; s < C::PQ; ++s) {
+    const int idx = tid + s * C::NT;
+    gq[s] = (nlay > 1 && idx < C::SQ) ? gt_t[C::NODES + idx / F] : -1;
+  }
+  for (int s = 0; s < C::PM; ++s) {
+    const int node = tid + s * C::NT;
+    gm[s] = (nlay > 1 && node < C::NODES) ? gt_t[C::NODES + node] : -1;
+  }
   double carry = 0.0;
 
-  for (int l = 0; l < A.nlay; ++l) {
-    const int32_t* g_l = A.gt + ((t * A.nlay + l) * (int64_t)C::NODES);
-    // ---- G: gather
-    for (int idx = tid; idx < C::SQ; idx += C::NT) {
-      const int node = idx / F, ff = idx % F;
-      const int g = g_l[node];
-      s_q[idx] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[ff]] : 0.0;
+  for (int l = 0; l < nlay; ++l) {
+    const int cur = l & 1, nxt = cur ^ 1;
+    // ---- prefetch of layer l+1 into registers (overlaps this layer's compute)
+    double qn[C::PQ], mn[C::PM];
+#pragma unroll
+    for (int s = 0; s < C::PQ; ++s) {
+      const int idx = tid + s * C::NT;
+      qn[s] = (gq[s] >= 0) ? A.q[(int64_t)gq[s] * A.ldq + A.qf.f[idx % F]] : 0.0;
     }
-    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < C::PM; ++s) mn[s] = (gm[s] >= 0) ? A.Minv[gm[s]] : 0.0;
     // ---- S1: strong xi and eta derivatives (one line each per thread)
     if (act) {
       const int b = ij / n, c = ij % n;
@@ -93,7 +171,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
         double d = 0.0;
 #pragma unroll
         for (int a = 0; a < n; ++a) d = fma(Dt.D[a2][a], v[a], d);
-        s_a[eidx(a2, b, c)] = d;
+        s_a[eidx(e, a2, b, c)] = d;
       }
 #pragma unroll
       for (int a = 0; a < n; ++a) v[a] = s_q[tidx(px * N + b, py * N + a, c)];
@@ -102,11 +180,12 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
         double d = 0.0;
 #pragma unroll
         for (int a = 0; a < n; ++a) d = fma(Dt.D[a2][a], v[a], d);
-        s_b[eidx(b, a2, c)] = d;
+        s_b[eidx(e, b, a2, c)] = d;
       }
     }
     __syncthreads();
     // ---- P: zeta derivative, metric contraction, zeta weak derivative
+    mbar_wait(bar, (uint32_t)(l & 1));
     double acc[n];
 #pragma unroll
     for (int k = 0; k < n; ++k) acc[k] = 0.0;
@@ -114,17 +193,17 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
       double qk[n], f2[n];
 #pragma unroll
       for (int k = 0; k < n; ++k) qk[k] = s_q[tidx(px * N + i, py * N + j, k)];
-      const double* W = A.Wt + ((t * A.nlay + l) * 6) * (int64_t)(n * NE * NN) + e * NN + ij;
+      const double* W = s_w + e * NN + ij;
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         double d2 = 0.0;
 #pragma unroll
         for (int a = 0; a < n; ++a) d2 = fma(Dt.D[k][a], qk[a], d2);
-        const int id = eidx(i, j, k);
+        const int id = eidx(e, i, j, k);
         const double d0 = s_a[id], d1 = s_b[id];
-        const double w00 = __ldg(W + (0 * n + k) * NE * NN), w01 = __ldg(W + (1 * n + k) * NE * NN);
-        const double w02 = __ldg(W + (2 * n + k) * NE * NN), w11 = __ldg(W + (3 * n + k) * NE * NN);
-        const double w12 = __ldg(W + (4 * n + k) * NE * NN), w22 = __ldg(W + (5 * n + k) * NE * NN);
+        const double w00 = W[(0 * n + k) * NE * NN], w01 = W[(1 * n + k) * NE * NN];
+        const double w02 = W[(2 * n + k) * NE * NN], w11 = W[(3 * n + k) * NE * NN];
+        const double w12 = W[(4 * n + k) * NE * NN], w22 = W[(5 * n + k) * NE * NN];
         s_a[id] = w00 * d0 + w01 * d1 + w02 * d2;
         s_b[id] = w01 * d0 + w11 * d1 + w12 * d2;
         f2[k] = w02 * d0 + w12 * d1 + w22 * d2;
@@ -138,70 +217,108 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT)
       }
     }
     __syncthreads();
-    // ---- W1: weak xi / eta derivatives in place; clear the tile accumulator
-    for (int idx = tid; idx < C::SQ; idx += C::NT) s_q[idx] = 0.0;
+    // s_q and s_w of layer l are dead: start W(l+1), park the prefetched layer l+1
+    if (l + 1 < nlay) {
+      if (tid == 0) {
+        fence_proxy_async();
+        tma_load_1d(s_w, Wt_t + (int64_t)(l + 1) * C::WL, C::WL * sizeof(double), bar);
+      }
+#pragma unroll
+      for (int s = 0; s < C::PQ; ++s) {
+        const int idx = tid + s * C::NT;
+        if (idx < C::SQ) s_q[idx] = qn[s];
+      }
+#pragma unroll
+      for (int s = 0; s < C::PM; ++s) {
+        const int node = tid + s * C::NT;
+        if (node < C::NODES) {
+          s_g[nxt * C::NODES + node] = gm[s];
+          s_mi[nxt * C::NODES + node] = mn[s];
+        }
+      }
+      // gids of layer l+2
+#pragma unroll
+      for (int s = 0; s < C::PQ; ++s) {
+        const int idx = tid + s * C::NT;
+        gq[s] = (l + 2 < nlay && idx < C::SQ) ? gt_t[(int64_t)(l + 2) * C::NODES + idx / F] : -1;
+      }
+#pragma unroll
+      for (int s = 0; s < C::PM; ++s) {
+        const int node = tid + s * C::NT;
+        gm[s] = (l + 2 < nlay && node < C::NODES) ? gt_t[(int64_t)(l + 2) * C::NODES + node] : -1;
+      }
+    }
+    // ---- W1: weak xi / eta derivatives in place
     if (act) {
       const int b = ij / n, c = ij % n;
       double v[n];
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_a[eidx(a, b, c)];
+      for (int a = 0; a < n; ++a) v[a] = s_a[eidx(e, a, b, c)];
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         double s = 0.0;
 #pragma unroll
         for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a], s);
-        s_a[eidx(a2, b, c)] = s;
+        s_a[eidx(e, a2, b, c)] = s;
       }
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_b[eidx(b, a, c)];
+      for (int a = 0; a < n; ++a) v[a] = s_b[eidx(e, b, a, c)];
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         double s = 0.0;
 #pragma unroll
         for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a], s);
-        s_b[eidx(b, a2, c)] = s;
+        s_b[eidx(e, b, a2, c)] = s;
       }
     }
     __syncthreads();
-    // ---- A: element accumulator, vertical carry, 4-colour tile DSS
-    const int kmax = (l == A.nlay - 1) ? n : N;
+    // ---- A: element accumulator (+ vertical carry) into s_a
+    const int kmax = (l == nlay - 1) ? n : N;
     if (act) {
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        const int id = eidx(i, j, k);
+        const int id = eidx(e, i, j, k);
         acc[k] -= s_a[id] + s_b[id];
       }
       acc[0] += carry;
       carry = acc[N];
-    }
 #pragma unroll
-    for (int c = 0; c < C::NCOL; ++c) {
-      if (act && color == c) {
-#pragma unroll
-        for (int k = 0; k < n; ++k)
-          if (k < kmax) s_q[tidx(px * N + i, py * N + j, k)] += acc[k];
-      }
-      __syncthreads();
+      for (int k = 0; k < n; ++k) s_a[eidx(e, i, j, k)] = acc[k];
     }
-    // ---- O: final values for tile-owned nodes, partial rows for shared ones
-    const int nout = U * V * kmax * F;
-    for (int idx = tid; idx < nout; idx += C::NT) {
-      const int ff = idx % F;
-      const int r = idx / F;
-      const int uv = r / kmax, k = r % kmax;
-      const int node = uv * n + k;
-      const int g = g_l[node];
-      if (g < 0) continue;
-      const double val = s_q[node * F + ff];
-      const int cd = code_t[uv];
-      if (cd < 0) {
-        double* o = A.out + (int64_t)g * A.ldo;
-        o[A.of.f[ff]] = A.scale * (A.Minv[g] * val);
-        if (ff == 0 && A.zero_mask)
-          for (int zc = 0; zc < A.ldo; ++zc)
-            if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
-      } else {
-        A.part[((int64_t)cd * A.n_z + l * N + k) * 5 + ff] = val;
+    __syncthreads();
+    // ---- O: node owners sum the (1, 2 or 4) element copies in fixed order
+    {
+      const int* g_l = s_g + cur * C::NODES;
+      const double* mi_l = s_mi + cur * C::NODES;
+      const int nout = U * V * kmax * F;
+      for (int idx = tid; idx < nout; idx += C::NT) {
+        const int ff = idx % F;
+        const int r = idx / F;
+        const int uv = r / kmax, k = r % kmax;
+        const int u = uv / V, v = uv % V;
+        const int node = uv * n + k;
+        const int g = g_l[node];
+        if (g < 0) continue;
+        const int pu1 = min(u / N, TX - 1), pv1 = min(v / N, TY - 1);
+        const int pu0 = (u % N == 0 && u > 0) ? u / N - 1 : pu1;
+        const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
+        double val = 0.0;
+        for (int a = pu0; a <= pu1; ++a)
+          for (int b = pv0; b <= pv1; ++b) {
+            if (a >= tx || b >= ty) continue;
+            const int ee = a * TY + b;
+            val += s_a[(((ee * n + (u - a * N)) * n + (v - b * N)) * n + k) * F + ff];
+          }
+        const int cd = code_t[uv];
+        if (cd < 0) {
+          double* o = A.out + (int64_t)g * A.ldo;
+          o[A.of.f[ff]] = A.scale * (mi_l[node] * val);
+          if (ff == 0 && A.zero_mask)
+            for (int zc = 0; zc < A.ldo; ++zc)
+              if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+        } else {
+          A.part[((int64_t)cd * A.n_z + l * N + k) * 5 + ff] = val;
+        }
       }
     }
     __syncthreads();
