@@ -46,7 +46,7 @@ struct TileCfg {
   static constexpr int PQ = (SQ + NT - 1) / NT;          // gather items per thread
   static constexpr int PM = (NODES + NT - 1) / NT;       // node items per thread
   // shared memory carve-up (doubles): q | W | a | b | Minv[2] ; ints: gid[2] ; mbarrier
-  static constexpr int OFF_W = SQ;
+  static constexpr int OFF_W = (SQ + 1) & ~1;             // 16-byte aligned TMA destination
   static constexpr int OFF_A = OFF_W + WL;
   static constexpr int OFF_B = OFF_A + SE;
   static constexpr int OFF_M = OFF_B + SE;
