@@ -25,6 +25,8 @@
 // bitwise reproducible run to run.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "hv_common.h"
 #include "lap_common.cuh"
 #include "lap_tile.cuh"
@@ -33,26 +35,54 @@ namespace {
 
 using hv::TileArgs;
 
-template <int n, int TX, int TY, int F>
+// FP doubles held per thread (FP = 2: one LDS.128 / STS.128 per access)
+template <int FP>
+struct Vec {
+  double x[FP];
+  __device__ __forceinline__ static Vec ld(const double* p) {
+    Vec r;
+    if constexpr (FP == 2) {
+      const double2 d = *reinterpret_cast<const double2*>(p);
+      r.x[0] = d.x;
+      r.x[1] = d.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < FP; ++q) r.x[q] = p[q];
+    }
+    return r;
+  }
+  __device__ __forceinline__ void st(double* p) const {
+    if constexpr (FP == 2) {
+      *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < FP; ++q) p[q] = x[q];
+    }
+  }
+};
+
+template <int n, int TX, int TY, int F, int FP>
 struct TileCfg {
   static constexpr int N = n - 1;
   static constexpr int U = TX * N + 1, V = TY * N + 1;
   static constexpr int NE = TX * TY, NN = n * n;
-  static constexpr int NT = NE * NN * F;
+  static constexpr int FL = F / FP;                       // field lanes per line
+  static constexpr int NT = NE * NN * FL;                 // threads
   static constexpr int NODES = U * V * n;
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
-  static constexpr int PQ = (SQ + NT - 1) / NT;          // gather items per thread
+  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // gather items (node, lane) per thread
   static constexpr int PM = (NODES + NT - 1) / NT;       // node items per thread
-  // shared memory carve-up (doubles): q | W | a | b | Minv[2] ; ints: gid[2] ; mbarrier
+  // shared memory carve-up (doubles): q | W | a | b | Minv | gid(int) | mbarrier
   static constexpr int OFF_W = (SQ + 1) & ~1;             // 16-byte aligned TMA destination
   static constexpr int OFF_A = OFF_W + WL;
   static constexpr int OFF_B = OFF_A + SE;
   static constexpr int OFF_M = OFF_B + SE;
-  static constexpr int OFF_G = OFF_M + 2 * NODES;         // in doubles; ints packed 2 per double
-  static constexpr int OFF_BAR = OFF_G + NODES;           // 2*NODES ints == NODES doubles
+  static constexpr int OFF_G = OFF_M + NODES;
+  static constexpr int OFF_BAR = (OFF_G + (NODES + 1) / 2 + 1) & ~1;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
+  static constexpr int MINB = (NT <= 256 && SMEM <= 75 * 1024) ? 3 : (NT <= 512 ? 2 : 1);
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -86,22 +116,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-template <int n, int TX, int TY, int F>
-__global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY, F>::NT <= 512 ? 2 : 1))
+template <int n, int TX, int TY, int F, int FP, int MB>
+__global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     lap_tile_kernel(hv::DTab<n> Dt, TileArgs A) {
-  using C = TileCfg<n, TX, TY, F>;
-  constexpr int N = C::N, V = C::V, NE = C::NE, NN = C::NN, U = C::U;
+  using C = TileCfg<n, TX, TY, F, FP>;
+  using VT = Vec<FP>;
+  constexpr int N = C::N, V = C::V, NE = C::NE, NN = C::NN, U = C::U, FL = C::FL;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                 // [U][V][n][F] gathered q of the current layer
-  double* s_w = sm + C::OFF_W;      // [6][n][NE][NN] packed metric of the current layer (TMA)
+  double* s_w = sm + C::OFF_W;      // [3 pairs][n][NE][NN][2] packed metric (TMA)
   double* s_a = sm + C::OFF_A;      // [NE][n][n][n][F] xi scratch / element accumulator
   double* s_b = sm + C::OFF_B;      // [NE][n][n][n][F] eta scratch
-  double* s_mi = sm + C::OFF_M;     // [2][NODES] Minv of the tile nodes
-  int* s_g = reinterpret_cast<int*>(sm + C::OFF_G);   // [2][NODES] gids of the tile nodes
+  double* s_mi = sm + C::OFF_M;     // [NODES] Minv of the current layer's tile nodes
+  int* s_g = reinterpret_cast<int*>(sm + C::OFF_G);   // [NODES] their gids
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   const int tid = threadIdx.x;
-  const int f = tid % F;
-  const int line = tid / F;
+  const int fl = tid % FL;
+  const int f0 = fl * FP;
+  const int line = tid / FL;
   const int e = line / NN;
   const int ij = line % NN;
   const int i = ij / n, j = ij % n;
@@ -113,14 +145,18 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY,
   const int32_t* code_t = A.code + t * (U * V);
   const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::NODES;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
-  auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
-  auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
+  auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f0; };
+  auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f0; };
+  auto gather = [&](int g, int lane, double* dst) {
+#pragma unroll
+    for (int p = 0; p < FP; ++p) dst[p] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[lane * FP + p]] : 0.0;
+  };
 
   if (tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  // prologue: layer 0 gather (direct), its gids / Minv, W(0) by TMA; gids of layer 1 in registers
+  // prologue: layer 0 gather, gids / Minv, W(0) by TMA; gids of layer 1 in registers
   for (int s = 0; s < C::PM; ++s) {
     const int node = tid + s * C::NT;
     if (node < C::NODES) {
@@ -130,94 +166,116 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY,
     }
   }
   for (int s = 0; s < C::PQ; ++s) {
-    const int idx = tid + s * C::NT;
-    if (idx < C::SQ) {
-      const int g = gt_t[idx / F];
-      s_q[idx] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[idx % F]] : 0.0;
+    const int it = tid + s * C::NT;
+    if (it < C::NODES * FL) {
+      VT v;
+      gather(gt_t[it / FL], it % FL, v.x);
+      v.st(s_q + (it / FL) * F + (it % FL) * FP);
     }
   }
   __syncthreads();
   if (tid == 0) tma_load_1d(s_w, Wt_t, C::WL * sizeof(double), bar);
   int gq[C::PQ], gm[C::PM];   // gids of the next layer's gather items
+#pragma unroll
   for (int s = 0; s < C::PQ; ++s) {
-    const int idx = tid + s * C::NT;
-    gq[s] = (nlay > 1 && idx < C::SQ) ? gt_t[C::NODES + idx / F] : -1;
+    const int it = tid + s * C::NT;
+    gq[s] = (nlay > 1 && it < C::NODES * FL) ? gt_t[C::NODES + it / FL] : -1;
   }
+#pragma unroll
   for (int s = 0; s < C::PM; ++s) {
     const int node = tid + s * C::NT;
     gm[s] = (nlay > 1 && node < C::NODES) ? gt_t[C::NODES + node] : -1;
   }
-  double carry = 0.0;
+  double carry[FP];
+#pragma unroll
+  for (int p = 0; p < FP; ++p) carry[p] = 0.0;
 
   for (int l = 0; l < nlay; ++l) {
-    const int cur = l & 1, nxt = cur ^ 1;
     // ---- prefetch of layer l+1 into registers (overlaps this layer's compute)
-    double qn[C::PQ], mn[C::PM];
+    double qn[C::PQ][FP], mn[C::PM];
 #pragma unroll
-    for (int s = 0; s < C::PQ; ++s) {
-      const int idx = tid + s * C::NT;
-      qn[s] = (gq[s] >= 0) ? A.q[(int64_t)gq[s] * A.ldq + A.qf.f[idx % F]] : 0.0;
-    }
+    for (int s = 0; s < C::PQ; ++s) gather(gq[s], (tid + s * C::NT) % FL, qn[s]);
 #pragma unroll
     for (int s = 0; s < C::PM; ++s) mn[s] = (gm[s] >= 0) ? A.Minv[gm[s]] : 0.0;
     // ---- S1: strong xi and eta derivatives (one line each per thread)
     if (act) {
       const int b = ij / n, c = ij % n;
-      double v[n];
+      VT v[n];
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_q[tidx(px * N + a, py * N + b, c)];
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + a, py * N + b, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
-        double d = 0.0;
+        VT d;
 #pragma unroll
-        for (int a = 0; a < n; ++a) d = fma(Dt.D[a2][a], v[a], d);
-        s_a[eidx(e, a2, b, c)] = d;
+        for (int p = 0; p < FP; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], v[a].x[p], s);
+          d.x[p] = s;
+        }
+        d.st(s_a + eidx(e, a2, b, c));
       }
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_q[tidx(px * N + b, py * N + a, c)];
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + b, py * N + a, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
-        double d = 0.0;
+        VT d;
 #pragma unroll
-        for (int a = 0; a < n; ++a) d = fma(Dt.D[a2][a], v[a], d);
-        s_b[eidx(e, b, a2, c)] = d;
+        for (int p = 0; p < FP; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], v[a].x[p], s);
+          d.x[p] = s;
+        }
+        d.st(s_b + eidx(e, b, a2, c));
       }
     }
     __syncthreads();
     // ---- P: zeta derivative, metric contraction, zeta weak derivative
     mbar_wait(bar, (uint32_t)(l & 1));
-    double acc[n];
+    double acc[n][FP];
 #pragma unroll
-    for (int k = 0; k < n; ++k) acc[k] = 0.0;
+    for (int k = 0; k < n; ++k)
+#pragma unroll
+      for (int p = 0; p < FP; ++p) acc[k][p] = 0.0;
     if (act) {
-      double qk[n], f2[n];
+      VT qk[n];
+      double f2[n][FP];
 #pragma unroll
-      for (int k = 0; k < n; ++k) qk[k] = s_q[tidx(px * N + i, py * N + j, k)];
-      const double* W = s_w + e * NN + ij;
+      for (int k = 0; k < n; ++k) qk[k] = VT::ld(s_q + tidx(px * N + i, py * N + j, k));
+      const double* W = s_w + (e * NN + ij) * 2;
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        double d2 = 0.0;
-#pragma unroll
-        for (int a = 0; a < n; ++a) d2 = fma(Dt.D[k][a], qk[a], d2);
+        const double2 wa = *reinterpret_cast<const double2*>(W + (0 * n + k) * NE * NN * 2);   // w00 w01
+        const double2 wb = *reinterpret_cast<const double2*>(W + (1 * n + k) * NE * NN * 2);   // w02 w11
+        const double2 wc = *reinterpret_cast<const double2*>(W + (2 * n + k) * NE * NN * 2);   // w12 w22
         const int id = eidx(e, i, j, k);
-        const double d0 = s_a[id], d1 = s_b[id];
-        const double w00 = W[(0 * n + k) * NE * NN], w01 = W[(1 * n + k) * NE * NN];
-        const double w02 = W[(2 * n + k) * NE * NN], w11 = W[(3 * n + k) * NE * NN];
-        const double w12 = W[(4 * n + k) * NE * NN], w22 = W[(5 * n + k) * NE * NN];
-        s_a[id] = w00 * d0 + w01 * d1 + w02 * d2;
-        s_b[id] = w01 * d0 + w11 * d1 + w12 * d2;
-        f2[k] = w02 * d0 + w12 * d1 + w22 * d2;
+        const VT d0 = VT::ld(s_a + id), d1 = VT::ld(s_b + id);
+        VT o0, o1;
+#pragma unroll
+        for (int p = 0; p < FP; ++p) {
+          double d2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) d2 = fma(Dt.D[k][a], qk[a].x[p], d2);
+          o0.x[p] = wa.x * d0.x[p] + wa.y * d1.x[p] + wb.x * d2;
+          o1.x[p] = wa.y * d0.x[p] + wb.y * d1.x[p] + wc.x * d2;
+          f2[k][p] = wb.x * d0.x[p] + wc.x * d1.x[p] + wc.y * d2;
+        }
+        o0.st(s_a + id);
+        o1.st(s_b + id);
       }
 #pragma unroll
-      for (int k = 0; k < n; ++k) {
-        double s = 0.0;
+      for (int k = 0; k < n; ++k)
 #pragma unroll
-        for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], f2[a], s);
-        acc[k] = -s;
-      }
+        for (int p = 0; p < FP; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], f2[a][p], s);
+          acc[k][p] = -s;
+        }
     }
     __syncthreads();
-    // s_q and s_w of layer l are dead: start W(l+1), park the prefetched layer l+1
+    // s_q and s_w of layer l are dead: start W(l+1), park the prefetched q(l+1)
     if (l + 1 < nlay) {
       if (tid == 0) {
         fence_proxy_async();
@@ -225,50 +283,51 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY,
       }
 #pragma unroll
       for (int s = 0; s < C::PQ; ++s) {
-        const int idx = tid + s * C::NT;
-        if (idx < C::SQ) s_q[idx] = qn[s];
-      }
+        const int it = tid + s * C::NT;
+        if (it < C::NODES * FL) {
+          VT v;
 #pragma unroll
-      for (int s = 0; s < C::PM; ++s) {
-        const int node = tid + s * C::NT;
-        if (node < C::NODES) {
-          s_g[nxt * C::NODES + node] = gm[s];
-          s_mi[nxt * C::NODES + node] = mn[s];
+          for (int p = 0; p < FP; ++p) v.x[p] = qn[s][p];
+          v.st(s_q + (it / FL) * F + (it % FL) * FP);
         }
       }
-      // gids of layer l+2
 #pragma unroll
       for (int s = 0; s < C::PQ; ++s) {
-        const int idx = tid + s * C::NT;
-        gq[s] = (l + 2 < nlay && idx < C::SQ) ? gt_t[(int64_t)(l + 2) * C::NODES + idx / F] : -1;
-      }
-#pragma unroll
-      for (int s = 0; s < C::PM; ++s) {
-        const int node = tid + s * C::NT;
-        gm[s] = (l + 2 < nlay && node < C::NODES) ? gt_t[(int64_t)(l + 2) * C::NODES + node] : -1;
+        const int it = tid + s * C::NT;
+        gq[s] = (l + 2 < nlay && it < C::NODES * FL) ? gt_t[(int64_t)(l + 2) * C::NODES + it / FL] : -1;
       }
     }
     // ---- W1: weak xi / eta derivatives in place
     if (act) {
       const int b = ij / n, c = ij % n;
-      double v[n];
+      VT v[n];
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_a[eidx(e, a, b, c)];
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_a + eidx(e, a, b, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
-        double s = 0.0;
+        VT d;
 #pragma unroll
-        for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a], s);
-        s_a[eidx(e, a2, b, c)] = s;
+        for (int p = 0; p < FP; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a].x[p], s);
+          d.x[p] = s;
+        }
+        d.st(s_a + eidx(e, a2, b, c));
       }
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = s_b[eidx(e, b, a, c)];
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_b + eidx(e, b, a, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
-        double s = 0.0;
+        VT d;
 #pragma unroll
-        for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a], s);
-        s_b[eidx(e, b, a2, c)] = s;
+        for (int p = 0; p < FP; ++p) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a].x[p], s);
+          d.x[p] = s;
+        }
+        d.st(s_b + eidx(e, b, a2, c));
       }
     }
     __syncthreads();
@@ -278,50 +337,83 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F>::NT, (TileCfg<n, TX, TY,
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         const int id = eidx(e, i, j, k);
-        acc[k] -= s_a[id] + s_b[id];
-      }
-      acc[0] += carry;
-      carry = acc[N];
+        const VT a = VT::ld(s_a + id), b = VT::ld(s_b + id);
 #pragma unroll
-      for (int k = 0; k < n; ++k) s_a[eidx(e, i, j, k)] = acc[k];
+        for (int p = 0; p < FP; ++p) acc[k][p] -= a.x[p] + b.x[p];
+      }
+#pragma unroll
+      for (int p = 0; p < FP; ++p) {
+        acc[0][p] += carry[p];
+        carry[p] = acc[N][p];
+      }
+#pragma unroll
+      for (int k = 0; k < n; ++k) {
+        VT o;
+#pragma unroll
+        for (int p = 0; p < FP; ++p) o.x[p] = acc[k][p];
+        o.st(s_a + eidx(e, i, j, k));
+      }
     }
     __syncthreads();
     // ---- O: node owners sum the (1, 2 or 4) element copies in fixed order
     {
-      const int* g_l = s_g + cur * C::NODES;
-      const double* mi_l = s_mi + cur * C::NODES;
-      const int nout = U * V * kmax * F;
-      for (int idx = tid; idx < nout; idx += C::NT) {
-        const int ff = idx % F;
-        const int r = idx / F;
+      const int nout = U * V * kmax * FL;
+      for (int it = tid; it < nout; it += C::NT) {
+        const int lane = it % FL;
+        const int r = it / FL;
         const int uv = r / kmax, k = r % kmax;
         const int u = uv / V, v = uv % V;
         const int node = uv * n + k;
-        const int g = g_l[node];
+        const int g = s_g[node];
         if (g < 0) continue;
         const int pu1 = min(u / N, TX - 1), pv1 = min(v / N, TY - 1);
         const int pu0 = (u % N == 0 && u > 0) ? u / N - 1 : pu1;
         const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
-        double val = 0.0;
+        double val[FP];
+#pragma unroll
+        for (int p = 0; p < FP; ++p) val[p] = 0.0;
         for (int a = pu0; a <= pu1; ++a)
           for (int b = pv0; b <= pv1; ++b) {
             if (a >= tx || b >= ty) continue;
             const int ee = a * TY + b;
-            val += s_a[(((ee * n + (u - a * N)) * n + (v - b * N)) * n + k) * F + ff];
+            const VT c = VT::ld(s_a + (((ee * n + (u - a * N)) * n + (v - b * N)) * n + k) * F + lane * FP);
+#pragma unroll
+            for (int p = 0; p < FP; ++p) val[p] += c.x[p];
           }
         const int cd = code_t[uv];
         if (cd < 0) {
           double* o = A.out + (int64_t)g * A.ldo;
-          o[A.of.f[ff]] = A.scale * (mi_l[node] * val);
-          if (ff == 0 && A.zero_mask)
+          const double m = A.scale * s_mi[node];
+#pragma unroll
+          for (int p = 0; p < FP; ++p) o[A.of.f[lane * FP + p]] = m * val[p];
+          if (lane == 0 && A.zero_mask)
             for (int zc = 0; zc < A.ldo; ++zc)
               if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
         } else {
-          A.part[((int64_t)cd * A.n_z + l * N + k) * 5 + ff] = val;
+          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5 + lane * FP;
+#pragma unroll
+          for (int p = 0; p < FP; ++p) o[p] = val[p];
         }
       }
     }
     __syncthreads();
+    // park gid / Minv of layer l+1, fetch the gids of layer l+2
+    if (l + 1 < nlay) {
+#pragma unroll
+      for (int s = 0; s < C::PM; ++s) {
+        const int node = tid + s * C::NT;
+        if (node < C::NODES) {
+          s_g[node] = gm[s];
+          s_mi[node] = mn[s];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < C::PM; ++s) {
+        const int node = tid + s * C::NT;
+        gm[s] = (l + 2 < nlay && node < C::NODES) ? gt_t[(int64_t)(l + 2) * C::NODES + node] : -1;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -352,7 +444,8 @@ __global__ void lap_tile_fixup(TileArgs A, int64_t nslot) {
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
 }
 
-// Tiled packed metric: Wt[t][l][c][k][e][ij] = W[c][elem(t,l,e)*n^3 + ij*n + k].
+// Tiled packed metric, component pairs (w00,w01) (w02,w11) (w12,w22):
+// Wt[t][l][cp][k][e][ij][2] = W[2cp + h][elem(t,l,e)*n^3 + ij*n + k].
 __global__ void tile_pack_metric(int n, int NE, int64_t ntiles, int nlay, const int32_t* __restrict__ elem,
                                  const double* __restrict__ W, int64_t nloc, double* __restrict__ Wt) {
   const int NN = n * n;
@@ -361,10 +454,11 @@ __global__ void tile_pack_metric(int n, int NE, int64_t ntiles, int nlay, const 
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tl = id / per;
     int64_t r = id % per;
+    const int h = (int)(r % 2); r /= 2;
     const int ij = (int)(r % NN); r /= NN;
     const int e = (int)(r % NE); r /= NE;
     const int k = (int)(r % n); r /= n;
-    const int c = (int)r;
+    const int c = (int)r * 2 + h;
     const int eg = elem[tl * NE + e];
     Wt[id] = (eg >= 0) ? W[c * nloc + (int64_t)eg * n * NN + ij * n + k] : 0.0;
   }
@@ -372,15 +466,17 @@ __global__ void tile_pack_metric(int n, int NE, int64_t ntiles, int nlay, const 
 
 template <int n, int TX, int TY, int F>
 int run_tile(const TileArgs& A, const double* Drow, cudaStream_t st) {
-  using C = TileCfg<n, TX, TY, F>;
+  constexpr int FP = (F % 2 == 0) ? 2 : 1;
+  using C = TileCfg<n, TX, TY, F, FP>;
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
-  auto kern = lap_tile_kernel<n, TX, TY, F>;
-  static bool attr = false;
-  if (!attr) {
-    HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  static const int mb_env = [] {
+    const char* s = getenv("HV_TILE_MINB");
+    return s ? atoi(s) : 0;
+  }();
+  auto kern = (C::MINB >= 3 && mb_env != 2) ? lap_tile_kernel<n, TX, TY, F, FP, (C::MINB >= 3 ? 3 : 1)>
+                                             : lap_tile_kernel<n, TX, TY, F, FP, (C::MINB >= 2 ? 2 : 1)>;
+  HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   if (A.nslot > 0) {
