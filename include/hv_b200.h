@@ -117,7 +117,8 @@ typedef struct hv_lap_plan {
    * element-parallel path */
   int TX, TY, nlay, n_z;
   int64_t ntiles, nslot;
-  const int32_t* d_gt;         /* (ntiles, nlay, TX*N+1, TY*N+1, N+1) tile node gids */
+  const int32_t* d_gt;         /* (ntiles, nlay, GTS) tile node gids, (TX*N+1, TY*N+1, N+1)
+                                  per layer padded to GTS = multiple of 4, -1 = absent */
   const int32_t* d_code;       /* (ntiles, TX*N+1, TY*N+1) -1 or partial row         */
   const int32_t* d_tmeta;      /* (ntiles, 2) active tile extent                     */
   const int32_t* d_slot_col;   /* (nslot) shared column ids                           */
@@ -125,12 +126,17 @@ typedef struct hv_lap_plan {
   const int32_t* d_slot_nc;    /* (nslot) owning tiles per shared column              */
   const int32_t* d_col_gid;    /* (ncol, n_z) int32 column gids                       */
   const double* d_Wt;          /* tiled packed metric                                 */
+  const double* d_Mt;          /* Minv in tile order (ntiles, nlay, MTS)              */
   double* d_part;              /* partial rows (rows, n_z, 5)                         */
 } hv_lap_plan;
 
 /* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
  * Wt[t][l][c][k][e][i*n+j] using d_elem (ntiles, nlay, TX*TY),
  * -1 for the absent elements of ragged tiles. */
+/* Minv in tile order: d_Mt[r*mts + c] = d_Minv[d_gt[r*gts + c]] for the rows r = (tile, layer)
+ * (0 for absent nodes and padding). */
+int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* d_gt, const double* d_Minv, double* d_Mt,
+                      void* stream);
 int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem, const double* d_W,
                         int64_t nloc, double* d_Wt, void* stream);
 

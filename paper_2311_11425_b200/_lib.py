@@ -56,6 +56,7 @@ class LapPlan(C.Structure):
         ("d_slot_nc", _P),
         ("d_col_gid", _P),
         ("d_Wt", _P),
+        ("d_Mt", _P),
         ("d_part", _P),
     ]
 
@@ -74,6 +75,7 @@ _SIGS = {
     "hv_mass_and_projection": (C.c_int, [C.c_int, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
     "hv_viscous_metric": (C.c_int, [C.c_int, C.c_int, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
+    "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, _P, _P]),
     "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, _P]),
     # test hook (host build of the metric arithmetic); never used by the product path

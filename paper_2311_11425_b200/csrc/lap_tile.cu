@@ -69,18 +69,19 @@ struct TileCfg {
   static constexpr int FL = F / FP;                       // field lanes per line
   static constexpr int NT = NE * NN * FL;                 // threads
   static constexpr int NODES = U * V * n;
+  static constexpr int GTS = (NODES + 3) & ~3;            // padded gid-table stride (ints, 16 B multiple)
+  static constexpr int MTS = (NODES + 1) & ~1;            // padded Minv-table stride (doubles)
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
   static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // gather items (node, lane) per thread
-  static constexpr int PM = (NODES + NT - 1) / NT;       // node items per thread
-  // shared memory carve-up (doubles): q | W | a | b | Minv | gid(int) | mbarrier
-  static constexpr int OFF_W = (SQ + 1) & ~1;             // 16-byte aligned TMA destination
-  static constexpr int OFF_A = OFF_W + WL;
+  // shared memory (doubles): q | W[2] | a | b | Minv[2] | gid[3] (ints) | mbarrier[2]
+  static constexpr int OFF_W = (SQ + 1) & ~1;
+  static constexpr int OFF_A = OFF_W + 2 * WL;
   static constexpr int OFF_B = OFF_A + SE;
   static constexpr int OFF_M = OFF_B + SE;
-  static constexpr int OFF_G = OFF_M + NODES;
-  static constexpr int OFF_BAR = (OFF_G + (NODES + 1) / 2 + 1) & ~1;
+  static constexpr int OFF_G = OFF_M + 2 * MTS;
+  static constexpr int OFF_BAR = OFF_G + 3 * GTS / 2;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
   static constexpr int MINB = (NT <= 256 && SMEM <= 75 * 1024) ? 3 : (NT <= 512 ? 2 : 1);
 };
@@ -105,6 +106,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
@@ -124,11 +131,11 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   constexpr int N = C::N, V = C::V, NE = C::NE, NN = C::NN, U = C::U, FL = C::FL;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                 // [U][V][n][F] gathered q of the current layer
-  double* s_w = sm + C::OFF_W;      // [3 pairs][n][NE][NN][2] packed metric (TMA)
+  double* s_w0 = sm + C::OFF_W;     // [2][3 pairs][n][NE][NN][2] packed metric ring (TMA)
   double* s_a = sm + C::OFF_A;      // [NE][n][n][n][F] xi scratch / element accumulator
   double* s_b = sm + C::OFF_B;      // [NE][n][n][n][F] eta scratch
-  double* s_mi = sm + C::OFF_M;     // [NODES] Minv of the current layer's tile nodes
-  int* s_g = reinterpret_cast<int*>(sm + C::OFF_G);   // [NODES] their gids
+  double* s_m0 = sm + C::OFF_M;     // [2][MTS] Minv of the tile nodes (TMA)
+  int* s_g0 = reinterpret_cast<int*>(sm + C::OFF_G);   // [3][GTS] gids of the tile nodes (TMA)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   const int tid = threadIdx.x;
   const int fl = tid % FL;
@@ -143,66 +150,72 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   const bool act = (px < tx) && (py < ty);
   const int nlay = A.nlay;
   const int32_t* code_t = A.code + t * (U * V);
-  const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::NODES;
+  const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::GTS;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
+  const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
   auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f0; };
   auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f0; };
   auto gather = [&](int g, int lane, double* dst) {
 #pragma unroll
     for (int p = 0; p < FP; ++p) dst[p] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[lane * FP + p]] : 0.0;
   };
+  // stage l: W(l) -> W[l%2], Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3], all on bar[l%2]
+  auto issue_stage = [&](int l) {
+    const int b = l & 1;
+    const bool nextg = (l + 1 < nlay);
+    const uint32_t bytes = C::WL * 8 + C::MTS * 8 + (nextg ? C::GTS * 4 : 0);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + b)), "r"(bytes)
+                 : "memory");
+    tma_copy(s_w0 + b * C::WL, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + b);
+    tma_copy(s_m0 + b * C::MTS, Mt_t + (int64_t)l * C::MTS, C::MTS * 8, bar + b);
+    if (nextg) tma_copy(s_g0 + ((l + 1) % 3) * C::GTS, gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4, bar + b);
+  };
 
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
-  // prologue: layer 0 gather, gids / Minv, W(0) by TMA; gids of layer 1 in registers
-  for (int s = 0; s < C::PM; ++s) {
-    const int node = tid + s * C::NT;
-    if (node < C::NODES) {
-      const int g = gt_t[node];
-      s_g[node] = g;
-      s_mi[node] = (g >= 0) ? A.Minv[g] : 0.0;
-    }
-  }
-  for (int s = 0; s < C::PQ; ++s) {
-    const int it = tid + s * C::NT;
-    if (it < C::NODES * FL) {
-      VT v;
-      gather(gt_t[it / FL], it % FL, v.x);
-      v.st(s_q + (it / FL) * F + (it % FL) * FP);
-    }
-  }
+  // prologue: gids and gather of layer 0 directly; stage 0 by TMA
+  for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
   __syncthreads();
-  if (tid == 0) tma_load_1d(s_w, Wt_t, C::WL * sizeof(double), bar);
-  int gq[C::PQ], gm[C::PM];   // gids of the next layer's gather items
-#pragma unroll
-  for (int s = 0; s < C::PQ; ++s) {
-    const int it = tid + s * C::NT;
-    gq[s] = (nlay > 1 && it < C::NODES * FL) ? gt_t[C::NODES + it / FL] : -1;
-  }
-#pragma unroll
-  for (int s = 0; s < C::PM; ++s) {
-    const int node = tid + s * C::NT;
-    gm[s] = (nlay > 1 && node < C::NODES) ? gt_t[C::NODES + node] : -1;
+  if (tid == 0) issue_stage(0);
+  for (int it = tid; it < C::NODES * FL; it += C::NT) {
+    VT v;
+    gather(s_g0[it / FL], it % FL, v.x);
+    v.st(s_q + (it / FL) * F + (it % FL) * FP);
   }
   double carry[FP];
 #pragma unroll
   for (int p = 0; p < FP; ++p) carry[p] = 0.0;
+  __syncthreads();
 
   for (int l = 0; l < nlay; ++l) {
-    // ---- prefetch of layer l+1 into registers (overlaps this layer's compute)
-    double qn[C::PQ][FP], mn[C::PM];
+    const int b = l & 1;
+    mbar_wait(bar + b, (uint32_t)((l >> 1) & 1));     // W(l), Minv(l), gids(l+1) have landed
+    if (tid == 0 && l + 1 < nlay) {
+      fence_proxy_async();
+      issue_stage(l + 1);                               // one full step ahead
+    }
+    const double* s_w = s_w0 + b * C::WL;
+    const double* s_mi = s_m0 + b * C::MTS;
+    const int* s_g = s_g0 + (l % 3) * C::GTS;
+    const int* s_gn = s_g0 + ((l + 1) % 3) * C::GTS;
+    // ---- prefetch q(l+1) into registers (addresses from shared memory)
+    double qn[C::PQ][FP];
+    if (l + 1 < nlay) {
 #pragma unroll
-    for (int s = 0; s < C::PQ; ++s) gather(gq[s], (tid + s * C::NT) % FL, qn[s]);
-#pragma unroll
-    for (int s = 0; s < C::PM; ++s) mn[s] = (gm[s] >= 0) ? A.Minv[gm[s]] : 0.0;
+      for (int s = 0; s < C::PQ; ++s) {
+        const int it = tid + s * C::NT;
+        if (it < C::NODES * FL) gather(s_gn[it / FL], it % FL, qn[s]);
+      }
+    }
     // ---- S1: strong xi and eta derivatives (one line each per thread)
     if (act) {
-      const int b = ij / n, c = ij % n;
+      const int b2 = ij / n, c = ij % n;
       VT v[n];
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + a, py * N + b, c));
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + a, py * N + b2, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         VT d;
@@ -213,10 +226,10 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], v[a].x[p], s);
           d.x[p] = s;
         }
-        d.st(s_a + eidx(e, a2, b, c));
+        d.st(s_a + eidx(e, a2, b2, c));
       }
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + b, py * N + a, c));
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_q + tidx(px * N + b2, py * N + a, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         VT d;
@@ -227,12 +240,11 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], v[a].x[p], s);
           d.x[p] = s;
         }
-        d.st(s_b + eidx(e, b, a2, c));
+        d.st(s_b + eidx(e, b2, a2, c));
       }
     }
     __syncthreads();
     // ---- P: zeta derivative, metric contraction, zeta weak derivative
-    mbar_wait(bar, (uint32_t)(l & 1));
     double acc[n][FP];
 #pragma unroll
     for (int k = 0; k < n; ++k)
@@ -275,12 +287,8 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
         }
     }
     __syncthreads();
-    // s_q and s_w of layer l are dead: start W(l+1), park the prefetched q(l+1)
+    // s_q of layer l is dead: park the prefetched q(l+1)
     if (l + 1 < nlay) {
-      if (tid == 0) {
-        fence_proxy_async();
-        tma_load_1d(s_w, Wt_t + (int64_t)(l + 1) * C::WL, C::WL * sizeof(double), bar);
-      }
 #pragma unroll
       for (int s = 0; s < C::PQ; ++s) {
         const int it = tid + s * C::NT;
@@ -291,18 +299,13 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           v.st(s_q + (it / FL) * F + (it % FL) * FP);
         }
       }
-#pragma unroll
-      for (int s = 0; s < C::PQ; ++s) {
-        const int it = tid + s * C::NT;
-        gq[s] = (l + 2 < nlay && it < C::NODES * FL) ? gt_t[(int64_t)(l + 2) * C::NODES + it / FL] : -1;
-      }
     }
     // ---- W1: weak xi / eta derivatives in place
     if (act) {
-      const int b = ij / n, c = ij % n;
+      const int b2 = ij / n, c = ij % n;
       VT v[n];
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_a + eidx(e, a, b, c));
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_a + eidx(e, a, b2, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         VT d;
@@ -313,10 +316,10 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a].x[p], s);
           d.x[p] = s;
         }
-        d.st(s_a + eidx(e, a2, b, c));
+        d.st(s_a + eidx(e, a2, b2, c));
       }
 #pragma unroll
-      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_b + eidx(e, b, a, c));
+      for (int a = 0; a < n; ++a) v[a] = VT::ld(s_b + eidx(e, b2, a, c));
 #pragma unroll
       for (int a2 = 0; a2 < n; ++a2) {
         VT d;
@@ -327,7 +330,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], v[a].x[p], s);
           d.x[p] = s;
         }
-        d.st(s_b + eidx(e, b, a2, c));
+        d.st(s_b + eidx(e, b2, a2, c));
       }
     }
     __syncthreads();
@@ -337,9 +340,9 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         const int id = eidx(e, i, j, k);
-        const VT a = VT::ld(s_a + id), b = VT::ld(s_b + id);
+        const VT a = VT::ld(s_a + id), bb = VT::ld(s_b + id);
 #pragma unroll
-        for (int p = 0; p < FP; ++p) acc[k][p] -= a.x[p] + b.x[p];
+        for (int p = 0; p < FP; ++p) acc[k][p] -= a.x[p] + bb.x[p];
       }
 #pragma unroll
       for (int p = 0; p < FP; ++p) {
@@ -373,10 +376,10 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
 #pragma unroll
         for (int p = 0; p < FP; ++p) val[p] = 0.0;
         for (int a = pu0; a <= pu1; ++a)
-          for (int b = pv0; b <= pv1; ++b) {
-            if (a >= tx || b >= ty) continue;
-            const int ee = a * TY + b;
-            const VT c = VT::ld(s_a + (((ee * n + (u - a * N)) * n + (v - b * N)) * n + k) * F + lane * FP);
+          for (int bq = pv0; bq <= pv1; ++bq) {
+            if (a >= tx || bq >= ty) continue;
+            const int ee = a * TY + bq;
+            const VT c = VT::ld(s_a + (((ee * n + (u - a * N)) * n + (v - bq * N)) * n + k) * F + lane * FP);
 #pragma unroll
             for (int p = 0; p < FP; ++p) val[p] += c.x[p];
           }
@@ -397,23 +400,6 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
       }
     }
     __syncthreads();
-    // park gid / Minv of layer l+1, fetch the gids of layer l+2
-    if (l + 1 < nlay) {
-#pragma unroll
-      for (int s = 0; s < C::PM; ++s) {
-        const int node = tid + s * C::NT;
-        if (node < C::NODES) {
-          s_g[node] = gm[s];
-          s_mi[node] = mn[s];
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < C::PM; ++s) {
-        const int node = tid + s * C::NT;
-        gm[s] = (l + 2 < nlay && node < C::NODES) ? gt_t[(int64_t)(l + 2) * C::NODES + node] : -1;
-      }
-      __syncthreads();
-    }
   }
 }
 
@@ -461,6 +447,18 @@ __global__ void tile_pack_metric(int n, int NE, int64_t ntiles, int nlay, const 
     const int c = (int)r * 2 + h;
     const int eg = elem[tl * NE + e];
     Wt[id] = (eg >= 0) ? W[c * nloc + (int64_t)eg * n * NN + ij * n + k] : 0.0;
+  }
+}
+
+// Minv in tile order: Mt[t][l][node] = Minv[gt[t][l][node]] (0 for absent nodes / padding).
+__global__ void tile_pack_minv_kernel(int64_t rows, int gts, int mts, const int32_t* __restrict__ gt,
+                                      const double* __restrict__ Minv, double* __restrict__ Mt) {
+  const int64_t total = rows * mts;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = id / mts;
+    const int c = (int)(id % mts);
+    const int g = (c < gts) ? gt[r * gts + c] : -1;
+    Mt[id] = (g >= 0) ? Minv[g] : 0.0;
   }
 }
 
@@ -518,6 +516,12 @@ int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStre
 int tile_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
               double* Wt, cudaStream_t st) {
   tile_pack_metric<<<148 * 8, 256, 0, st>>>(N + 1, NE, ntiles, nlay, elem, W, nloc, Wt);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+int tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* gt, const double* Minv, double* Mt, cudaStream_t st) {
+  tile_pack_minv_kernel<<<148 * 8, 256, 0, st>>>(rows, gts, mts, gt, Minv, Mt);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

@@ -9,14 +9,15 @@ namespace hv {
 struct TileArgs {
   int TX, TY, nlay, n_z;
   int64_t ntiles, nslot;
-  const int32_t* gt;        // (ntiles, nlay, U, V, n) tile node gids, -1 = absent
+  const int32_t* gt;        // (ntiles, nlay, GTS) tile node gids (U*V*n used, padded to 4), -1 = absent
   const int32_t* code;      // (ntiles, U, V) -1 = tile-owned column node, else partial row
   const int32_t* tmeta;     // (ntiles, 2) active tx, ty of ragged tiles
   const int32_t* slot_col;  // (nslot) column id of each shared column node
   const int32_t* slot_row0; // (nslot) first partial row
   const int32_t* slot_nc;   // (nslot) number of owning tiles
   const int32_t* col_gid;   // (ncol, n_z) int32
-  const double* Wt;         // tiled packed metric (ntiles, nlay, 6, n, NE, n*n)
+  const double* Wt;         // tiled packed metric (ntiles, nlay, 3 pairs, n, NE, n*n, 2)
+  const double* Mt;         // Minv in tile order (ntiles, nlay, MTS)
   const double* Minv;
   const double* q;
   int64_t ldq, ldo;
@@ -29,6 +30,7 @@ struct TileArgs {
 
 bool tile_supported(int N, int TX, int TY, int F);
 int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
+int tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* gt, const double* Minv, double* Mt, cudaStream_t st);
 int tile_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
               double* Wt, cudaStream_t st);
 

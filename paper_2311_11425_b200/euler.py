@@ -108,8 +108,12 @@ class EulerOps:
                 p.d_gt, p.d_code, p.d_tmeta = d["gt"].data_ptr(), d["code"].data_ptr(), d["tmeta"].data_ptr()
                 p.d_slot_col, p.d_slot_row0 = d["slot_col"].data_ptr(), d["slot_row0"].data_ptr()
                 p.d_slot_nc, p.d_col_gid = d["slot_nc"].data_ptr(), d["col_gid"].data_ptr()
-                p.d_Wt, p.d_part = Wt.data_ptr(), d["part"].data_ptr()
-                keep.append(Wt)
+                Mt = torch.empty(tp.ntiles * tp.nlay * tp.mts, dtype=torch.float64, device="cuda")
+                _lib.check(_lib.lib().hv_tile_pack_minv(tp.ntiles * tp.nlay, tp.gts, tp.mts, d["gt"].data_ptr(),
+                                                        self.mass.d_Minv.data_ptr(), Mt.data_ptr(),
+                                                        _lib.stream_handle()))
+                p.d_Wt, p.d_Mt, p.d_part = Wt.data_ptr(), Mt.data_ptr(), d["part"].data_ptr()
+                keep += [Wt, Mt]
             self._plans[key] = (p, keep)
         return self._plans[key][0]
 

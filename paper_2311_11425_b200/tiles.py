@@ -119,8 +119,13 @@ def build_tile_plan(mesh, TX, TY):
         rows = np.where(sl >= 0, slot_row0[np.maximum(sl, 0)] + rank[idx], -1)
         code[mq] = rows
     npart = int(slot_nc.sum()) if nslot else 0
+    nodes = U * V * n
+    gts = (nodes + 3) & ~3
+    mts = (nodes + 1) & ~1
+    gtp = np.full((nt, nlay, gts), -1, dtype=np.int32)
+    gtp[:, :, :nodes] = gt.reshape(nt, nlay, nodes)
     return TilePlan(N=N, n=n, TX=TX, TY=TY, U=U, V=V, NE=NE, nlay=nlay, ntiles=nt, tiles=tiles, elem=elem,
-                    gt=gt.astype(np.int32), code=code.astype(np.int32), nslot=nslot,
+                    gt=gtp, gts=gts, mts=mts, nodes=nodes, code=code.astype(np.int32), nslot=nslot,
                     slot_col=shared_cols.astype(np.int32), slot_row0=slot_row0.astype(np.int32),
                     slot_nc=slot_nc.astype(np.int32), npart=npart, n_z=mesh.n_z,
                     tmeta=tiles[:, 3:5].astype(np.int32))

@@ -1,0 +1,19 @@
+"""Summarise an ncu report: key throughput / stall metrics per kernel (dev helper)."""
+import csv, subprocess, sys
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(out.splitlines()))
+h = r[0]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
+        "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem", "sm__warps_active.avg.per_cycle_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_bytes.sum", "sm__cycles_elapsed.avg"]
+stalls = [c for c in h if c.startswith("smsp__average_warp_latency_issue_stalled") or (c.startswith("smsp__warp_issue_stalled") and c.endswith("per_warp_active.pct"))]
+for w in want + stalls:
+    if w in h:
+        i = h.index(w)
+        vals = [x[i] for x in r[2:]]
+        print(f"{w:75s} {vals}")
