@@ -51,6 +51,10 @@ struct Vec {
     }
     return r;
   }
+  __device__ __forceinline__ void st_any(double* p) const {
+#pragma unroll
+    for (int q = 0; q < FP; ++q) p[q] = x[q];
+  }
   __device__ __forceinline__ void st(double* p) const {
     if constexpr (FP == 2) {
       *reinterpret_cast<double2*>(p) = make_double2(x[0], x[1]);
@@ -74,16 +78,21 @@ struct TileCfg {
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
-  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // gather items (node, lane) per thread
-  // shared memory (doubles): q | W[2] | a | b | Minv[2] | gid[3] (ints) | mbarrier[2]
+  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // gather / output items (node, lane) per thread
+  static constexpr int UV = U * V;
+  // shared memory (doubles): q | W[WB] | a | b | Minv[2] | gid[3] (ints) | ctab (ints) | mbarrier[2]
   static constexpr int OFF_W = (SQ + 1) & ~1;
-  static constexpr int OFF_A = OFF_W + 2 * WL;
+  static constexpr size_t SMEM2 = sizeof(double) * (OFF_W + 2 * WL + 2 * SE + 2 * MTS + 3 * GTS / 2 + 2 * UV + 4);
+  static constexpr int WB = (SMEM2 <= 220 * 1024) ? 2 : 1;   // metric ring depth
+  static constexpr int OFF_A = OFF_W + WB * WL;
   static constexpr int OFF_B = OFF_A + SE;
   static constexpr int OFF_M = OFF_B + SE;
   static constexpr int OFF_G = OFF_M + 2 * MTS;
-  static constexpr int OFF_BAR = OFF_G + 3 * GTS / 2;
+  static constexpr int OFF_T = OFF_G + 3 * GTS / 2;        // ctab: 4 ints per tile column node
+  static constexpr int OFF_BAR = OFF_T + 2 * UV;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
-  static constexpr int MINB = (NT <= 256 && SMEM <= 75 * 1024) ? 3 : (NT <= 512 ? 2 : 1);
+  static constexpr int BY_SMEM = (int)((227 * 1024) / (SMEM + 1024));
+  static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);   // CTAs per SM we aim for
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -155,10 +164,18 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
   auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f0; };
   auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f0; };
-  auto gather = [&](int g, int lane, double* dst) {
+  // this thread's fields are fixed (NT is a multiple of FL): column indices in q and out
+  int qcol[FP], ocol[FP];
 #pragma unroll
-    for (int p = 0; p < FP; ++p) dst[p] = (g >= 0) ? A.q[(int64_t)g * A.ldq + A.qf.f[lane * FP + p]] : 0.0;
+  for (int p = 0; p < FP; ++p) {
+    qcol[p] = A.qf.f[f0 + p];
+    ocol[p] = A.of.f[f0 + p];
+  }
+  auto gather = [&](int g, double* dst) {
+#pragma unroll
+    for (int p = 0; p < FP; ++p) dst[p] = (g >= 0) ? A.q[(int64_t)g * A.ldq + qcol[p]] : 0.0;
   };
+  int* s_ct = reinterpret_cast<int*>(sm + C::OFF_T);  // [UV][4] scratch offsets of the element copies
   // stage l: W(l) -> W[l%2], Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3], all on bar[l%2]
   auto issue_stage = [&](int l) {
     const int b = l & 1;
@@ -166,7 +183,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     const uint32_t bytes = C::WL * 8 + C::MTS * 8 + (nextg ? C::GTS * 4 : 0);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + b)), "r"(bytes)
                  : "memory");
-    tma_copy(s_w0 + b * C::WL, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + b);
+    tma_copy(s_w0 + (C::WB == 2 ? b : 0) * C::WL, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + b);
     tma_copy(s_m0 + b * C::MTS, Mt_t + (int64_t)l * C::MTS, C::MTS * 8, bar + b);
     if (nextg) tma_copy(s_g0 + ((l + 1) % 3) * C::GTS, gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4, bar + b);
   };
@@ -176,14 +193,26 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
+  // ctab: for tile column node (u, v) the scratch offsets (k = 0, field 0) of its 1, 2 or 4
+  // element copies, -1 padded (absent elements of ragged tiles hold zeros, see phase A)
+  for (int uv = tid; uv < C::UV; uv += C::NT) {
+    const int u = uv / V, v = uv % V;
+    const int pu1 = min(u / N, TX - 1), pv1 = min(v / N, TY - 1);
+    const int pu0 = (u % N == 0 && u > 0) ? u / N - 1 : pu1;
+    const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
+    int c = 0;
+    for (int a = pu0; a <= pu1; ++a)
+      for (int b = pv0; b <= pv1; ++b) s_ct[uv * 4 + c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n * F;
+    for (; c < 4; ++c) s_ct[uv * 4 + c] = -1;
+  }
   // prologue: gids and gather of layer 0 directly; stage 0 by TMA
   for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
   __syncthreads();
   if (tid == 0) issue_stage(0);
   for (int it = tid; it < C::NODES * FL; it += C::NT) {
     VT v;
-    gather(s_g0[it / FL], it % FL, v.x);
-    v.st(s_q + (it / FL) * F + (it % FL) * FP);
+    gather(s_g0[it / FL], v.x);
+    v.st(s_q + (it / FL) * F + f0);
   }
   double carry[FP];
 #pragma unroll
@@ -193,11 +222,11 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   for (int l = 0; l < nlay; ++l) {
     const int b = l & 1;
     mbar_wait(bar + b, (uint32_t)((l >> 1) & 1));     // W(l), Minv(l), gids(l+1) have landed
-    if (tid == 0 && l + 1 < nlay) {
+    if (C::WB == 2 && tid == 0 && l + 1 < nlay) {
       fence_proxy_async();
       issue_stage(l + 1);                               // one full step ahead
     }
-    const double* s_w = s_w0 + b * C::WL;
+    const double* s_w = s_w0 + (C::WB == 2 ? b : 0) * C::WL;
     const double* s_mi = s_m0 + b * C::MTS;
     const int* s_g = s_g0 + (l % 3) * C::GTS;
     const int* s_gn = s_g0 + ((l + 1) % 3) * C::GTS;
@@ -207,7 +236,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
 #pragma unroll
       for (int s = 0; s < C::PQ; ++s) {
         const int it = tid + s * C::NT;
-        if (it < C::NODES * FL) gather(s_gn[it / FL], it % FL, qn[s]);
+        if (it < C::NODES * FL) gather(s_gn[it / FL], qn[s]);
       }
     }
     // ---- S1: strong xi and eta derivatives (one line each per thread)
@@ -287,6 +316,10 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
         }
     }
     __syncthreads();
+    if (C::WB == 1 && tid == 0 && l + 1 < nlay) {
+      fence_proxy_async();
+      issue_stage(l + 1);                               // metric buffer free after phase P
+    }
     // s_q of layer l is dead: park the prefetched q(l+1)
     if (l + 1 < nlay) {
 #pragma unroll
@@ -296,7 +329,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           VT v;
 #pragma unroll
           for (int p = 0; p < FP; ++p) v.x[p] = qn[s][p];
-          v.st(s_q + (it / FL) * F + (it % FL) * FP);
+          v.st(s_q + (it / FL) * F + f0);
         }
       }
     }
@@ -336,7 +369,13 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     __syncthreads();
     // ---- A: element accumulator (+ vertical carry) into s_a
     const int kmax = (l == nlay - 1) ? n : N;
-    if (act) {
+    if (!act) {
+      VT z;
+#pragma unroll
+      for (int p = 0; p < FP; ++p) z.x[p] = 0.0;
+#pragma unroll
+      for (int k = 0; k < n; ++k) z.st(s_a + eidx(e, i, j, k));
+    } else {
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         const int id = eidx(e, i, j, k);
@@ -359,44 +398,39 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     }
     __syncthreads();
     // ---- O: node owners sum the (1, 2 or 4) element copies in fixed order
-    {
-      const int nout = U * V * kmax * FL;
-      for (int it = tid; it < nout; it += C::NT) {
-        const int lane = it % FL;
-        const int r = it / FL;
-        const int uv = r / kmax, k = r % kmax;
-        const int u = uv / V, v = uv % V;
-        const int node = uv * n + k;
-        const int g = s_g[node];
-        if (g < 0) continue;
-        const int pu1 = min(u / N, TX - 1), pv1 = min(v / N, TY - 1);
-        const int pu0 = (u % N == 0 && u > 0) ? u / N - 1 : pu1;
-        const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
-        double val[FP];
 #pragma unroll
-        for (int p = 0; p < FP; ++p) val[p] = 0.0;
-        for (int a = pu0; a <= pu1; ++a)
-          for (int bq = pv0; bq <= pv1; ++bq) {
-            if (a >= tx || bq >= ty) continue;
-            const int ee = a * TY + bq;
-            const VT c = VT::ld(s_a + (((ee * n + (u - a * N)) * n + (v - bq * N)) * n + k) * F + lane * FP);
+    for (int sidx = 0; sidx < C::PQ; ++sidx) {
+      const int it = tid + sidx * C::NT;
+      if (it >= C::NODES * FL) break;
+      const int node = it / FL;               // = uv * n + k
+      const int k = node % n, uv = node / n;
+      if (k >= kmax) continue;
+      const int g = s_g[node];
+      if (g < 0) continue;
+      const int4 ct = *reinterpret_cast<const int4*>(s_ct + uv * 4);
+      const int kof = k * F + f0;
+      VT val = VT::ld(s_a + ct.x + kof);
+      if (ct.y >= 0) {
+        const VT c1 = VT::ld(s_a + ct.y + kof);
 #pragma unroll
-            for (int p = 0; p < FP; ++p) val[p] += c.x[p];
-          }
-        const int cd = code_t[uv];
-        if (cd < 0) {
-          double* o = A.out + (int64_t)g * A.ldo;
-          const double m = A.scale * s_mi[node];
+        for (int p = 0; p < FP; ++p) val.x[p] += c1.x[p];
+      }
+      if (ct.z >= 0) {
+        const VT c2 = VT::ld(s_a + ct.z + kof), c3 = VT::ld(s_a + ct.w + kof);
 #pragma unroll
-          for (int p = 0; p < FP; ++p) o[A.of.f[lane * FP + p]] = m * val[p];
-          if (lane == 0 && A.zero_mask)
-            for (int zc = 0; zc < A.ldo; ++zc)
-              if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
-        } else {
-          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5 + lane * FP;
+        for (int p = 0; p < FP; ++p) val.x[p] += c2.x[p] + c3.x[p];
+      }
+      const int cd = code_t[uv];
+      if (cd < 0) {
+        double* o = A.out + (int64_t)g * A.ldo;
+        const double m = A.scale * s_mi[node];
 #pragma unroll
-          for (int p = 0; p < FP; ++p) o[p] = val[p];
-        }
+        for (int p = 0; p < FP; ++p) o[ocol[p]] = m * val.x[p];
+        if (fl == 0 && A.zero_mask)
+          for (int zc = 0; zc < A.ldo; ++zc)
+            if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+      } else {
+        val.st_any(A.part + ((int64_t)cd * A.n_z + l * N + k) * 5 + f0);
       }
     }
     __syncthreads();
@@ -468,12 +502,7 @@ int run_tile(const TileArgs& A, const double* Drow, cudaStream_t st) {
   using C = TileCfg<n, TX, TY, F, FP>;
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
-  static const int mb_env = [] {
-    const char* s = getenv("HV_TILE_MINB");
-    return s ? atoi(s) : 0;
-  }();
-  auto kern = (C::MINB >= 3 && mb_env != 2) ? lap_tile_kernel<n, TX, TY, F, FP, (C::MINB >= 3 ? 3 : 1)>
-                                             : lap_tile_kernel<n, TX, TY, F, FP, (C::MINB >= 2 ? 2 : 1)>;
+  auto kern = lap_tile_kernel<n, TX, TY, F, FP, C::MINB>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
