@@ -28,7 +28,8 @@ int check_plan(const hv_lap_plan* P) {
 // Run one Laplacian pass with the best available kernel for this plan.
 int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st) {
-  if (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf)) {
+  const bool plane = P->d_gt && P->d_Mt && hv::plane_supported(P->N, P->TX, P->TY, nf);
+  if (plane || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf))) {
     hv::TileArgs A{};
     A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
     A.ntiles = P->ntiles; A.nslot = P->nslot;
@@ -36,7 +37,7 @@ int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const h
     A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
     A.Wt = P->d_Wt; A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
     A.zero_mask = zero_mask; A.scale = scale; A.out = out; A.part = P->d_part;
-    return hv::laplacian_tile(A, P->N, nf, P->D, st);
+    return plane ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
   }
   if (zero_mask) {
     const int64_t tot = P->nglobal * ldo;
@@ -52,6 +53,8 @@ extern "C" int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nl
                                    const double* d_W, int64_t nloc, double* d_Wt, void* stream) {
   if (N < 1 || N > 8 || TX < 1 || TY < 1 || ntiles <= 0 || nlay <= 0 || !d_elem || !d_W || !d_Wt)
     HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_metric: bad arguments");
+  if (hv::plane_supported(N, TX, TY, 4))
+    return hv::plane_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
   return hv::tile_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
 }
 

@@ -22,7 +22,10 @@ __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 
 def tile_shape(N, F=4):
-    """(TX, TY) of the compiled tile kernels (lap_tile.cu): 2x2 columns, 2x1 for N = 7."""
+    """(TX, TY) of the compiled sweep kernels: 4x2 columns for the plane-owner kernel
+    (lap_plane.cu, N <= 4), 2x2 for the line kernel (lap_tile.cu, N = 5, 6), 2x1 for N = 7."""
+    if N <= 4:
+        return (4, 2)
     return (2, 1) if N == 7 else (2, 2)
 
 
