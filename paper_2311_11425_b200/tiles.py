@@ -22,9 +22,12 @@ __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 
 def tile_shape(N, F=4):
-    """(TX, TY) of the compiled sweep kernels: 4x2 columns for the plane-owner kernel
-    (lap_plane.cu, N <= 4), 2x2 for the line kernel (lap_tile.cu, N = 5, 6), 2x1 for N = 7."""
-    if N <= 4:
+    """(TX, TY) of the compiled sweep kernels: 2x2 columns for the line kernel
+    (lap_tile.cu), 2x1 for N = 7.  HV_KERNEL=plane selects the experimental
+    plane-owner kernel (lap_plane.cu, 4x2 tiles, N <= 4)."""
+    import os
+
+    if N <= 4 and os.environ.get("HV_KERNEL", "") == "plane":
         return (4, 2)
     return (2, 1) if N == 7 else (2, 2)
 
