@@ -148,9 +148,29 @@ int hv_laplacian(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf
 
 /* hyperdiffusion_apply (hyperdiff.py:97-106): out (nglobal, ldo) gets
  * (-1)^(alpha+1) L^alpha q on the nvar listed variables and 0 on every other
- * column of out (out[:,0] = 0 as in the reference). q is (nglobal, ldq). */
+ * column of out (out[:,0] = 0 as in the reference). q is (nglobal, ldq).
+ * accumulate != 0: out += H_nu(q) instead (rhs_horizontal's `out += ...`,
+ * euler.py:130-133), other columns untouched. */
 int hv_hyperdiffusion(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nvar, const int32_t* h_vars,
-                      int alpha, double* d_out, int64_t ldo, void* stream);
+                      int alpha, double* d_out, int64_t ldo, int accumulate, void* stream);
+
+/* ------------------------------------------------------------ Euler RHS
+ * EulerOps._precompute element part (euler.py:39-59): per element node the
+ * record read by hv_euler_rhs, component-major (18, nelem*n^3): grad xi (3),
+ * grad eta (3), grad zeta gathered (3), Jg gathered (1), dPhi_m (3), flux mask
+ * (1), Phi (1), rhat (3).  d_Phi_g / d_mask_g are gridpoint arrays. */
+int hv_euler_setup(int N, const double* h_D, int64_t nelem, const int32_t* d_gid, const double* d_grad,
+                   const double* d_Jg, const double* d_gz, const double* d_Phi_g, const double* d_mask_g,
+                   const double* d_coords, int sphere, double* d_M, void* stream);
+/* rhs_full (dirs = 7, coriolis 0 = rhat) / rhs_horizontal without H_nu (dirs = 3,
+ * coriolis 1 = zetahat) for set_id 0 = 2NC, 1 = 2C, 2 = 3C (euler.py:111-129,
+ * 159-224): element fluxes -> flat-order DSS -> Minv.  out (nglobal, ldo>=5)
+ * receives the 5 tendencies (accumulate != 0: added). d_work >= 5*nelem*n^3. */
+int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int coriolis, double P_A, double R, double gamma,
+                 double omega, int64_t nelem, int64_t nglobal, const int32_t* d_gid, const double* d_w3,
+                 const double* d_M, const int64_t* d_off, const int32_t* d_idx, const double* d_Minv,
+                 const double* d_q, int64_t ldq, double* d_work, double* d_out, int64_t ldo, int accumulate,
+                 void* stream);
 
 #ifdef __cplusplus
 }

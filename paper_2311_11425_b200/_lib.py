@@ -77,7 +77,10 @@ _SIGS = {
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
     "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, _P, _P]),
-    "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, _P]),
+    "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, C.c_int, _P]),
+    "hv_euler_setup": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P]),
+    "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, _P,
+                               _P, _P, _P, _P, _I64, _P, _P, _I64, C.c_int, _P]),
     # test hook (host build of the metric arithmetic); never used by the product path
     "hv_debug_metric_terms_host": (C.c_int, [C.c_int, C.c_int, _P, _P, _I64, _P, _P, _P]),
 }

@@ -27,7 +27,8 @@ int check_plan(const hv_lap_plan* P) {
 
 // Run one Laplacian pass with the best available kernel for this plan.
 int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
-             int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st) {
+             int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st,
+             int accumulate = 0) {
   const bool plane = P->d_gt && P->d_Mt && hv::plane_supported(P->N, P->TX, P->TY, nf);
   if (plane || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf))) {
     hv::TileArgs A{};
@@ -36,15 +37,15 @@ int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const h
     A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
     A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
     A.Wt = P->d_Wt; A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
-    A.zero_mask = zero_mask; A.scale = scale; A.out = out; A.part = P->d_part;
+    A.zero_mask = zero_mask; A.accumulate = accumulate; A.scale = scale; A.out = out; A.part = P->d_part;
     return plane ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
   }
-  if (zero_mask) {
+  if (zero_mask && !accumulate) {
     const int64_t tot = P->nglobal * ldo;
     zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(out, P->nglobal, ldo, ~zero_mask);
     HV_LAUNCH_CHECK();
   }
-  return hv::laplacian_v1(P, q, ldq, nf, qf, out, ldo, of, scale, st);
+  return hv::laplacian_v1(P, q, ldq, nf, qf, out, ldo, of, scale, accumulate, st);
 }
 
 }  // namespace
@@ -81,7 +82,8 @@ extern "C" int hv_laplacian(const hv_lap_plan* P, const double* d_q, int64_t ldq
 }
 
 extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar,
-                                 const int32_t* h_vars, int alpha, double* d_out, int64_t ldo, void* stream) {
+                                 const int32_t* h_vars, int alpha, double* d_out, int64_t ldo, int accumulate,
+                                 void* stream) {
   int rc = check_plan(P);
   if (rc) return rc;
   if (alpha != 1 && alpha != 2) HV_FAIL(HV_ERR_INVALID, "alpha must be 1 or 2");
@@ -99,14 +101,15 @@ extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_
   }
   const unsigned zmask = ((ldo >= 32) ? 0xffffffffu : ((1u << ldo) - 1u)) & ~keep;
   if (nvar == 0) {
+    if (accumulate) return HV_OK;
     const int64_t tot = P->nglobal * ldo;
     zero_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_out, P->nglobal, ldo, 0u);
     HV_LAUNCH_CHECK();
     return HV_OK;
   }
   const double sign = (alpha % 2 == 1) ? 1.0 : -1.0;  // (-1)^(alpha+1)
-  if (alpha == 1) return lap_pass(P, d_q, ldq, nvar, qf, d_out, ldo, of, sign, zmask, st);
+  if (alpha == 1) return lap_pass(P, d_q, ldq, nvar, qf, d_out, ldo, of, sign, zmask, st, accumulate);
   rc = lap_pass(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, 0u, st);
   if (rc) return rc;
-  return lap_pass(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st);
+  return lap_pass(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st, accumulate);
 }

@@ -1,0 +1,317 @@
+// Compressible-Euler right-hand side on the device (sets 2NC / 2C / 3C).
+//
+// Reference: EulerOps._precompute (euler.py:39-59), rhs_full / rhs_horizontal
+// (euler.py:111-134), _contravariant (148-154), _acc_advective (159-189),
+// _acc_flux (191-224), pressure (state.py:84-101).
+//
+// euler_setup  (once per EulerOps): per element node the 13-15 doubles the RHS
+//              reads -- grad xi, grad eta (element), grad zeta (projected,
+//              gathered), Jg (projected, gathered), dPhi_m (strong derivative of
+//              the gathered geopotential), flux mask, Phi (3C), rhat.
+// euler_elem   one CTA per element, one thread per node: gathers the 5 fields,
+//              EOS, contravariant velocities, all fluxes of the requested
+//              directions into shared memory, then every node forms its weak /
+//              strong line sums, geopotential and Coriolis terms -> element
+//              accumulator (5 fields).
+// DSS + Minv   the flat-order CSR sum of lap_v1 (dss_minv_v1), optionally
+//              accumulating into the output (S + H_nu in one buffer).
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "hv_common.h"
+#include "lap_common.cuh"
+
+namespace hv {
+int dss_minv_accumulate(const double* work, int64_t nloc, const int64_t* off, const int32_t* idx, const double* Minv,
+                        int64_t ng, double* out, int64_t ldo, int nf, bool accumulate, cudaStream_t st);
+}
+
+namespace {
+
+// metric record per element node (component-major, nloc stride)
+enum { M_GXI = 0, M_GETA = 3, M_GZETA = 6, M_JG = 9, M_DPHI = 10, M_MASK = 13, M_PHI = 14, M_RHAT = 15, M_NCOMP = 18 };
+
+struct EulerConsts {
+  double P_A, R, gamma, omega;
+  int set;       // 0 = 2NC, 1 = 2C, 2 = 3C
+  int dirs;      // bit mask of reference directions
+  int coriolis;  // 0 = rhat, 1 = zetahat
+};
+
+template <int n>
+__global__ void __launch_bounds__(512) euler_setup_kernel(hv::DTab<n> Dt, int64_t nelem, const int32_t* __restrict__ gid,
+                                                          const double* __restrict__ grad, const double* __restrict__ Jg,
+                                                          const double* __restrict__ gz, const double* __restrict__ Phi_g,
+                                                          const double* __restrict__ mask_g,
+                                                          const double* __restrict__ coords, int sphere,
+                                                          double* __restrict__ Mout) {
+  constexpr int nn = n * n * n;
+  __shared__ double sPhi[nn];
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t nloc = nelem * nn;
+  const int64_t p = e * nn + t;
+  const int i = t / (n * n), j = (t / n) % n, k = t % n;
+  int g = 0;
+  if (t < nn) {
+    g = gid[p];
+    sPhi[t] = Phi_g[g];
+  }
+  __syncthreads();
+  if (t >= nn) return;
+  for (int c = 0; c < 3; ++c) {
+    Mout[(M_GXI + c) * nloc + p] = grad[(e * 9 + 0 * 3 + c) * nn + t];
+    Mout[(M_GETA + c) * nloc + p] = grad[(e * 9 + 1 * 3 + c) * nn + t];
+    Mout[(M_GZETA + c) * nloc + p] = gz[(int64_t)g * 3 + c];
+  }
+  Mout[M_JG * nloc + p] = Jg[g];
+  // dPhi_m = strong derivative of the gathered geopotential (euler.py:58-59)
+  double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < n; ++a) {
+    d0 += Dt.D[i][a] * sPhi[(a * n + j) * n + k];
+    d1 += Dt.D[j][a] * sPhi[(i * n + a) * n + k];
+    d2 += Dt.D[k][a] * sPhi[(i * n + j) * n + a];
+  }
+  Mout[(M_DPHI + 0) * nloc + p] = d0;
+  Mout[(M_DPHI + 1) * nloc + p] = d1;
+  Mout[(M_DPHI + 2) * nloc + p] = d2;
+  Mout[M_MASK * nloc + p] = mask_g[g];
+  Mout[M_PHI * nloc + p] = sPhi[t];
+  // rhat: element coordinates / |x| on the sphere, zhat in the box (euler.py:48-55)
+  if (sphere) {
+    const double x = coords[(e * 3 + 0) * nn + t], y = coords[(e * 3 + 1) * nn + t], z = coords[(e * 3 + 2) * nn + t];
+    const double r = sqrt(x * x + y * y + z * z);
+    Mout[(M_RHAT + 0) * nloc + p] = x / r;
+    Mout[(M_RHAT + 1) * nloc + p] = y / r;
+    Mout[(M_RHAT + 2) * nloc + p] = z / r;
+  } else {
+    Mout[(M_RHAT + 0) * nloc + p] = 0.0;
+    Mout[(M_RHAT + 1) * nloc + p] = 0.0;
+    Mout[(M_RHAT + 2) * nloc + p] = 1.0;
+  }
+}
+
+template <int n>
+__global__ void __launch_bounds__(512) euler_elem_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
+                                                         const int32_t* __restrict__ gid, const double* __restrict__ w3,
+                                                         const double* __restrict__ Mt, const double* __restrict__ q,
+                                                         int64_t ldq, double* __restrict__ work) {
+  constexpr int nn = n * n * n;
+  extern __shared__ double sm[];
+  // 2C / 3C: per direction m: [0] w3*F_rho, [1] w3*F_thermo (weak), [2..4] momentum fluxes (strong)
+  // 2NC: [0..2] w3*F_rho per m (weak), [3..7] u, v, w, theta, P (strong derivatives)
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x;
+  const bool act = t < nn;
+  const int64_t nloc = nelem * nn;
+  const int64_t p = e * nn + (act ? t : 0);
+  const int i = t / (n * n), j = (t / n) % n, k = t % n;
+  double qv[5] = {0, 0, 0, 0, 0}, gm[3][3] = {}, Jg = 0, mask = 0, dphi[3] = {}, phi = 0, P = 0, un[3] = {};
+  if (act) {
+    const int g = gid[p];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) gm[m][c] = Mt[(m * 3 + c) * nloc + p];
+    Jg = Mt[M_JG * nloc + p];
+    mask = Mt[M_MASK * nloc + p];
+#pragma unroll
+    for (int m = 0; m < 3; ++m) dphi[m] = Mt[(M_DPHI + m) * nloc + p];
+    phi = Mt[M_PHI * nloc + p];
+    const double rho = qv[0];
+    // EOS (state.py:84-101), reference expression order
+    if (K.set == 0) P = K.P_A * pow(qv[0] * K.R * qv[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+    else {
+      const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
+      P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);
+    }
+    // contravariant velocities (euler.py:148-154)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      double s = gm[m][0] * qv[1] + gm[m][1] * qv[2] + gm[m][2] * qv[3];
+      if (K.set != 0) s = s / rho;
+      un[m] = (m == 2) ? s * mask : s;
+    }
+  }
+  const double w = act ? w3[t] : 0.0;
+  const double wj = w * Jg;
+  double acc[5] = {0, 0, 0, 0, 0};
+  if (K.set != 0) {
+    const double tflux = (K.set == 1) ? qv[4] / qv[0] : (qv[4] + P) / qv[0];
+    double* s = sm;  // [m][5][nn]
+    if (act) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const double jun = Jg * un[m];
+        s[(m * 5 + 0) * nn + t] = w * (jun * qv[0]);
+        s[(m * 5 + 1) * nn + t] = w * (jun * qv[0] * tflux);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s[(m * 5 + 2 + c) * nn + t] = Jg * (qv[1 + c] * un[m] + P * gm[m][c]);
+      }
+    }
+    __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        if (!((K.dirs >> m) & 1)) continue;
+        double wk0 = 0.0, wk4 = 0.0, st[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < n; ++a) {
+          const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
+          const int ii = (m == 0) ? i : (m == 1) ? j : k;
+          const double dw = Dt.D[a][ii], ds = Dt.D[ii][a];
+          wk0 += dw * s[(m * 5 + 0) * nn + o];
+          wk4 += dw * s[(m * 5 + 1) * nn + o];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) st[c] += ds * s[(m * 5 + 2 + c) * nn + o];
+        }
+        acc[0] += wk0;   // acc -= weak = acc + sum_a D[a,i] (w3 F)_a
+        acc[4] += wk4;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[1 + c] -= w * st[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double sg = 0.0;
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+          if ((K.dirs >> m) & 1) sg += dphi[m] * gm[m][c];
+        acc[1 + c] -= wj * qv[0] * sg;
+      }
+    }
+  } else {
+    double* s = sm;  // [0..2]: w3*Jg*rho*un_m ; [3..7]: u, v, w, theta, P
+    if (act) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) s[m * nn + t] = w * (Jg * qv[0] * un[m]);
+#pragma unroll
+      for (int f = 0; f < 4; ++f) s[(3 + f) * nn + t] = qv[1 + f];
+      s[7 * nn + t] = P;
+    }
+    __syncthreads();
+    if (act) {
+      double adv[4] = {0, 0, 0, 0}, pg[3] = {0, 0, 0};
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        if (!((K.dirs >> m) & 1)) continue;
+        double wk0 = 0.0, dd[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < n; ++a) {
+          const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
+          const int ii = (m == 0) ? i : (m == 1) ? j : k;
+          wk0 += Dt.D[a][ii] * s[m * nn + o];
+#pragma unroll
+          for (int f = 0; f < 5; ++f) dd[f] += Dt.D[ii][a] * s[(3 + f) * nn + o];
+        }
+        acc[0] += wk0;
+#pragma unroll
+        for (int f = 0; f < 4; ++f) adv[f] += un[m] * dd[f];
+        const double pm = dd[4] / qv[0] + dphi[m];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pg[c] += pm * gm[m][c];
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f) acc[1 + f] -= wj * adv[f];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[1 + c] -= wj * pg[c];
+    }
+  }
+  if (!act) return;
+  // Coriolis 2 omega e x u (euler.py:183-188, 217-223)
+  if (K.omega > 0.0) {
+    double ev[3];
+    if (K.coriolis == 0) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ev[c] = Mt[(M_RHAT + c) * nloc + p];
+    } else {
+      const double zn = sqrt(gm[2][0] * gm[2][0] + gm[2][1] * gm[2][1] + gm[2][2] * gm[2][2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) ev[c] = gm[2][c] / zn;
+    }
+    const double ux = qv[1], uy = qv[2], uz = qv[3];
+    const double cx = ev[1] * uz - ev[2] * uy, cy = ev[2] * ux - ev[0] * uz, cz = ev[0] * uy - ev[1] * ux;
+    acc[1] -= wj * 2.0 * K.omega * cx;
+    acc[2] -= wj * 2.0 * K.omega * cy;
+    acc[3] -= wj * 2.0 * K.omega * cz;
+  }
+#pragma unroll
+  for (int f = 0; f < 5; ++f) work[f * nloc + p] = acc[f];
+}
+
+template <int n>
+int run_setup(const double* Drow, int64_t nelem, const int32_t* gid, const double* grad, const double* Jg,
+              const double* gz, const double* Phi_g, const double* mask_g, const double* coords, int sphere,
+              double* Mout, cudaStream_t st) {
+  hv::DTab<n> Dt;
+  hv::fill_dtab(Dt, Drow);
+  constexpr int nn = n * n * n;
+  euler_setup_kernel<n><<<(unsigned)nelem, ((nn + 31) / 32) * 32, 0, st>>>(Dt, nelem, gid, grad, Jg, gz, Phi_g, mask_g,
+                                                                           coords, sphere, Mout);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+template <int n>
+int run_elem(const double* Drow, const EulerConsts& K, int64_t nelem, const int32_t* gid, const double* w3,
+             const double* Mt, const double* q, int64_t ldq, double* work, cudaStream_t st) {
+  hv::DTab<n> Dt;
+  hv::fill_dtab(Dt, Drow);
+  constexpr int nn = n * n * n;
+  const size_t smem = sizeof(double) * 15 * nn;
+  auto kern = euler_elem_kernel<n>;
+  if (smem > 48 * 1024) HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)nelem, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, work);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+}  // namespace
+
+extern "C" int hv_euler_setup(int N, const double* h_D, int64_t nelem, const int32_t* d_gid, const double* d_grad,
+                              const double* d_Jg, const double* d_gz, const double* d_Phi_g, const double* d_mask_g,
+                              const double* d_coords, int sphere, double* d_M, void* stream) {
+  if (N < 1 || N > 7 || !h_D || nelem <= 0 || !d_gid || !d_grad || !d_Jg || !d_gz || !d_Phi_g || !d_mask_g ||
+      !d_coords || !d_M)
+    HV_FAIL(HV_ERR_INVALID, "hv_euler_setup: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (N + 1) {
+    case 2: return run_setup<2>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    case 3: return run_setup<3>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    case 4: return run_setup<4>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    case 5: return run_setup<5>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    case 6: return run_setup<6>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    case 7: return run_setup<7>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+    default: return run_setup<8>(h_D, nelem, d_gid, d_grad, d_Jg, d_gz, d_Phi_g, d_mask_g, d_coords, sphere, d_M, st);
+  }
+}
+
+extern "C" int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int coriolis, double P_A, double R,
+                            double gamma, double omega, int64_t nelem, int64_t nglobal, const int32_t* d_gid,
+                            const double* d_w3, const double* d_M, const int64_t* d_off, const int32_t* d_idx,
+                            const double* d_Minv, const double* d_q, int64_t ldq, double* d_work, double* d_out,
+                            int64_t ldo, int accumulate, void* stream) {
+  if (N < 1 || N > 7 || set_id < 0 || set_id > 2 || dirs <= 0 || dirs > 7 || !d_q || !d_out || !d_work || ldq < 5 ||
+      ldo < 5)
+    HV_FAIL(HV_ERR_INVALID, "hv_euler_rhs: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  EulerConsts K{P_A, R, gamma, omega, set_id, dirs, coriolis};
+  int rc;
+  switch (N + 1) {
+    case 2: rc = run_elem<2>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 3: rc = run_elem<3>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 4: rc = run_elem<4>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 5: rc = run_elem<5>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 6: rc = run_elem<6>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 7: rc = run_elem<7>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    default: rc = run_elem<8>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+  }
+  if (rc) return rc;
+  const int n = N + 1;
+  return hv::dss_minv_accumulate(d_work, nelem * n * n * n, d_off, d_idx, d_Minv, nglobal, d_out, ldo, 5,
+                                 accumulate != 0, st);
+}

@@ -25,6 +25,6 @@ struct FieldMap {
 };
 
 int laplacian_v1(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const FieldMap& qf, double* out,
-                 int64_t ldo, const FieldMap& of, double scale, cudaStream_t st);
+                 int64_t ldo, const FieldMap& of, double scale, int accumulate, cudaStream_t st);
 
 }  // namespace hv

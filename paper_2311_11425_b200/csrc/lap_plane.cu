@@ -317,8 +317,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         const int cd = code_t[uv];
         if (cd < 0) {
           double* o = A.out + (int64_t)g * A.ldo;
-          o[ocol] = A.scale * (s_mi[node] * val);
-          if (f == 0 && A.zero_mask)
+          const double r = A.scale * (s_mi[node] * val);
+          o[ocol] = A.accumulate ? o[ocol] + r : r;
+          if (f == 0 && A.zero_mask && !A.accumulate)
             for (int zc = 0; zc < A.ldo; ++zc)
               if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
         } else {
@@ -351,8 +352,11 @@ __global__ void plane_fixup(TileArgs A, int64_t nslot) {
   double* o = A.out + (int64_t)g * A.ldo;
   const double mi = A.Minv[g];
 #pragma unroll
-  for (int ff = 0; ff < F; ++ff) o[A.of.f[ff]] = A.scale * (mi * acc[ff]);
-  if (A.zero_mask)
+  for (int ff = 0; ff < F; ++ff) {
+    const double r = A.scale * (mi * acc[ff]);
+    o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r : r;
+  }
+  if (A.zero_mask && !A.accumulate)
     for (int zc = 0; zc < A.ldo; ++zc)
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
 }

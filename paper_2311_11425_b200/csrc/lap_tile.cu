@@ -425,8 +425,8 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
         double* o = A.out + (int64_t)g * A.ldo;
         const double m = A.scale * s_mi[node];
 #pragma unroll
-        for (int p = 0; p < FP; ++p) o[ocol[p]] = m * val.x[p];
-        if (fl == 0 && A.zero_mask)
+        for (int p = 0; p < FP; ++p) o[ocol[p]] = A.accumulate ? o[ocol[p]] + m * val.x[p] : m * val.x[p];
+        if (fl == 0 && A.zero_mask && !A.accumulate)
           for (int zc = 0; zc < A.ldo; ++zc)
             if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
       } else {
@@ -458,8 +458,11 @@ __global__ void lap_tile_fixup(TileArgs A, int64_t nslot) {
   double* o = A.out + (int64_t)g * A.ldo;
   const double mi = A.Minv[g];
 #pragma unroll
-  for (int ff = 0; ff < F; ++ff) o[A.of.f[ff]] = A.scale * (mi * acc[ff]);
-  if (A.zero_mask)
+  for (int ff = 0; ff < F; ++ff) {
+    const double r = A.scale * (mi * acc[ff]);
+    o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r : r;
+  }
+  if (A.zero_mask && !A.accumulate)
     for (int zc = 0; zc < A.ldo; ++zc)
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
 }

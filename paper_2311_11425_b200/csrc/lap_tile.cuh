@@ -23,6 +23,7 @@ struct TileArgs {
   int64_t ldq, ldo;
   FieldMap qf, of;
   unsigned zero_mask;
+  int accumulate;            // out += result (no zeroing of other columns)
   double scale;
   double* out;
   double* part;             // (rows, n_z, 5)

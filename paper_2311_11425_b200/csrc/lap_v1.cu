@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(512) lap_elem_v1(hv::DTab<n> Dt, const int32_t
 template <int NF>
 __global__ void dss_minv_v1(const double* __restrict__ work, int64_t nloc, const int64_t* __restrict__ off,
                             const int32_t* __restrict__ idx, const double* __restrict__ Minv, int64_t ng,
-                            double scale, double* __restrict__ out, int64_t ldo, hv::FieldMap fm) {
+                            double scale, double* __restrict__ out, int64_t ldo, hv::FieldMap fm, int accumulate) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= ng) return;
   const int64_t o0 = off[g], o1 = off[g + 1];
@@ -85,12 +85,15 @@ __global__ void dss_minv_v1(const double* __restrict__ work, int64_t nloc, const
   }
   const double mi = Minv[g] * scale;
 #pragma unroll
-  for (int f = 0; f < NF; ++f) out[g * ldo + fm.f[f]] = s[f] * mi;
+  for (int f = 0; f < NF; ++f) {
+    double* o = out + g * ldo + fm.f[f];
+    *o = accumulate ? *o + s[f] * mi : s[f] * mi;
+  }
 }
 
 template <int n, int NF>
 int run_v1(const hv_lap_plan* P, const double* q, int64_t ldq, const hv::FieldMap& qf, double* out, int64_t ldo,
-           const hv::FieldMap& of, double scale, cudaStream_t st) {
+           const hv::FieldMap& of, double scale, int accumulate, cudaStream_t st) {
   constexpr int nn = n * n * n;
   const int64_t nloc = P->nelem * nn;
   hv::DTab<n> Dt;
@@ -103,20 +106,20 @@ int run_v1(const hv_lap_plan* P, const double* q, int64_t ldq, const hv::FieldMa
   HV_LAUNCH_CHECK();
   const int T = 256;
   dss_minv_v1<NF><<<(unsigned)((P->nglobal + T - 1) / T), T, 0, st>>>(P->d_work, nloc, P->d_off, P->d_idx, P->d_Minv,
-                                                                    P->nglobal, scale, out, ldo, of);
+                                                                    P->nglobal, scale, out, ldo, of, accumulate);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
 
 template <int n>
 int run_v1_nf(int nf, const hv_lap_plan* P, const double* q, int64_t ldq, const hv::FieldMap& qf, double* out,
-              int64_t ldo, const hv::FieldMap& of, double scale, cudaStream_t st) {
+              int64_t ldo, const hv::FieldMap& of, double scale, int acc, cudaStream_t st) {
   switch (nf) {
-    case 1: return run_v1<n, 1>(P, q, ldq, qf, out, ldo, of, scale, st);
-    case 2: return run_v1<n, 2>(P, q, ldq, qf, out, ldo, of, scale, st);
-    case 3: return run_v1<n, 3>(P, q, ldq, qf, out, ldo, of, scale, st);
-    case 4: return run_v1<n, 4>(P, q, ldq, qf, out, ldo, of, scale, st);
-    default: return run_v1<n, 5>(P, q, ldq, qf, out, ldo, of, scale, st);
+    case 1: return run_v1<n, 1>(P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 2: return run_v1<n, 2>(P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 3: return run_v1<n, 3>(P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 4: return run_v1<n, 4>(P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    default: return run_v1<n, 5>(P, q, ldq, qf, out, ldo, of, scale, acc, st);
   }
 }
 
@@ -124,16 +127,28 @@ int run_v1_nf(int nf, const hv_lap_plan* P, const double* q, int64_t ldq, const 
 
 namespace hv {
 
+int dss_minv_accumulate(const double* work, int64_t nloc, const int64_t* off, const int32_t* idx, const double* Minv,
+                        int64_t ng, double* out, int64_t ldo, int nf, bool accumulate, cudaStream_t st) {
+  FieldMap fm{};
+  for (int f = 0; f < 5; ++f) fm.f[f] = f;
+  const int T = 256;
+  const unsigned G = (unsigned)((ng + T - 1) / T);
+  if (nf != 5) HV_FAIL(HV_ERR_UNSUPPORTED, "dss_minv_accumulate: nf=%d", nf);
+  dss_minv_v1<5><<<G, T, 0, st>>>(work, nloc, off, idx, Minv, ng, 1.0, out, ldo, fm, accumulate ? 1 : 0);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
 int laplacian_v1(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const FieldMap& qf, double* out,
-                 int64_t ldo, const FieldMap& of, double scale, cudaStream_t st) {
+                 int64_t ldo, const FieldMap& of, double scale, int acc, cudaStream_t st) {
   switch (P->N) {
-    case 1: return run_v1_nf<2>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 2: return run_v1_nf<3>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 3: return run_v1_nf<4>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 4: return run_v1_nf<5>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 5: return run_v1_nf<6>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 6: return run_v1_nf<7>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
-    case 7: return run_v1_nf<8>(nf, P, q, ldq, qf, out, ldo, of, scale, st);
+    case 1: return run_v1_nf<2>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 2: return run_v1_nf<3>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 3: return run_v1_nf<4>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 4: return run_v1_nf<5>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 5: return run_v1_nf<6>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 6: return run_v1_nf<7>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
+    case 7: return run_v1_nf<8>(nf, P, q, ldq, qf, out, ldo, of, scale, acc, st);
     default: HV_FAIL(HV_ERR_UNSUPPORTED, "laplacian: degree %d not supported (1..7)", P->N);
   }
 }

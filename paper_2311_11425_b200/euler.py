@@ -117,11 +117,89 @@ class EulerOps:
             self._plans[key] = (p, keep)
         return self._plans[key][0]
 
-    # ------------------------------------------------------------ operators
-    def rhs_full(self, state):
-        """S(q) (euler.py:111-118)."""
-        raise NotImplementedError("rhs_full: fused Euler kernel not built yet")
+    # ------------------------------------------------------------ Euler RHS
+    _SETS = {"2NC": 0, "2C": 1, "3C": 2}
 
-    def rhs_horizontal(self, state, with_hyperdiff=True):
-        """H(q) (euler.py:122-134)."""
-        raise NotImplementedError("rhs_horizontal: fused Euler kernel not built yet")
+    @property
+    def Phi_g(self):
+        """Geopotential g*height at the gridpoints (euler.py:48-53), host."""
+        if "Phi_g" not in self._h:
+            m = self.mesh
+            if m.cfg.geometry == "sphere":
+                self._h["Phi_g"] = self.c.g * m.height()
+            else:
+                self._h["Phi_g"] = self.c.g * m.xg[:, 2]
+        return self._h["Phi_g"]
+
+    def _euler_record(self):
+        """Per element node RHS record on the device (hv_euler_setup)."""
+        if "euler_M" not in self._h:
+            torch = torch_mod()
+            dev = self.mesh.device()
+            M = torch.empty((18, dev.nloc), dtype=torch.float64, device="cuda")
+            phi = to_dev(np.ascontiguousarray(self.Phi_g, dtype=np.float64))
+            mask = to_dev(np.ascontiguousarray(self.mesh.flux_mask, dtype=np.float64))
+            _lib.check(_lib.lib().hv_euler_setup(
+                dev.N, dev.D.ctypes.data, dev.nelem, dev.gid32.data_ptr(), self.metrics.d_grad.data_ptr(),
+                self.metrics.d_Jg.data_ptr(), self.metrics.d_gz.data_ptr(), phi.data_ptr(), mask.data_ptr(),
+                dev.coords.data_ptr(), int(self.mesh.cfg.geometry == "sphere"), M.data_ptr(), _lib.stream_handle()))
+            self._h["euler_M"] = M
+        return self._h["euler_M"]
+
+    def _rhs(self, state, dirs, coriolis, out=None, accumulate=False):
+        from .hyperdiff import _as_device
+
+        torch = torch_mod()
+        data = state.data if hasattr(state, "data") else state
+        q, host = _as_device(data)
+        if q.dim() != 2 or q.shape[1] != 5:
+            raise ValueError("state data must be (nglobal, 5)")
+        dev = self.mesh.device()
+        M = self._euler_record()
+        work, _ = self._workspace()
+        if out is None:
+            out = torch.empty_like(q)
+        k = self.c
+        _lib.check(_lib.lib().hv_euler_rhs(
+            dev.N, dev.D.ctypes.data, self._SETS[self.set_name], dirs, coriolis, k.P_A, k.R, k.gamma, k.omega,
+            dev.nelem, dev.nglobal, dev.gid32.data_ptr(), dev.w3.data_ptr(), M.data_ptr(), dev.off.data_ptr(),
+            dev.idx.data_ptr(), self.mass.d_Minv.data_ptr(), q.data_ptr(), 5, work.data_ptr(), out.data_ptr(), 5,
+            int(bool(accumulate)), _lib.stream_handle()))
+        return out, host
+
+    # ------------------------------------------------------------ operators
+    def rhs_full(self, state, out=None):
+        """S(q) with Coriolis 2 omega rhat x u; hyper-diffusion excluded (euler.py:111-118)."""
+        o, host = self._rhs(state, 7, 0, out=out)
+        return o.cpu().numpy() if host else o
+
+    def rhs_horizontal(self, state, with_hyperdiff=True, out=None):
+        """H(q): xi/eta terms, Coriolis 2 omega zetahat x u, plus H_nu (euler.py:122-134)."""
+        o, host = self._rhs(state, 3, 1, out=out)
+        if self.hyper is not None and with_hyperdiff:
+            from .hyperdiff import hyperdiffusion_apply
+            from .state import StateField
+
+            cfg, viscous = self.hyper
+            data = state.data if hasattr(state, "data") else state
+            qd = o.new_tensor(data) if host else data
+            hyperdiffusion_apply(StateField(self.set_name, qd), cfg, viscous, self, out=o, accumulate=True)
+        return o.cpu().numpy() if host else o
+
+    def rhs_full_hyper(self, state, out=None):
+        """S(q) + H_nu(q) in one output (the config-4 quantity; extension)."""
+        if self.hyper is None:
+            raise ValueError("rhs_full_hyper needs EulerOps(..., hyper=(cfg, viscous))")
+        from .hyperdiff import _as_device, hyperdiffusion_apply
+        from .state import StateField
+
+        data = state.data if hasattr(state, "data") else state
+        qd, host = _as_device(data)
+        o, _ = self._rhs(qd, 7, 0, out=out)
+        cfg, viscous = self.hyper
+        hyperdiffusion_apply(StateField(self.set_name, qd), cfg, viscous, self, out=o, accumulate=True)
+        return o.cpu().numpy() if host else o
+
+    def rhs_vertical(self, state):
+        """V(q) column operator (euler.py:138-144): SURVEY §8(f) 'next', not in this build."""
+        raise NotImplementedError("rhs_vertical (column operator) is the next component, see DESIGN.md §8")

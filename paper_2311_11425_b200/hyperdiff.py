@@ -182,11 +182,12 @@ def laplacian_apply_fields(q, viscous, ops, fields):
     return out.cpu().numpy() if host else out
 
 
-def hyperdiffusion_apply(state, cfg, viscous, ops, out=None):
+def hyperdiffusion_apply(state, cfg, viscous, ops, out=None, accumulate=False):
     """(-1)^(alpha+1) L^alpha on cfg.variables, zero elsewhere (hyperdiff.py:97-106).
 
     ``state`` is a StateField (numpy or CUDA data).  With CUDA data an
-    ``out`` tensor of the same shape may be supplied to avoid an allocation.
+    ``out`` tensor of the same shape may be supplied to avoid an allocation;
+    with ``accumulate=True`` the result is added to ``out`` (rhs_horizontal).
     """
     torch = torch_mod()
     data = state.data if hasattr(state, "data") else state
@@ -196,5 +197,6 @@ def hyperdiffusion_apply(state, cfg, viscous, ops, out=None):
         out = torch.empty_like(q)
     vars_ = (C.c_int32 * len(cfg.variables))(*cfg.variables)
     _lib.check(_lib.lib().hv_hyperdiffusion(C.byref(plan), q.data_ptr(), q.shape[1], len(cfg.variables), vars_,
-                                            cfg.alpha, out.data_ptr(), out.shape[1], _lib.stream_handle()))
+                                            cfg.alpha, out.data_ptr(), out.shape[1], int(bool(accumulate)),
+                                            _lib.stream_handle()))
     return out.cpu().numpy() if host else out

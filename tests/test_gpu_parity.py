@@ -164,3 +164,40 @@ def test_all_five_fields_one_pass(pair):
     got = hyperdiff.laplacian_apply_fields(o.state, p.vm, p.ops, (0, 1, 2, 3, 4))
     ref = np.stack([o.lap(f) for f in range(5)], axis=1)
     assert rel_l2(got, ref) <= TOL
+
+
+def test_rhs_full_and_horizontal_parity(pair):
+    """S(q) and H(q) (sets 2NC / 2C / 3C) vs the oracle and the reference goldens, random states."""
+    name, p, o = pair
+    from cases import random_state
+    from paper_2311_11425_b200 import euler, state
+
+    g = golden(name)
+    for s in p.c["sets"]:
+        ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
+        rs = random_state(p.m.nglobal, s)
+        oe = o.euler(s)
+        full = ops.rhs_full(state.StateField(s, rs))
+        assert rel_l2(full, oe.rhs_full(rs)) <= TOL, (s, rel_l2(full, oe.rhs_full(rs)))
+        assert rel_l2(full, g[f"rhs_full_{s}"]) <= TOL
+        hor = ops.rhs_horizontal(state.StateField(s, rs), with_hyperdiff=False)
+        assert rel_l2(hor, oe.rhs_horizontal_nohd(rs)) <= TOL, s
+        assert rel_l2(hor, g[f"rhs_h_{s}"]) <= TOL
+
+
+def test_rhs_full_plus_hyperdiffusion(pair):
+    """The config-4 quantity S + H_nu in one buffer, and rhs_horizontal with H_nu."""
+    name, p, o = pair
+    from cases import random_state
+    from paper_2311_11425_b200 import euler, state
+
+    s = "2C"
+    ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
+    rs = o.state if name == "box_n7" else random_state(p.m.nglobal, s)
+    oe = o.euler(s)
+    ref = oe.rhs_full(rs) + o.hyper(rs)
+    got = ops.rhs_full_hyper(state.StateField(s, rs))
+    assert rel_l2(got, ref) <= TOL, rel_l2(got, ref)
+    ref_h = oe.rhs_horizontal_nohd(rs) + o.hyper(rs)
+    got_h = ops.rhs_horizontal(state.StateField(s, rs), with_hyperdiff=True)
+    assert rel_l2(got_h, ref_h) <= TOL
