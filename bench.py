@@ -113,6 +113,13 @@ def algorithmic_bytes_hnu(ng, nloc, F=4, alpha=2):
     return alpha * (2 * F * ng * 8 + 6 * nloc * 8 + ng * 8 + nloc * 4)
 
 
+def algorithmic_bytes_c4(ng, nloc):
+    """SURVEY §8(d) Euler+H_nu: fused pass A (S and L pass 1) + pass B (L pass 2, accumulate)."""
+    A = 5 * ng * 8 + 19 * nloc * 8 + ng * 8 + nloc * 4 + 5 * ng * 8 + 4 * ng * 8
+    B = 4 * ng * 8 + 6 * nloc * 8 + ng * 8 + nloc * 4 + 2 * 4 * ng * 8
+    return A + B
+
+
 def build_workload(name, rank, world, scale=1):
     from paper_2311_11425_b200 import euler, hyperdiff, metrics, state, synthetic
 
@@ -124,10 +131,61 @@ def build_workload(name, rank, world, scale=1):
     cfg = hyperdiff.HyperDiffConfig(alpha=w.alpha, c=w.c)
     vm = hyperdiff.build_viscous_metric(m, mets, cfg, dt=w.dt)
     ops = euler.EulerOps(m, mets, state.PhysConstants(omega=0.0), w.set_name, hyper=(cfg, vm))
+    if w.operator == "euler+hyperdiff":
+        ops.rhs_full_hyper(state.StateField(w.set_name, torch_zeros_state(m.nglobal)))
     import torch
 
     q = synthetic.make_state(w, m, device=torch.device("cuda"))
     return dict(w=w, m=m, mets=mets, cfg=cfg, vm=vm, ops=ops, q=q, t_mesh=t_mesh)
+
+
+def torch_zeros_state(ng):
+    import torch
+
+    z = torch.zeros((ng, 5), dtype=torch.float64, device="cuda")
+    z[:, 0] = 1.0
+    z[:, 4] = 300.0
+    return z
+
+
+def time_secondary(name, steps=5, warmup=3):
+    """Device time of one op of a secondary BASELINE config (same process, inputs resident)."""
+    import torch
+
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    P = build_workload(name, 0, 1)
+    w, m, ops, vm, cfg = P["w"], P["m"], P["ops"], P["vm"], P["cfg"]
+    n3 = (w.N + 1) ** 3
+    qd = torch.from_numpy(P["q"]).cuda()
+    out = torch.empty_like(qd)
+    st = state.StateField(w.set_name, qd)
+    if w.operator == "euler+hyperdiff":
+        step = lambda: ops.rhs_full_hyper(st, out=out)  # noqa: E731
+        alg = algorithmic_bytes_c4(m.nglobal, m.nelem * n3)
+    elif w.operator == "laplacian":
+        step = lambda: hyperdiff.laplacian_apply_fields(qd, vm, ops, (0, 1, 2, 3, 4))  # noqa: E731
+        alg = algorithmic_bytes_hnu(m.nglobal, m.nelem * n3, F=5, alpha=1)
+    else:
+        step = lambda: hyperdiff.hyperdiffusion_apply(st, cfg, vm, ops, out=out)  # noqa: E731
+        alg = algorithmic_bytes_hnu(m.nglobal, m.nelem * n3)
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    peak, _, _ = _peaks()
+    res = {"workload": f"{name}: {w.operator}, N={w.N}, nelem={m.nelem}, nglobal={m.nglobal}",
+           "ms_per_op": ms, "dof_updates_per_s": w.fields_out * m.nglobal / (ms * 1e-3),
+           "roofline_frac": alg / (ms * 1e-3) / 1e9 / peak, "algorithmic_bytes_per_op": alg}
+    del P, ops, vm, qd, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def cpu_sample(name, seconds=8.0):
@@ -318,6 +376,15 @@ def run_ours(args, rank, world, local):
             "clocks": clk.summary(),
             "setup_s": {"mesh": round(P["t_mesh"], 2)},
         }
+        if world == 1 and not args.no_extras:
+            line["secondary"] = {}
+            del P, ops, vm, qd, out, st, d_in, h_in, h_out
+            torch.cuda.empty_cache()
+            for name in ("c1", "c2", "c3", "c4"):
+                try:
+                    line["secondary"][name] = time_secondary(name)
+                except Exception as exc:  # a failing secondary config must not hide the headline
+                    line["secondary"][name] = {"error": repr(exc)[:300]}
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -330,8 +397,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c5", "c2", "c3"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c3", "c4"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary configs c1-c4")
     args = ap.parse_args()
     rank, world, local = _dist()
     if args.impl == "reference":
