@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libhv_b200.so"
+LIB_PATH = Path(os.environ["HV_LIB"]) if os.environ.get("HV_LIB") else _HERE / "libhv_b200.so"
 
 HV_OK = 0
 HV_ERR_INVALID = 1

@@ -27,6 +27,10 @@
 
 #include <cstdlib>
 
+#ifndef HV_ABLATE
+#define HV_ABLATE 0   // timing experiments only: bit 1 skip S1, 2 skip W1, 4 skip O, 8 skip P
+#endif
+
 #include "hv_common.h"
 #include "lap_common.cuh"
 #include "lap_tile.cuh"
@@ -78,7 +82,8 @@ struct TileCfg {
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
-  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // gather / output items (node, lane) per thread
+  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // (node, lane) items per thread
+  static constexpr int PN = (NODES + NT - 1) / NT;       // node items per thread (gather / output)
   static constexpr int UV = U * V;
   // shared memory (doubles): q | W[WB] | a | b | Minv[2] | gid[3] (ints) | ctab (ints) | mbarrier[2]
   static constexpr int OFF_W = (SQ + 1) & ~1;
@@ -164,16 +169,28 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
   auto eidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f0; };
   auto tidx = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f0; };
-  // this thread's fields are fixed (NT is a multiple of FL): column indices in q and out
-  int qcol[FP], ocol[FP];
+  // column indices of the F fields in q and out (node-granular gather / output)
+  int qcol[F], ocol[F];
 #pragma unroll
-  for (int p = 0; p < FP; ++p) {
-    qcol[p] = A.qf.f[f0 + p];
-    ocol[p] = A.of.f[f0 + p];
+  for (int p = 0; p < F; ++p) {
+    qcol[p] = A.qf.f[p];
+    ocol[p] = A.of.f[p];
   }
-  auto gather = [&](int g, double* dst) {
+  // the common state-row case: out is (ng, 5) with fields 1..4 written and column 0 zeroed
+  const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
+  auto gather = [&](int g, double* dst) {   // all F fields of one node
+    const double* src = A.q + (int64_t)g * A.ldq;
 #pragma unroll
-    for (int p = 0; p < FP; ++p) dst[p] = (g >= 0) ? A.q[(int64_t)g * A.ldq + qcol[p]] : 0.0;
+    for (int p = 0; p < F; ++p) dst[p] = (g >= 0) ? src[qcol[p]] : 0.0;
+  };
+  auto park = [&](int node, const double* v) {
+    if constexpr (F % 2 == 0) {
+#pragma unroll
+      for (int p = 0; p < F; p += 2) *reinterpret_cast<double2*>(s_q + node * F + p) = make_double2(v[p], v[p + 1]);
+    } else {
+#pragma unroll
+      for (int p = 0; p < F; ++p) s_q[node * F + p] = v[p];
+    }
   };
   int* s_ct = reinterpret_cast<int*>(sm + C::OFF_T);  // [UV][4] scratch offsets of the element copies
   // stage l: W(l) -> W[l%2], Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3], all on bar[l%2]
@@ -209,10 +226,10 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
   __syncthreads();
   if (tid == 0) issue_stage(0);
-  for (int it = tid; it < C::NODES * FL; it += C::NT) {
-    VT v;
-    gather(s_g0[it / FL], v.x);
-    v.st(s_q + (it / FL) * F + f0);
+  for (int node = tid; node < C::NODES; node += C::NT) {
+    double v[F];
+    gather(s_g0[node], v);
+    park(node, v);
   }
   double carry[FP];
 #pragma unroll
@@ -231,16 +248,16 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     const int* s_g = s_g0 + (l % 3) * C::GTS;
     const int* s_gn = s_g0 + ((l + 1) % 3) * C::GTS;
     // ---- prefetch q(l+1) into registers (addresses from shared memory)
-    double qn[C::PQ][FP];
+    double qn[C::PN][F];
     if (l + 1 < nlay) {
 #pragma unroll
-      for (int s = 0; s < C::PQ; ++s) {
-        const int it = tid + s * C::NT;
-        if (it < C::NODES * FL) gather(s_gn[it / FL], qn[s]);
+      for (int s = 0; s < C::PN; ++s) {
+        const int node = tid + s * C::NT;
+        if (node < C::NODES) gather(s_gn[node], qn[s]);
       }
     }
     // ---- S1: strong xi and eta derivatives (one line each per thread)
-    if (act) {
+    if (act && !(HV_ABLATE & 1)) {
       const int b2 = ij / n, c = ij % n;
       VT v[n];
 #pragma unroll
@@ -279,7 +296,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     for (int k = 0; k < n; ++k)
 #pragma unroll
       for (int p = 0; p < FP; ++p) acc[k][p] = 0.0;
-    if (act) {
+    if (act && !(HV_ABLATE & 8)) {
       VT qk[n];
       double f2[n][FP];
 #pragma unroll
@@ -323,18 +340,13 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     // s_q of layer l is dead: park the prefetched q(l+1)
     if (l + 1 < nlay) {
 #pragma unroll
-      for (int s = 0; s < C::PQ; ++s) {
-        const int it = tid + s * C::NT;
-        if (it < C::NODES * FL) {
-          VT v;
-#pragma unroll
-          for (int p = 0; p < FP; ++p) v.x[p] = qn[s][p];
-          v.st(s_q + (it / FL) * F + f0);
-        }
+      for (int s = 0; s < C::PN; ++s) {
+        const int node = tid + s * C::NT;
+        if (node < C::NODES) park(node, qn[s]);
       }
     }
     // ---- W1: weak xi / eta derivatives in place
-    if (act) {
+    if (act && !(HV_ABLATE & 2)) {
       const int b2 = ij / n, c = ij % n;
       VT v[n];
 #pragma unroll
@@ -397,40 +409,65 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
       }
     }
     __syncthreads();
-    // ---- O: node owners sum the (1, 2 or 4) element copies in fixed order
+    // ---- O: node owners sum the (1, 2 or 4) element copies in fixed order and write
+    //      whole rows (all fields of a node from one thread: full sectors, no partial writes)
 #pragma unroll
-    for (int sidx = 0; sidx < C::PQ; ++sidx) {
-      const int it = tid + sidx * C::NT;
-      if (it >= C::NODES * FL) break;
-      const int node = it / FL;               // = uv * n + k
+    for (int sidx = 0; sidx < ((HV_ABLATE & 4) ? 0 : C::PN); ++sidx) {
+      const int node = tid + sidx * C::NT;    // = uv * n + k
+      if (node >= C::NODES) break;
       const int k = node % n, uv = node / n;
       if (k >= kmax) continue;
       const int g = s_g[node];
       if (g < 0) continue;
       const int4 ct = *reinterpret_cast<const int4*>(s_ct + uv * 4);
-      const int kof = k * F + f0;
-      VT val = VT::ld(s_a + ct.x + kof);
-      if (ct.y >= 0) {
-        const VT c1 = VT::ld(s_a + ct.y + kof);
+      const int kof = k * F;
+      double val[F];
 #pragma unroll
-        for (int p = 0; p < FP; ++p) val.x[p] += c1.x[p];
-      }
-      if (ct.z >= 0) {
-        const VT c2 = VT::ld(s_a + ct.z + kof), c3 = VT::ld(s_a + ct.w + kof);
-#pragma unroll
-        for (int p = 0; p < FP; ++p) val.x[p] += c2.x[p] + c3.x[p];
+      for (int p = 0; p < F; p += (F % 2 == 0 ? 2 : 1)) {
+        if constexpr (F % 2 == 0) {
+          double2 a = *reinterpret_cast<const double2*>(s_a + ct.x + kof + p);
+          if (ct.y >= 0) {
+            const double2 b = *reinterpret_cast<const double2*>(s_a + ct.y + kof + p);
+            a.x += b.x;
+            a.y += b.y;
+          }
+          if (ct.z >= 0) {
+            const double2 c = *reinterpret_cast<const double2*>(s_a + ct.z + kof + p);
+            const double2 d = *reinterpret_cast<const double2*>(s_a + ct.w + kof + p);
+            a.x += c.x + d.x;
+            a.y += c.y + d.y;
+          }
+          val[p] = a.x;
+          val[p + 1] = a.y;
+        } else {
+          double a = s_a[ct.x + kof + p];
+          if (ct.y >= 0) a += s_a[ct.y + kof + p];
+          if (ct.z >= 0) a += s_a[ct.z + kof + p] + s_a[ct.w + kof + p];
+          val[p] = a;
+        }
       }
       const int cd = code_t[uv];
       if (cd < 0) {
         double* o = A.out + (int64_t)g * A.ldo;
         const double m = A.scale * s_mi[node];
+        if (A.accumulate) {
 #pragma unroll
-        for (int p = 0; p < FP; ++p) o[ocol[p]] = A.accumulate ? o[ocol[p]] + m * val.x[p] : m * val.x[p];
-        if (fl == 0 && A.zero_mask && !A.accumulate)
-          for (int zc = 0; zc < A.ldo; ++zc)
-            if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+          for (int p = 0; p < F; ++p) o[ocol[p]] += m * val[p];
+        } else if (row5) {
+          o[0] = 0.0;
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[1 + p] = m * val[p];
+        } else {
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[ocol[p]] = m * val[p];
+          if (A.zero_mask)
+            for (int zc = 0; zc < A.ldo; ++zc)
+              if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+        }
       } else {
-        val.st_any(A.part + ((int64_t)cd * A.n_z + l * N + k) * 5 + f0);
+        double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5;
+#pragma unroll
+        for (int p = 0; p < F; ++p) o[p] = val[p];
       }
     }
     __syncthreads();
