@@ -87,14 +87,15 @@ struct TileCfg {
   static constexpr int UV = U * V;
   // shared memory (doubles): q | W[WB] | a | b | Minv[2] | gid[3] (ints) | ctab (ints) | mbarrier[2]
   static constexpr int OFF_W = (SQ + 1) & ~1;
-  static constexpr size_t SMEM2 = sizeof(double) * (OFF_W + 2 * WL + 2 * SE + 2 * MTS + 3 * GTS / 2 + 2 * UV + 4);
+  static constexpr size_t SMEM2 = sizeof(double) * (OFF_W + 2 * WL + 2 * SE + 2 * MTS + 3 * GTS / 2 + 3 * UV + 6);
   static constexpr int WB = (SMEM2 <= 220 * 1024) ? 2 : 1;   // metric ring depth
   static constexpr int OFF_A = OFF_W + WB * WL;
   static constexpr int OFF_B = OFF_A + SE;
   static constexpr int OFF_M = OFF_B + SE;
   static constexpr int OFF_G = OFF_M + 2 * MTS;
   static constexpr int OFF_T = OFF_G + 3 * GTS / 2;        // ctab: 4 ints per tile column node
-  static constexpr int OFF_BAR = OFF_T + 2 * UV;
+  static constexpr int OFF_C = OFF_T + 2 * UV;              // code: 1 int per tile column node
+  static constexpr int OFF_BAR = OFF_C + (UV + 1) / 2 + 1;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
   static constexpr int BY_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);   // CTAs per SM we aim for
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     }
   };
   int* s_ct = reinterpret_cast<int*>(sm + C::OFF_T);  // [UV][4] scratch offsets of the element copies
+  int* s_code = reinterpret_cast<int*>(sm + C::OFF_C);  // [UV] partial row of a shared column node, -1 owned
   // stage l: W(l) -> W[l%2], Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3], all on bar[l%2]
   auto issue_stage = [&](int l) {
     const int b = l & 1;
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
     for (int a = pu0; a <= pu1; ++a)
       for (int b = pv0; b <= pv1; ++b) s_ct[uv * 4 + c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n * F;
     for (; c < 4; ++c) s_ct[uv * 4 + c] = -1;
+    s_code[uv] = code_t[uv];
   }
   // prologue: gids and gather of layer 0 directly; stage 0 by TMA
   for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
           val[p] = a;
         }
       }
-      const int cd = code_t[uv];
+      const int cd = s_code[uv];
       if (cd < 0) {
         double* o = A.out + (int64_t)g * A.ldo;
         const double m = A.scale * s_mi[node];
