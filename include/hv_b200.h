@@ -128,17 +128,19 @@ typedef struct hv_lap_plan {
   const double* d_Wt;          /* tiled packed metric                                 */
   const double* d_Mt;          /* Minv in tile order (ntiles, nlay, MTS)              */
   double* d_part;              /* partial rows (rows, n_z, 5)                         */
+  int kernel;                  /* 0: line-tile kernel (lap_tile.cu), 1: plane-owner kernel (lap_plane.cu) */
 } hv_lap_plan;
 
 /* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
- * Wt[t][l][c][k][e][i*n+j] using d_elem (ntiles, nlay, TX*TY),
+ * (layout 0: line-tile kernel, [t][l][pair][k][e][i*n+j][2]; layout 1: plane kernel,
+ * [t][l][pair][i][k][e][j][2]) using d_elem (ntiles, nlay, TX*TY),
  * -1 for the absent elements of ragged tiles. */
 /* Minv in tile order: d_Mt[r*mts + c] = d_Minv[d_gt[r*gts + c]] for the rows r = (tile, layer)
  * (0 for absent nodes and padding). */
 int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* d_gt, const double* d_Minv, double* d_Mt,
                       void* stream);
 int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem, const double* d_W,
-                        int64_t nloc, double* d_Wt, void* stream);
+                        int64_t nloc, int layout, double* d_Wt, void* stream);
 
 /* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
  * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].

@@ -58,6 +58,7 @@ class LapPlan(C.Structure):
         ("d_Wt", _P),
         ("d_Mt", _P),
         ("d_part", _P),
+        ("kernel", C.c_int),
     ]
 
 
@@ -76,7 +77,7 @@ _SIGS = {
     "hv_viscous_metric": (C.c_int, [C.c_int, C.c_int, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
     "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
-    "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, _P, _P]),
+    "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, C.c_int, _P, _P]),
     "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, C.c_int, _P]),
     "hv_euler_setup": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P]),
     "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, _P,

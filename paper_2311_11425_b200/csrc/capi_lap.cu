@@ -29,7 +29,7 @@ int check_plan(const hv_lap_plan* P) {
 int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st,
              int accumulate = 0) {
-  const bool plane = P->d_gt && P->d_Mt && hv::plane_supported(P->N, P->TX, P->TY, nf);
+  const bool plane = P->d_gt && P->d_Mt && P->kernel == 1 && hv::plane_supported(P->N, P->TX, P->TY, nf);
   if (plane || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf))) {
     hv::TileArgs A{};
     A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
@@ -51,10 +51,10 @@ int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const h
 }  // namespace
 
 extern "C" int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem,
-                                   const double* d_W, int64_t nloc, double* d_Wt, void* stream) {
+                                   const double* d_W, int64_t nloc, int layout, double* d_Wt, void* stream) {
   if (N < 1 || N > 8 || TX < 1 || TY < 1 || ntiles <= 0 || nlay <= 0 || !d_elem || !d_W || !d_Wt)
     HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_metric: bad arguments");
-  if (hv::plane_supported(N, TX, TY, 4))
+  if (layout == 1 && hv::plane_supported(N, TX, TY, 4))
     return hv::plane_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
   return hv::tile_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
 }

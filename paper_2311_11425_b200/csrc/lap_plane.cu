@@ -74,30 +74,39 @@ struct PlaneCfg {
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * n * n;          // packed metric doubles per tile-layer
-  // shared memory (doubles): q[2] | scratch | Minv[2] | gid[3] (ints) | ctab (int4) | mbarrier[2]
-  static constexpr int OFF_S = 2 * ((SQ + 1) & ~1);
+  static constexpr int PN = (NODES + NT - 1) / NT;       // node items per thread
+  // shared memory (doubles): q | W | scratch | Minv[2] | gid[3] (ints) | ctab (int4) | code | mbarrier[2]
+  static constexpr int OFF_W = (SQ + 1) & ~1;
+  static constexpr int OFF_S = OFF_W + WL;
   static constexpr int OFF_M = OFF_S + SE;
   static constexpr int OFF_G = OFF_M + 2 * MTS;
   static constexpr int OFF_T = OFF_G + 3 * GTS / 2;
-  static constexpr int OFF_BAR = OFF_T + 2 * UV;
+  static constexpr int OFF_C = OFF_T + 2 * UV;
+  static constexpr int OFF_BAR = OFF_C + (UV + 1) / 2 + 1;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
   static constexpr int BY_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);
 };
 
-// Wp layout (per tile-layer): [c 6][i n][k n][e NE][j n]; lanes (e, j, f) read consecutive
-// doubles for a fixed (c, i, k) and the F field lanes of a plane broadcast.
+__device__ __forceinline__ void cp_async16cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+// Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
+// (w02,w11) (w12,w22)); the F field lanes of a plane broadcast one LDS.128.
 template <int n, int TX, int TY, int F, int MB>
 __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F>;
   constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV;
   extern __shared__ __align__(16) double sm[];
-  double* s_q0 = sm;                                   // [2][NODES][F]
+  double* s_q = sm;                                    // [NODES][F]
+  double* s_w = sm + C::OFF_W;                         // metric of the current layer (TMA)
   double* s_s = sm + C::OFF_S;                         // [NE][n i][n j][n k][F] eta scratch / element acc
   double* s_m0 = sm + C::OFF_M;                        // [2][MTS] Minv (TMA)
   int* s_g0 = reinterpret_cast<int*>(sm + C::OFF_G);   // [3][GTS] gids (TMA)
   int4* s_ct = reinterpret_cast<int4*>(sm + C::OFF_T); // [UV] element-copy offsets
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  int* s_code = reinterpret_cast<int*>(sm + C::OFF_C); // [UV] partial row or -1
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // [0] Minv/gid stage, [1] metric
   const int tid = threadIdx.x;
   const int f = tid % F;
   const int jp = (tid / F) % n;
@@ -107,29 +116,50 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
   const bool act = (px < tx) && (py < ty);
   const int nlay = A.nlay;
-  const int32_t* code_t = A.code + t * UV;
   const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::GTS;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
   const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
-  const int qcol = A.qf.f[f], ocol = A.of.f[f];
-  // scratch index (element-private), tile-node index
+  int qcol[F], ocol[F];
+#pragma unroll
+  for (int p = 0; p < F; ++p) {
+    qcol[p] = A.qf.f[p];
+    ocol[p] = A.of.f[p];
+  }
+  const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
+  const bool q_contig = (F == 4 && A.ldq == 4 && qcol[0] == 0 && qcol[1] == 1 && qcol[2] == 2 && qcol[3] == 3);
+  // element-private scratch index (this thread's field); tile-node index
   auto sidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
   auto tq = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
 
-  auto issue_stage = [&](int l) {       // Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3] on bar[l%2]
+  auto issue_stage = [&](int l) {       // Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3] on bar[0]
     const int b = l & 1;
     const bool nextg = (l + 1 < nlay);
     const uint32_t bytes = C::MTS * 8 + (nextg ? C::GTS * 4 : 0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + b)), "r"(bytes)
-                 : "memory");
-    tma_copy(s_m0 + b * C::MTS, Mt_t + (int64_t)l * C::MTS, C::MTS * 8, bar + b);
-    if (nextg) tma_copy(s_g0 + ((l + 1) % 3) * C::GTS, gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4, bar + b);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    tma_copy(s_m0 + b * C::MTS, Mt_t + (int64_t)l * C::MTS, C::MTS * 8, bar);
+    if (nextg) tma_copy(s_g0 + ((l + 1) % 3) * C::GTS, gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4, bar);
   };
-  auto issue_gather = [&](const int* g_src, double* dst) {   // async gather of one layer of q
-    for (int it = tid; it < C::SQ; it += C::NT) {
-      const int g = g_src[it / F];
-      if (g >= 0) cp_async8(dst + it, A.q + (int64_t)g * A.ldq + A.qf.f[it % F]);
-      else dst[it] = 0.0;
+  auto issue_metric = [&](int l) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + 1)), "r"(C::WL * 8)
+                 : "memory");
+    tma_copy(s_w, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + 1);
+  };
+  // node-granular async gather of one layer of q (all F fields of a node per item)
+  auto issue_gather = [&](const int* g_src) {
+    for (int node = tid; node < C::NODES; node += C::NT) {
+      const int g = g_src[node];
+      double* dst = s_q + node * F;
+      if (g < 0) {
+#pragma unroll
+        for (int p = 0; p < F; ++p) dst[p] = 0.0;
+      } else if (q_contig) {
+        cp_async16cg(dst, A.q + (int64_t)g * 4);
+        cp_async16cg(dst + 2, A.q + (int64_t)g * 4 + 2);
+      } else {
+        const double* src = A.q + (int64_t)g * A.ldq;
+#pragma unroll
+        for (int p = 0; p < F; ++p) cp_async8(dst + p, src + qcol[p]);
+      }
     }
     cp_async_commit();
   };
@@ -148,36 +178,31 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     for (int a = pu0; a <= pu1; ++a)
       for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n * F;
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
+    s_code[uv] = A.code[t * UV + uv];
   }
   for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
   __syncthreads();
   if (tid == 0) {
     issue_stage(0);
-    l2_prefetch(Wt_t, C::WL * 8);
+    issue_metric(0);
   }
-  issue_gather(s_g0, s_q0);
+  issue_gather(s_g0);
   double carry[n];
 #pragma unroll
   for (int i = 0; i < n; ++i) carry[i] = 0.0;
 
   for (int l = 0; l < nlay; ++l) {
     const int b = l & 1;
-    // ---- a: q(l) and stage l have landed; start q(l+1), Minv / gids of l+1, metric of l+1 into L2
+    // ---- a: q(l) and stage l have landed; start Minv / gids of l+1
     cp_async_wait_all();
-    mbar_wait(bar + b, (uint32_t)((l >> 1) & 1));
+    mbar_wait(bar, (uint32_t)(l & 1));
     __syncthreads();
-    const double* s_q = s_q0 + b * ((C::SQ + 1) & ~1);
+    if (tid == 0 && l + 1 < nlay) {
+      fence_proxy_async();
+      issue_stage(l + 1);
+    }
     const double* s_mi = s_m0 + b * C::MTS;
     const int* s_g = s_g0 + (l % 3) * C::GTS;
-    if (l + 1 < nlay) {
-      if (tid == 0) {
-        fence_proxy_async();
-        issue_stage(l + 1);
-        l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
-      }
-      issue_gather(s_g0 + ((l + 1) % 3) * C::GTS, s_q0 + (b ^ 1) * ((C::SQ + 1) & ~1));
-    }
-    const double* W = Wt_t + (int64_t)l * C::WL + e * n + jp;   // + ((c*n + i)*n + k)*NE*n
     // ---- b: plane derivatives in registers, eta lines (i = jp) strong
     double p0[n][n], p2[n][n];   // [i][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
     if (act) {
@@ -193,12 +218,14 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
           for (int a = 0; a < n; ++a) s = fma(Dt.D[k][a], ql[a], s);
           p2[i][k] = s;
         }
+#pragma unroll
+        for (int k = 0; k < n; ++k) p0[i][k] = ql[k];   // q plane, xi-differentiated below
       }
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         double ql[n];
 #pragma unroll
-        for (int i = 0; i < n; ++i) ql[i] = s_q[tq(px * N + i, py * N + jp, k)];
+        for (int i = 0; i < n; ++i) ql[i] = p0[i][k];
 #pragma unroll
         for (int i = 0; i < n; ++i) {
           double s = 0.0;
@@ -223,21 +250,25 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
       }
     }
     __syncthreads();
+    // s_q of layer l is dead: gather q(l+1) (addresses arrived with stage l)
+    if (l + 1 < nlay) issue_gather(s_g0 + ((l + 1) % 3) * C::GTS);
     // ---- c: flux at the plane nodes, weak xi / zeta in registers
+    mbar_wait(bar + 1, (uint32_t)(l & 1));
     if (act) {
+      const double* W = s_w + (e * n + jp) * 2;
 #pragma unroll
       for (int i = 0; i < n; ++i)
 #pragma unroll
         for (int k = 0; k < n; ++k) {
-          const int wo = (i * n + k) * NE * n;
-          const double w00 = __ldg(W + 0 * n * n * NE * n + wo), w01 = __ldg(W + 1 * n * n * NE * n + wo);
-          const double w02 = __ldg(W + 2 * n * n * NE * n + wo), w11 = __ldg(W + 3 * n * n * NE * n + wo);
-          const double w12 = __ldg(W + 4 * n * n * NE * n + wo), w22 = __ldg(W + 5 * n * n * NE * n + wo);
+          const int wo = (i * n + k) * NE * n * 2;
+          const double2 wa = *reinterpret_cast<const double2*>(W + 0 * n * n * NE * n * 2 + wo);   // w00 w01
+          const double2 wb = *reinterpret_cast<const double2*>(W + 1 * n * n * NE * n * 2 + wo);   // w02 w11
+          const double2 wc = *reinterpret_cast<const double2*>(W + 2 * n * n * NE * n * 2 + wo);   // w12 w22
           const int id = sidx(e, i, jp, k);
           const double d0 = p0[i][k], d1 = s_s[id], d2 = p2[i][k];
-          p0[i][k] = w00 * d0 + w01 * d1 + w02 * d2;
-          s_s[id] = w01 * d0 + w11 * d1 + w12 * d2;
-          p2[i][k] = w02 * d0 + w12 * d1 + w22 * d2;
+          p0[i][k] = wa.x * d0 + wa.y * d1 + wb.x * d2;
+          s_s[id] = wa.y * d0 + wb.y * d1 + wc.x * d2;
+          p2[i][k] = wb.x * d0 + wc.x * d1 + wc.y * d2;
         }
       // weak xi (columns of p0, in place): p0[i][k] <- -sum_a D[a][i] f_xi[a][k]
 #pragma unroll
@@ -265,6 +296,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         }
     }
     __syncthreads();
+    if (tid == 0 && l + 1 < nlay) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
+      fence_proxy_async();
+      issue_metric(l + 1);
+    }
     // ---- d: eta lines weak, in place (line i = jp of element e)
     if (act) {
 #pragma unroll
@@ -300,30 +335,49 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = 0.0;
     }
     __syncthreads();
-    // ---- f: node owners sum the element copies; final values / partial rows
+    // ---- f: node owners sum the element copies (all F fields per item); whole-row stores
     {
       const int kmax = (l == nlay - 1) ? n : N;
-      for (int it = tid; it < C::SQ; it += C::NT) {
-        const int node = it / F;            // = uv * n + k, field = it % F == f
+#pragma unroll
+      for (int it = 0; it < C::PN; ++it) {
+        const int node = tid + it * C::NT;   // = uv * n + k
+        if (node >= C::NODES) break;
         const int k = node % n, uv = node / n;
         if (k >= kmax) continue;
         const int g = s_g[node];
         if (g < 0) continue;
         const int4 ct = s_ct[uv];
-        const int kof = k * F + f;
-        double val = s_s[ct.x + kof];
-        if (ct.y >= 0) val += s_s[ct.y + kof];
-        if (ct.z >= 0) val += s_s[ct.z + kof] + s_s[ct.w + kof];
-        const int cd = code_t[uv];
+        const int kof = k * F;
+        double val[F];
+#pragma unroll
+        for (int p = 0; p < F; ++p) {
+          double a = s_s[ct.x + kof + p];
+          if (ct.y >= 0) a += s_s[ct.y + kof + p];
+          if (ct.z >= 0) a += s_s[ct.z + kof + p] + s_s[ct.w + kof + p];
+          val[p] = a;
+        }
+        const int cd = s_code[uv];
         if (cd < 0) {
           double* o = A.out + (int64_t)g * A.ldo;
-          const double r = A.scale * (s_mi[node] * val);
-          o[ocol] = A.accumulate ? o[ocol] + r : r;
-          if (f == 0 && A.zero_mask && !A.accumulate)
-            for (int zc = 0; zc < A.ldo; ++zc)
-              if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+          const double m = A.scale * s_mi[node];
+          if (A.accumulate) {
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[ocol[p]] += m * val[p];
+          } else if (row5) {
+            o[0] = 0.0;
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[1 + p] = m * val[p];
+          } else {
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[ocol[p]] = m * val[p];
+            if (A.zero_mask)
+              for (int zc = 0; zc < A.ldo; ++zc)
+                if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+          }
         } else {
-          A.part[((int64_t)cd * A.n_z + l * N + k) * 5 + f] = val;
+          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5;
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[p] = val[p];
         }
       }
     }
@@ -361,7 +415,8 @@ __global__ void plane_fixup(TileArgs A, int64_t nslot) {
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
 }
 
-// Plane-layout packed metric: Wp[t][l][c][i][k][e][j] = W[c][elem(t,l,e)*n^3 + (i*n + j)*n + k].
+// Plane-layout packed metric, component pairs:
+// Wp[t][l][cp][i][k][e][j][h] = W[2cp+h][elem(t,l,e)*n^3 + (i*n + j)*n + k].
 __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const int32_t* __restrict__ elem,
                                   const double* __restrict__ W, int64_t nloc, double* __restrict__ Wp) {
   const int64_t per = (int64_t)6 * n * n * NE * n;
@@ -369,11 +424,12 @@ __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tl = id / per;
     int64_t r = id % per;
+    const int h = (int)(r % 2); r /= 2;
     const int j = (int)(r % n); r /= n;
     const int e = (int)(r % NE); r /= NE;
     const int k = (int)(r % n); r /= n;
     const int i = (int)(r % n); r /= n;
-    const int c = (int)r;
+    const int c = (int)r * 2 + h;
     const int eg = elem[tl * NE + e];
     Wp[id] = (eg >= 0) ? W[c * nloc + (int64_t)eg * n * n * n + (i * n + j) * n + k] : 0.0;
   }
@@ -401,15 +457,15 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
 namespace hv {
 
 bool plane_supported(int N, int TX, int TY, int F) {
-  return (F == 1 || F == 4 || F == 5) && TX == 4 && TY == 2 && N >= 1 && N <= 4;
+  return (F == 1 || F == 4 || F == 5) && TX == 2 && TY == 2 && N >= 1 && N <= 4;
 }
 
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st) {
 #define HV_PLANE_CASE(NN_)                                        \
   if (N == NN_) {                                                 \
-    if (F == 1) return run_plane<NN_ + 1, 4, 2, 1>(A, Drow, st);  \
-    if (F == 4) return run_plane<NN_ + 1, 4, 2, 4>(A, Drow, st);  \
-    if (F == 5) return run_plane<NN_ + 1, 4, 2, 5>(A, Drow, st);  \
+    if (F == 1) return run_plane<NN_ + 1, 2, 2, 1>(A, Drow, st);  \
+    if (F == 4) return run_plane<NN_ + 1, 2, 2, 4>(A, Drow, st);  \
+    if (F == 5) return run_plane<NN_ + 1, 2, 2, 5>(A, Drow, st);  \
   }
   HV_PLANE_CASE(1)
   HV_PLANE_CASE(2)

@@ -100,9 +100,11 @@ class EulerOps:
                 torch = torch_mod()
                 tp, d = ta
                 Wt = torch.empty(tp.ntiles * tp.nlay * 6 * n * tp.NE * n * n, dtype=torch.float64, device="cuda")
+                layout = 1 if (os.environ.get("HV_KERNEL", "") == "plane" and dev.N <= 4) else 0
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
-                                                          d["elem"].data_ptr(), W.data_ptr(), dev.nloc,
+                                                          d["elem"].data_ptr(), W.data_ptr(), dev.nloc, layout,
                                                           Wt.data_ptr(), _lib.stream_handle()))
+                p.kernel = layout
                 p.TX, p.TY, p.nlay, p.n_z = tp.TX, tp.TY, tp.nlay, tp.n_z
                 p.ntiles, p.nslot = tp.ntiles, tp.nslot
                 p.d_gt, p.d_code, p.d_tmeta = d["gt"].data_ptr(), d["code"].data_ptr(), d["tmeta"].data_ptr()

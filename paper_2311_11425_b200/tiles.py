@@ -23,12 +23,7 @@ __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 def tile_shape(N, F=4):
     """(TX, TY) of the compiled sweep kernels: 2x2 columns for the line kernel
-    (lap_tile.cu), 2x1 for N = 7.  HV_KERNEL=plane selects the experimental
-    plane-owner kernel (lap_plane.cu, 4x2 tiles, N <= 4)."""
-    import os
-
-    if N <= 4 and os.environ.get("HV_KERNEL", "") == "plane":
-        return (4, 2)
+    (lap_tile.cu) and the plane-owner kernel (lap_plane.cu), 2x1 for N = 7."""
     return (2, 1) if N == 7 else (2, 2)
 
 
