@@ -119,6 +119,14 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::GTS;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
   const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
+  int qcol[F], ocol[F];
+#pragma unroll
+  for (int p = 0; p < F; ++p) {
+    qcol[p] = A.qf.f[p];
+    ocol[p] = A.of.f[p];
+  }
+  const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
+  const bool q_contig = (F == 4 && A.ldq == 4 && qcol[0] == 0 && qcol[1] == 1 && qcol[2] == 2 && qcol[3] == 3);
   // element-private scratch index (this thread's field); tile-node index
   auto sidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
   auto tq = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
@@ -136,15 +144,22 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
                  : "memory");
     tma_copy(s_w, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + 1);
   };
-  // async gather of one layer of q: lanes (node, f) with f fastest, so 4 consecutive lanes
-  // fill one node's 32 contiguous bytes of s_q (conflict-free) and read one row
-  const int qc = A.qf.f[f], oc = A.of.f[f];
+  // node-granular async gather of one layer of q (all F fields of a node per item)
   auto issue_gather = [&](const int* g_src) {
-    for (int node = tid / F; node < C::NODES; node += C::NT / F) {
+    for (int node = tid; node < C::NODES; node += C::NT) {
       const int g = g_src[node];
-      double* dst = s_q + node * F + f;
-      if (g < 0) *dst = 0.0;
-      else cp_async8(dst, A.q + (int64_t)g * A.ldq + qc);
+      double* dst = s_q + node * F;
+      if (g < 0) {
+#pragma unroll
+        for (int p = 0; p < F; ++p) dst[p] = 0.0;
+      } else if (q_contig) {
+        cp_async16cg(dst, A.q + (int64_t)g * 4);
+        cp_async16cg(dst + 2, A.q + (int64_t)g * 4 + 2);
+      } else {
+        const double* src = A.q + (int64_t)g * A.ldq;
+#pragma unroll
+        for (int p = 0; p < F; ++p) cp_async8(dst + p, src + qcol[p]);
+      }
     }
     cp_async_commit();
   };
@@ -320,33 +335,49 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = 0.0;
     }
     __syncthreads();
-    // ---- f: node owners sum the element copies; lanes (node, f), f fastest
+    // ---- f: node owners sum the element copies (all F fields per item); whole-row stores
     {
       const int kmax = (l == nlay - 1) ? n : N;
-      for (int node = tid / F; node < C::NODES; node += C::NT / F) {   // node = uv * n + k
+#pragma unroll
+      for (int it = 0; it < C::PN; ++it) {
+        const int node = tid + it * C::NT;   // = uv * n + k
+        if (node >= C::NODES) break;
         const int k = node % n, uv = node / n;
         if (k >= kmax) continue;
         const int g = s_g[node];
         if (g < 0) continue;
         const int4 ct = s_ct[uv];
-        const int kof = k * F + f;
-        double val = s_s[ct.x + kof];
-        if (ct.y >= 0) val += s_s[ct.y + kof];
-        if (ct.z >= 0) val += s_s[ct.z + kof] + s_s[ct.w + kof];
+        const int kof = k * F;
+        double val[F];
+#pragma unroll
+        for (int p = 0; p < F; ++p) {
+          double a = s_s[ct.x + kof + p];
+          if (ct.y >= 0) a += s_s[ct.y + kof + p];
+          if (ct.z >= 0) a += s_s[ct.z + kof + p] + s_s[ct.w + kof + p];
+          val[p] = a;
+        }
         const int cd = s_code[uv];
         if (cd < 0) {
           double* o = A.out + (int64_t)g * A.ldo;
-          const double r = A.scale * (s_mi[node] * val);
+          const double m = A.scale * s_mi[node];
           if (A.accumulate) {
-            o[oc] += r;
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[ocol[p]] += m * val[p];
+          } else if (row5) {
+            o[0] = 0.0;
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[1 + p] = m * val[p];
           } else {
-            o[oc] = r;
-            if (f == 0 && A.zero_mask)
+#pragma unroll
+            for (int p = 0; p < F; ++p) o[ocol[p]] = m * val[p];
+            if (A.zero_mask)
               for (int zc = 0; zc < A.ldo; ++zc)
                 if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
           }
         } else {
-          A.part[((int64_t)cd * A.n_z + l * N + k) * 5 + f] = val;
+          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5;
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[p] = val[p];
         }
       }
     }
