@@ -88,6 +88,10 @@ struct PlaneCfg {
   static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);
 };
 
+__device__ __forceinline__ void cp_async16cg(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
 // Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
 // (w02,w11) (w12,w22)); the F field lanes of a plane broadcast one LDS.128.
 template <int n, int TX, int TY, int F, int MB>
@@ -123,15 +127,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   }
   const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
   const bool q_contig = (F == 4 && A.ldq == 4 && qcol[0] == 0 && qcol[1] == 1 && qcol[2] == 2 && qcol[3] == 3);
-  // node records of F doubles; for F = 4 the field slot is XOR-swizzled with bits 2-3 of the
-  // record index so that node-granular lanes (consecutive records) are bank-conflict free
-  auto sw = [](int rec, int p) {
-    if constexpr (F == 4) return rec * 4 + (p ^ ((rec >> 2) & 3));
-    else return rec * F + p;
-  };
   // element-private scratch index (this thread's field); tile-node index
-  auto sidx = [&](int ee, int a, int b, int c) { return sw(((ee * n + a) * n + b) * n + c, f); };
-  auto tq = [&](int u, int v, int k) { return sw((u * V + v) * n + k, f); };
+  auto sidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
+  auto tq = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
 
   auto issue_stage = [&](int l) {       // Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3] on bar[0]
     const int b = l & 1;
@@ -150,13 +148,17 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   auto issue_gather = [&](const int* g_src) {
     for (int node = tid; node < C::NODES; node += C::NT) {
       const int g = g_src[node];
+      double* dst = s_q + node * F;
       if (g < 0) {
 #pragma unroll
-        for (int p = 0; p < F; ++p) s_q[sw(node, p)] = 0.0;
+        for (int p = 0; p < F; ++p) dst[p] = 0.0;
+      } else if (q_contig) {
+        cp_async16cg(dst, A.q + (int64_t)g * 4);
+        cp_async16cg(dst + 2, A.q + (int64_t)g * 4 + 2);
       } else {
         const double* src = A.q + (int64_t)g * A.ldq;
 #pragma unroll
-        for (int p = 0; p < F; ++p) cp_async8(s_q + sw(node, p), src + qcol[p]);
+        for (int p = 0; p < F; ++p) cp_async8(dst + p, src + qcol[p]);
       }
     }
     cp_async_commit();
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
     int o[4] = {-1, -1, -1, -1}, c = 0;
     for (int a = pu0; a <= pu1; ++a)
-      for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n;
+      for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n * F;
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
     s_code[uv] = A.code[t * UV + uv];
   }
@@ -345,12 +347,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         const int g = s_g[node];
         if (g < 0) continue;
         const int4 ct = s_ct[uv];
+        const int kof = k * F;
         double val[F];
 #pragma unroll
         for (int p = 0; p < F; ++p) {
-          double a = s_s[sw(ct.x + k, p)];
-          if (ct.y >= 0) a += s_s[sw(ct.y + k, p)];
-          if (ct.z >= 0) a += s_s[sw(ct.z + k, p)] + s_s[sw(ct.w + k, p)];
+          double a = s_s[ct.x + kof + p];
+          if (ct.y >= 0) a += s_s[ct.y + kof + p];
+          if (ct.z >= 0) a += s_s[ct.z + kof + p] + s_s[ct.w + kof + p];
           val[p] = a;
         }
         const int cd = s_code[uv];
