@@ -100,7 +100,9 @@ class EulerOps:
                 torch = torch_mod()
                 tp, d = ta
                 Wt = torch.empty(tp.ntiles * tp.nlay * 6 * n * tp.NE * n * n, dtype=torch.float64, device="cuda")
-                layout = 1 if (os.environ.get("HV_KERNEL", "") == "plane" and dev.N <= 4) else 0
+                # plane-owner kernel (lap_plane.cu) for N <= 4, line-tile kernel otherwise;
+                # HV_KERNEL=line forces the line-tile kernel (cross-checks)
+                layout = 1 if (os.environ.get("HV_KERNEL", "") != "line" and dev.N <= 4) else 0
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
                                                           d["elem"].data_ptr(), W.data_ptr(), dev.nloc, layout,
                                                           Wt.data_ptr(), _lib.stream_handle()))
