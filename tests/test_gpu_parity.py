@@ -144,16 +144,27 @@ def test_tile_path_used_and_matches_element_path(pair):
     name, p, o = pair
     from paper_2311_11425_b200 import euler, hyperdiff, state
 
+    import os
+
     assert p.ops._tile_arrays() is not None, "tile plan rejected"
     ops_v1 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
     ops_v1._h["tiles"] = None
-    a = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
-    b = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, ops_v1)
-    assert rel_l2(a, b) <= 1e-14
+    os.environ["HV_KERNEL"] = "line"          # the line-tile kernel (default is plane-owner for N <= 4)
+    try:
+        ops_line = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+        ops_line.lap_plan(p.vm)
+    finally:
+        del os.environ["HV_KERNEL"]
+    st = state.StateField("2C", o.state)
+    a = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops)
+    b = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops_v1)
+    c = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops_line)
+    assert rel_l2(a, b) <= 1e-14 and rel_l2(c, b) <= 1e-14
     for f in range(1, 5):
         la = hyperdiff.laplacian_apply(o.state[:, f], p.vm, p.ops)
         lb = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops_v1)
-        assert rel_l2(la, lb) <= 1e-14
+        lc = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops_line)
+        assert rel_l2(la, lb) <= 1e-14 and rel_l2(lc, lb) <= 1e-14
 
 
 def test_all_five_fields_one_pass(pair):
