@@ -88,6 +88,15 @@ int hv_mass_and_projection(int N, const double* d_w3, const double* d_J, const d
                            const int64_t* d_off, const int32_t* d_idx, int64_t nglobal, double* d_M,
                            double* d_Minv, double* d_Jg, double* d_gz, void* stream);
 
+/* The same two reductions split for the multi-GPU slab decomposition: raw
+ * flat-order sums per node d_S (nglobal, 5) = [sum w3 J, sum (w3 J) J,
+ * sum (w3 J) grad_zeta_c] (the host adds the neighbours' interface sums in
+ * rank order), then M = S0, Minv = 1/M, Jg = S1/M, gz = S2..4/M (d_Jg nullable). */
+int hv_mass_proj_sums(int N, const double* d_w3, const double* d_J, const double* d_grad, int64_t nelem,
+                      const int64_t* d_off, const int32_t* d_idx, int64_t nglobal, double* d_S, void* stream);
+int hv_mass_proj_finalize(int64_t nglobal, const double* d_S, double* d_M, double* d_Minv, double* d_Jg, double* d_gz,
+                          void* stream);
+
 /* build_viscous_metric (hyperdiff.py:54-81) fused with the packing of the
  * Laplacian metric W = w3 * Jg[gid] * G_nu (6 unique components).
  * mode 0 = scaled: nu_m*vals_m = ((a_m * lam_m) / b) * vals_m with host-computed
@@ -129,7 +138,27 @@ typedef struct hv_lap_plan {
   const double* d_Mt;          /* Minv in tile order (ntiles, nlay, MTS)              */
   double* d_part;              /* partial rows (rows, n_z, 5)                         */
   int kernel;                  /* 0: line-tile kernel (lap_tile.cu), 1: plane-owner kernel (lap_plane.cu) */
+  /* multi-GPU slab interface (parallel.py); d_slot_ext == NULL on one GPU */
+  const int32_t* d_slot_ext;   /* (nslot) -1 or side*face + jf, side 0 = lower rank, 1 = upper   */
+  const int32_t* d_ext_slots;  /* (next) slots with d_slot_ext >= 0                             */
+  int64_t next;
+  int face;                    /* column nodes per slab face                                   */
+  double* d_send;              /* (2*face, n_z, 5) local interface sums (NCCL send payload)    */
+  double* d_recv;              /* (2*face, n_z, 5) neighbour sums (NCCL receive buffer)        */
 } hv_lap_plan;
+
+/* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the
+ * neighbour exchange of d_send -> d_recv in between, ncclSend/ncclRecv):
+ *   hv_lap_local : tile sweep; final values for tile-owned nodes, partial rows
+ *                  for shared ones, local interface sums packed into d_send;
+ *   hv_lap_finish: fixed-order sums of the shared nodes (interface: lower rank
+ *                  first), times scale * Minv, into out.
+ * Same argument meaning as hv_laplacian; zero_mask lists out columns to zero,
+ * accumulate != 0 adds into out. */
+int hv_lap_local(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf, double* d_out,
+                 int64_t ldo, const int32_t* h_of, double scale, uint32_t zero_mask, int accumulate, void* stream);
+int hv_lap_finish(const hv_lap_plan* plan, double* d_out, int64_t ldo, int nf, const int32_t* h_of, double scale,
+                  uint32_t zero_mask, int accumulate, void* stream);
 
 /* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
  * (layout 0: line-tile kernel, [t][l][pair][k][e][i*n+j][2]; layout 1: plane kernel,

@@ -59,6 +59,12 @@ class LapPlan(C.Structure):
         ("d_Mt", _P),
         ("d_part", _P),
         ("kernel", C.c_int),
+        ("d_slot_ext", _P),
+        ("d_ext_slots", _P),
+        ("next", _I64),
+        ("face", C.c_int),
+        ("d_send", _P),
+        ("d_recv", _P),
     ]
 
 
@@ -74,10 +80,15 @@ _SIGS = {
     "hv_metric_terms": (C.c_int, [C.c_int, C.c_int, _P, _P, _I64, _P, _P, _P, _P]),
     "hv_dss_csr": (C.c_int, [_P, C.c_int, _I64, _P, _P, _I64, _P, _P]),
     "hv_mass_and_projection": (C.c_int, [C.c_int, _P, _P, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "hv_mass_proj_sums": (C.c_int, [C.c_int, _P, _P, _P, _I64, _P, _P, _I64, _P, _P]),
+    "hv_mass_proj_finalize": (C.c_int, [_I64, _P, _P, _P, _P, _P, _P]),
     "hv_viscous_metric": (C.c_int, [C.c_int, C.c_int, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
     "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, C.c_int, _P, _P]),
+    "hv_lap_local": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, C.c_uint32, C.c_int,
+                               _P]),
+    "hv_lap_finish": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _D, C.c_uint32, C.c_int, _P]),
     "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, C.c_int, _P]),
     "hv_euler_setup": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P]),
     "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, _P,

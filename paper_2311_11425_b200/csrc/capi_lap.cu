@@ -25,20 +25,52 @@ int check_plan(const hv_lap_plan* P) {
   return HV_OK;
 }
 
-// Run one Laplacian pass with the best available kernel for this plan.
+hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const hv::FieldMap& qf, double* out,
+                       int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, int accumulate) {
+  hv::TileArgs A{};
+  A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
+  A.ntiles = P->ntiles; A.nslot = P->nslot;
+  A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
+  A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
+  A.Wt = P->d_Wt; A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
+  A.zero_mask = zero_mask; A.accumulate = accumulate; A.scale = scale; A.out = out; A.part = P->d_part;
+  A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
+  A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
+  return A;
+}
+
+bool use_plane(const hv_lap_plan* P, int nf) {
+  return P->d_gt && P->d_Mt && P->kernel == 1 && hv::plane_supported(P->N, P->TX, P->TY, nf);
+}
+bool use_tiles(const hv_lap_plan* P, int nf) {
+  return use_plane(P, nf) || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf));
+}
+
+// tile sweep + packing of the interface sums (no-op on one GPU)
+int lap_local(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
+              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st, int accumulate) {
+  const hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
+  const int rc = use_plane(P, nf) ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
+  if (rc) return rc;
+  return hv::slot_pack(A, nf, st);
+}
+
+int lap_finish(const hv_lap_plan* P, int nf, double* out, int64_t ldo, const hv::FieldMap& of, double scale,
+               unsigned zero_mask, cudaStream_t st, int accumulate) {
+  const hv::TileArgs A = tile_args(P, nullptr, 0, hv::FieldMap{}, out, ldo, of, scale, zero_mask, accumulate);
+  return hv::slot_fixup(A, nf, st);
+}
+
+// Run one whole Laplacian pass (single GPU) with the best available kernel for this plan.
 int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st,
              int accumulate = 0) {
-  const bool plane = P->d_gt && P->d_Mt && P->kernel == 1 && hv::plane_supported(P->N, P->TX, P->TY, nf);
-  if (plane || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf))) {
-    hv::TileArgs A{};
-    A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
-    A.ntiles = P->ntiles; A.nslot = P->nslot;
-    A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
-    A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
-    A.Wt = P->d_Wt; A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
-    A.zero_mask = zero_mask; A.accumulate = accumulate; A.scale = scale; A.out = out; A.part = P->d_part;
-    return plane ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
+  if (use_tiles(P, nf)) {
+    if (P->d_slot_ext && P->next > 0)
+      HV_FAIL(HV_ERR_INVALID, "multi-GPU plan: use hv_lap_local / exchange / hv_lap_finish");
+    int rc = lap_local(P, q, ldq, nf, qf, out, ldo, of, scale, zero_mask, st, accumulate);
+    if (rc) return rc;
+    return lap_finish(P, nf, out, ldo, of, scale, zero_mask, st, accumulate);
   }
   if (zero_mask && !accumulate) {
     const int64_t tot = P->nglobal * ldo;
@@ -46,6 +78,20 @@ int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const h
     HV_LAUNCH_CHECK();
   }
   return hv::laplacian_v1(P, q, ldq, nf, qf, out, ldo, of, scale, accumulate, st);
+}
+
+int field_maps(int nf, const int32_t* h_qf, int64_t ldq, const int32_t* h_of, int64_t ldo, hv::FieldMap& qf,
+               hv::FieldMap& of) {
+  if (nf < 1 || nf > 5 || !h_of || ldo < 1) HV_FAIL(HV_ERR_INVALID, "bad field map");
+  for (int f = 0; f < nf; ++f) {
+    if (h_of[f] < 0 || h_of[f] >= ldo) HV_FAIL(HV_ERR_INVALID, "output field index out of range");
+    of.f[f] = h_of[f];
+    if (h_qf) {
+      if (h_qf[f] < 0 || h_qf[f] >= ldq) HV_FAIL(HV_ERR_INVALID, "input field index out of range");
+      qf.f[f] = h_qf[f];
+    }
+  }
+  return HV_OK;
 }
 
 }  // namespace
@@ -63,6 +109,28 @@ extern "C" int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* 
                                  double* d_Mt, void* stream) {
   if (rows <= 0 || gts <= 0 || mts <= 0 || !d_gt || !d_Minv || !d_Mt) HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_minv: bad args");
   return hv::tile_pack_minv(rows, gts, mts, d_gt, d_Minv, d_Mt, (cudaStream_t)stream);
+}
+
+extern "C" int hv_lap_local(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,
+                            double* d_out, int64_t ldo, const int32_t* h_of, double scale, uint32_t zero_mask,
+                            int accumulate, void* stream) {
+  int rc = check_plan(P);
+  if (rc) return rc;
+  hv::FieldMap qf{}, of{};
+  if ((rc = field_maps(nf, h_qf, ldq, h_of, ldo, qf, of))) return rc;
+  if (!h_qf || !d_q || !d_out) HV_FAIL(HV_ERR_INVALID, "hv_lap_local: null argument");
+  if (!use_tiles(P, nf)) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_lap_local needs a tile plan");
+  return lap_local(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, zero_mask, (cudaStream_t)stream, accumulate);
+}
+
+extern "C" int hv_lap_finish(const hv_lap_plan* P, double* d_out, int64_t ldo, int nf, const int32_t* h_of,
+                             double scale, uint32_t zero_mask, int accumulate, void* stream) {
+  int rc = check_plan(P);
+  if (rc) return rc;
+  hv::FieldMap qf{}, of{};
+  if ((rc = field_maps(nf, nullptr, 0, h_of, ldo, qf, of))) return rc;
+  if (!d_out) HV_FAIL(HV_ERR_INVALID, "hv_lap_finish: null output");
+  return lap_finish(P, nf, d_out, ldo, of, scale, zero_mask, (cudaStream_t)stream, accumulate);
 }
 
 extern "C" int hv_laplacian(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,

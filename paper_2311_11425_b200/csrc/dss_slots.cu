@@ -1,0 +1,116 @@
+// Off-chip part of the DSS for the tile-sweep kernels: column nodes shared by
+// several tiles ("slots", tiles.py) and, with several GPUs, slab-interface
+// column nodes shared with a neighbouring rank (parallel.py).
+//
+// slot_pack   per interface slot and level: the fixed-order sum of the local
+//             partial rows -> the send buffer of that side (ncclSend payload).
+// slot_fixup  per slot and level: the fixed-order sum of the local partial rows,
+//             plus the neighbour's sum (received) in global rank order
+//             (lower rank first) so both ranks produce bitwise identical values;
+//             times scale * Minv, written to the output row (reference DSS
+//             semantics, assembly.py:17-26 and hyperdiff.py:94).
+#include <cuda_runtime.h>
+
+#include "hv_common.h"
+#include "lap_common.cuh"
+#include "lap_tile.cuh"
+
+namespace {
+
+using hv::TileArgs;
+
+template <int F>
+__device__ __forceinline__ void local_sum(const TileArgs& A, int64_t s, int z, double acc[F]) {
+  const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
+  for (int r = 0; r < nc; ++r) {
+    const double* p = A.part + ((int64_t)(r0 + r) * A.n_z + z) * 5;
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) acc[ff] += p[ff];
+  }
+}
+
+template <int F>
+__global__ void slot_pack_kernel(TileArgs A) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= A.next * A.n_z) return;
+  const int64_t s = A.ext_slots[id / A.n_z];
+  const int z = (int)(id % A.n_z);
+  double acc[F];
+  local_sum<F>(A, s, z, acc);
+  double* o = A.send + ((int64_t)A.slot_ext[s] * A.n_z + z) * 5;
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) o[ff] = acc[ff];
+}
+
+template <int F>
+__global__ void slot_fixup_kernel(TileArgs A) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= A.nslot * A.n_z) return;
+  const int64_t s = id / A.n_z;
+  const int z = (int)(id % A.n_z);
+  const int c = A.slot_col[s];
+  const int g = A.col_gid[(int64_t)c * A.n_z + z];
+  double acc[F];
+  local_sum<F>(A, s, z, acc);
+  if (A.slot_ext && A.slot_ext[s] >= 0) {
+    const int ext = A.slot_ext[s];
+    const double* rm = A.recv + ((int64_t)ext * A.n_z + z) * 5;
+    const bool lower_side = ext < A.face;   // side 0: the neighbour has the lower rank
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) acc[ff] = lower_side ? rm[ff] + acc[ff] : acc[ff] + rm[ff];
+  }
+  double* o = A.out + (int64_t)g * A.ldo;
+  const double mi = A.Minv[g];
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) {
+    const double r = A.scale * (mi * acc[ff]);
+    o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r : r;
+  }
+  if (A.zero_mask && !A.accumulate)
+    for (int zc = 0; zc < A.ldo; ++zc)
+      if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+}
+
+template <int F>
+int pack_f(const TileArgs& A, cudaStream_t st) {
+  if (A.next <= 0) return HV_OK;
+  const int64_t tot = A.next * A.n_z;
+  slot_pack_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+template <int F>
+int fixup_f(const TileArgs& A, cudaStream_t st) {
+  if (A.nslot <= 0) return HV_OK;
+  const int64_t tot = A.nslot * A.n_z;
+  slot_fixup_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+}  // namespace
+
+namespace hv {
+
+int slot_pack(const TileArgs& A, int F, cudaStream_t st) {
+  switch (F) {
+    case 1: return pack_f<1>(A, st);
+    case 4: return pack_f<4>(A, st);
+    case 5: return pack_f<5>(A, st);
+    default: HV_FAIL(HV_ERR_UNSUPPORTED, "slot_pack: F=%d", F);
+  }
+}
+
+int slot_fixup(const TileArgs& A, int F, cudaStream_t st) {
+  switch (F) {
+    case 1: return fixup_f<1>(A, st);
+    case 4: return fixup_f<4>(A, st);
+    case 5: return fixup_f<5>(A, st);
+    default: HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: F=%d", F);
+  }
+}
+
+}  // namespace hv

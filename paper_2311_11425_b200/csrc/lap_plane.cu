@@ -385,35 +385,6 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   }
 }
 
-// fixed-order perimeter fix-up (same as lap_tile.cu, one thread per (slot, level))
-template <int F>
-__global__ void plane_fixup(TileArgs A, int64_t nslot) {
-  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (id >= nslot * A.n_z) return;
-  const int64_t s = id / A.n_z;
-  const int z = (int)(id % A.n_z);
-  const int c = A.slot_col[s];
-  const int g = A.col_gid[(int64_t)c * A.n_z + z];
-  const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
-  double acc[F];
-#pragma unroll
-  for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
-  for (int r = 0; r < nc; ++r) {
-    const double* p = A.part + ((int64_t)(r0 + r) * A.n_z + z) * 5;
-#pragma unroll
-    for (int ff = 0; ff < F; ++ff) acc[ff] += p[ff];
-  }
-  double* o = A.out + (int64_t)g * A.ldo;
-  const double mi = A.Minv[g];
-#pragma unroll
-  for (int ff = 0; ff < F; ++ff) {
-    const double r = A.scale * (mi * acc[ff]);
-    o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r : r;
-  }
-  if (A.zero_mask && !A.accumulate)
-    for (int zc = 0; zc < A.ldo; ++zc)
-      if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
-}
 
 // Plane-layout packed metric, component pairs:
 // Wp[t][l][cp][i][k][e][j][h] = W[2cp+h][elem(t,l,e)*n^3 + (i*n + j)*n + k].
@@ -444,11 +415,6 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
-  if (A.nslot > 0) {
-    const int64_t tot = A.nslot * A.n_z;
-    plane_fixup<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, A.nslot);
-    HV_LAUNCH_CHECK();
-  }
   return HV_OK;
 }
 

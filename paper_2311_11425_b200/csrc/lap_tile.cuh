@@ -27,9 +27,18 @@ struct TileArgs {
   double scale;
   double* out;
   double* part;             // (rows, n_z, 5)
+  // slab-interface slots (multi-GPU, parallel.py); slot_ext == nullptr on one GPU
+  const int32_t* slot_ext;  // (nslot) -1, or side * face + jf  (side 0: lower rank, 1: upper rank)
+  const int32_t* ext_slots; // (next) slots with slot_ext >= 0
+  int64_t next;
+  int face;                 // column nodes per slab face
+  double* send;             // (2 * face, n_z, 5) local sums for the neighbours
+  const double* recv;       // (2 * face, n_z, 5) neighbours' sums
 };
 
 bool tile_supported(int N, int TX, int TY, int F);
+int slot_pack(const TileArgs& A, int F, cudaStream_t st);
+int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,

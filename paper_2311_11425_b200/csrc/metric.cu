@@ -104,6 +104,49 @@ __global__ void mass_proj_kernel(int nn, const double* __restrict__ w3, const do
   }
 }
 
+// Raw flat-order sums per node: [sum w3J, sum (w3J)J, sum (w3J) gz_c] (the numerators of
+// GlobalMass / project_metrics_to_columns before any cross-rank addition).
+__global__ void mass_proj_sums_kernel(int nn, const double* __restrict__ w3, const double* __restrict__ J,
+                                      const double* __restrict__ grad, const int64_t* __restrict__ off,
+                                      const int32_t* __restrict__ idx, int64_t ng, double* __restrict__ S) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  double m = 0.0, sj = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t o = off[g]; o < off[g + 1]; ++o) {
+    const int64_t p = idx[o];
+    const int64_t e = p / nn, r = p % nn;
+    const double Jp = J[p];
+    const double wj = __dmul_rn(w3[r], Jp);
+    m = __dadd_rn(m, wj);
+    sj = __dadd_rn(sj, __dmul_rn(wj, Jp));
+    const double* gze = grad + (e * 9 + 6) * nn + r;
+    s0 = __dadd_rn(s0, __dmul_rn(wj, gze[0]));
+    s1 = __dadd_rn(s1, __dmul_rn(wj, gze[nn]));
+    s2 = __dadd_rn(s2, __dmul_rn(wj, gze[2 * nn]));
+  }
+  S[g * 5 + 0] = m;
+  S[g * 5 + 1] = sj;
+  S[g * 5 + 2] = s0;
+  S[g * 5 + 3] = s1;
+  S[g * 5 + 4] = s2;
+}
+
+__global__ void mass_proj_finalize_kernel(int64_t ng, const double* __restrict__ S, double* __restrict__ M,
+                                          double* __restrict__ Minv, double* __restrict__ Jg, double* __restrict__ gz) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const double m = S[g * 5];
+  M[g] = m;
+  Minv[g] = __ddiv_rn(1.0, m);
+  if (!(m > 0.0)) atomicOr(&g_setup_flags[2], 1u);
+  if (m == 0.0) atomicOr(&g_setup_flags[3], 1u);
+  if (Jg) {
+    Jg[g] = __ddiv_rn(S[g * 5 + 1], m);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) gz[g * 3 + c] = __ddiv_rn(S[g * 5 + 2 + c], m);
+  }
+}
+
 // Cyclic Jacobi eigensolver for a symmetric 3x3 matrix; eigenvalues ascending,
 // V columns = eigenvectors (LAPACK dsyevd's convention for ordering; signs and
 // degenerate-eigenspace bases are arbitrary, the reference only relies on
@@ -347,5 +390,33 @@ extern "C" int hv_viscous_metric(int N, int mode, const double* h_a, double b, c
   rc = read_flags(st, f);
   if (rc) return rc;
   if (f[1]) HV_FAIL(HV_ERR_DEGENERATE, "degenerate element: non-positive metric eigenvalue");
+  return HV_OK;
+}
+
+extern "C" int hv_mass_proj_sums(int N, const double* d_w3, const double* d_J, const double* d_grad, int64_t nelem,
+                                 const int64_t* d_off, const int32_t* d_idx, int64_t nglobal, double* d_S, void* stream) {
+  if (N < 1 || !d_w3 || !d_J || !d_grad || !d_off || !d_idx || !d_S || nelem <= 0 || nglobal <= 0)
+    HV_FAIL(HV_ERR_INVALID, "hv_mass_proj_sums: bad args");
+  const int n = N + 1, nn = n * n * n, T = 256;
+  mass_proj_sums_kernel<<<(unsigned)((nglobal + T - 1) / T), T, 0, (cudaStream_t)stream>>>(nn, d_w3, d_J, d_grad, d_off,
+                                                                                         d_idx, nglobal, d_S);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+extern "C" int hv_mass_proj_finalize(int64_t nglobal, const double* d_S, double* d_M, double* d_Minv, double* d_Jg,
+                                     double* d_gz, void* stream) {
+  if (nglobal <= 0 || !d_S || !d_M || !d_Minv || (d_Jg && !d_gz)) HV_FAIL(HV_ERR_INVALID, "hv_mass_proj_finalize: bad args");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = reset_flags(st);
+  if (rc) return rc;
+  const int T = 256;
+  mass_proj_finalize_kernel<<<(unsigned)((nglobal + T - 1) / T), T, 0, st>>>(nglobal, d_S, d_M, d_Minv, d_Jg, d_gz);
+  HV_LAUNCH_CHECK();
+  unsigned int f[4];
+  rc = read_flags(st, f);
+  if (rc) return rc;
+  if (d_Jg && f[3]) HV_FAIL(HV_ERR_DEGENERATE, "zero mass-matrix entry in projection");
+  if (f[2]) HV_FAIL(HV_ERR_DEGENERATE, "non-positive mass-matrix entry (inverted element?)");
   return HV_OK;
 }

@@ -21,7 +21,9 @@ __all__ = ["EulerOps"]
 class EulerOps:
     """euler.py:27-35: mesh, metrics, constants, equation set, optional (cfg, viscous)."""
 
-    def __init__(self, mesh, mets, constants, set_name, hyper=None):
+    def __init__(self, mesh, mets, constants, set_name, hyper=None, mass=None, ext_cols=None):
+        """``mass`` / ``ext_cols``: supplied by the multi-GPU slab decomposition (parallel.py):
+        the cross-rank mass and the slab-interface column nodes."""
         if set_name not in ("2NC", "2C", "3C"):
             raise ValueError(f"unknown equation set {set_name!r}")
         self.mesh = mesh
@@ -29,7 +31,10 @@ class EulerOps:
         self.c = constants
         self.set_name = set_name
         self.hyper = hyper
-        self.mass = GlobalMass(mesh, mets.d_J)
+        self.mass = mass if mass is not None else GlobalMass(mesh, mets.d_J)
+        self.ext_cols = ext_cols
+        self.ext_face = 0
+        self.halo = None
         self.w3 = weights3(mesh)
         self._plans = {}
         self._work = None
@@ -60,12 +65,13 @@ class EulerOps:
             dev = self.mesh.device()
             tp = None
             if os.environ.get("HV_DISABLE_TILES", "0") != "1" and dev.N <= 7:
-                tp = build_tile_plan(self.mesh, *tile_shape(dev.N))
+                tp = build_tile_plan(self.mesh, *tile_shape(dev.N), ext_cols=self.ext_cols)
             if tp is None:
                 self._h["tiles"] = None
             else:
                 torch = torch_mod()
-                d = {k: to_dev(getattr(tp, k)) for k in ("gt", "code", "tmeta", "slot_col", "slot_row0", "slot_nc")}
+                d = {k: to_dev(getattr(tp, k)) for k in ("gt", "code", "tmeta", "slot_col", "slot_row0", "slot_nc",
+                                                         "slot_ext", "ext_slots")}
                 d["elem"] = to_dev(tp.elem.reshape(tp.ntiles, tp.nlay, -1).astype(np.int32))
                 d["col_gid"] = to_dev(self.mesh.col_gid.astype(np.int32))
                 d["part"] = torch.empty(max(1, tp.npart) * tp.n_z * 5, dtype=torch.float64, device="cuda")
@@ -118,6 +124,15 @@ class EulerOps:
                                                         _lib.stream_handle()))
                 p.d_Wt, p.d_Mt, p.d_part = Wt.data_ptr(), Mt.data_ptr(), d["part"].data_ptr()
                 keep += [Wt, Mt]
+                if self.ext_cols:
+                    face = self.ext_face
+                    p.d_slot_ext, p.d_ext_slots = d["slot_ext"].data_ptr(), d["ext_slots"].data_ptr()
+                    p.next, p.face = len(tp.ext_slots), face
+                    send = torch.zeros((2, face, tp.n_z, 5), dtype=torch.float64, device="cuda")
+                    recv = torch.zeros_like(send)
+                    p.d_send, p.d_recv = send.data_ptr(), recv.data_ptr()
+                    self.halo = (send, recv)
+                    keep += [send, recv]
             self._plans[key] = (p, keep)
         return self._plans[key][0]
 

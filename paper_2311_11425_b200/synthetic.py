@@ -40,12 +40,15 @@ STATE_SEED = 1
 
 
 # ------------------------------------------------------------------ geometry
-def perturbed_box_coords(nx, ny, nv, N, extents, frac=0.1, seed=GEOM_SEED, perturb=True):
+def perturbed_box_coords(nx, ny, nv, N, extents, frac=0.1, seed=GEOM_SEED, perturb=True, ia_range=None):
     """Trilinear map of a (optionally) perturbed vertex lattice to LGL nodes.
 
     Element order e = (ia*ny + ib)*nv + l, the box order of mesh.py:246-257
-    generalised to nx != ny.  Returns coords (nelem,3,n,n,n), elem_layer,
-    elem_hcol.
+    generalised to nx != ny.  ``ia_range = (ia0, ia1)`` generates only the
+    x-slab ia0 <= ia < ia1 of the same global lattice (multi-GPU slabs: the
+    vertex perturbation is drawn for the whole lattice, so every rank sees the
+    same bits on a shared face); its elements are numbered locally.
+    Returns coords (nelem,3,n,n,n), elem_layer, elem_hcol.
     """
     x1 = lobatto(N).nodes
     n = N + 1
@@ -65,6 +68,10 @@ def perturbed_box_coords(nx, ny, nv, N, extents, frac=0.1, seed=GEOM_SEED, pertu
         interior = np.zeros((nx + 1, ny + 1, nv + 1), dtype=bool)
         interior[1:-1, 1:-1, 1:-1] = True
         V[interior] += d[interior]
+    if ia_range is not None:
+        ia0, ia1 = ia_range
+        V = V[ia0:ia1 + 1]
+        nx = ia1 - ia0
     s = 0.5 * (1.0 + x1)            # exact 0 and 1 at the end nodes
     S = (1.0 - s, s)
     nel = nx * ny * nv

@@ -34,7 +34,10 @@ class TilePlan:
         self.__dict__.update(kw)
 
 
-def build_tile_plan(mesh, TX, TY):
+def build_tile_plan(mesh, TX, TY, ext_cols=None):
+    """Tile plan of ``mesh``; ``ext_cols`` maps column id -> interface code
+    (side * face + jf) for column nodes also owned by a neighbouring rank
+    (parallel.py): they become slots even when a single local tile owns them."""
     N = mesh.degree
     n = N + 1
     if mesh.hgrid is None:
@@ -98,7 +101,13 @@ def build_tile_plan(mesh, TX, TY):
     m = cf >= 0
     pairs = np.unique(np.stack([cf[m], tid[m]], axis=1), axis=0)          # (col, tile) sorted by col then tile
     cnt = np.bincount(pairs[:, 0], minlength=mesh.ncol)
-    shared_cols = np.nonzero(cnt >= 2)[0]
+    is_ext = np.zeros(mesh.ncol, dtype=bool)
+    ext_code = np.full(mesh.ncol, -1, dtype=np.int64)
+    if ext_cols:
+        kk = np.fromiter(ext_cols.keys(), dtype=np.int64)
+        is_ext[kk] = True
+        ext_code[kk] = np.fromiter(ext_cols.values(), dtype=np.int64)
+    shared_cols = np.nonzero((cnt >= 2) | (is_ext & (cnt >= 1)))[0]
     nslot = len(shared_cols)
     slot_of_col = np.full(mesh.ncol, -1, dtype=np.int64)
     slot_of_col[shared_cols] = np.arange(nslot)
@@ -125,7 +134,10 @@ def build_tile_plan(mesh, TX, TY):
     mts = (nodes + 1) & ~1
     gtp = np.full((nt, nlay, gts), -1, dtype=np.int32)
     gtp[:, :, :nodes] = gt.reshape(nt, nlay, nodes)
+    slot_ext = ext_code[shared_cols].astype(np.int32)
+    ext_slots = np.nonzero(slot_ext >= 0)[0].astype(np.int32)
     return TilePlan(N=N, n=n, TX=TX, TY=TY, U=U, V=V, NE=NE, nlay=nlay, ntiles=nt, tiles=tiles, elem=elem,
+                    slot_ext=slot_ext, ext_slots=ext_slots,
                     gt=gtp, gts=gts, mts=mts, nodes=nodes, code=code.astype(np.int32), nslot=nslot,
                     slot_col=shared_cols.astype(np.int32), slot_row0=slot_row0.astype(np.int32),
                     slot_nc=slot_nc.astype(np.int32), npart=npart, n_z=mesh.n_z,
