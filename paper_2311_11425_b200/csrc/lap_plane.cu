@@ -126,6 +126,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     ocol[p] = A.of.f[p];
   }
   const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
+  const bool q_contig = (F == 4 && A.ldq == 4 && qcol[0] == 0 && qcol[1] == 1 && qcol[2] == 2 && qcol[3] == 3);
   // element-private scratch index (this thread's field); tile-node index
   auto sidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
   auto tq = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
@@ -143,23 +144,21 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
                  : "memory");
     tma_copy(s_w, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + 1);
   };
-  // async gather of one layer of q: lanes (node, field) with the field fastest, so consecutive
-  // lanes fill consecutive 8-byte slots of s_q (conflict-free) and read one state row per node
-  const bool qf_contig = [&] {
-    bool c = true;
-#pragma unroll
-    for (int p = 1; p < F; ++p) c = c && (qcol[p] == qcol[0] + p);
-    return c;
-  }();
+  // node-granular async gather of one layer of q (all F fields of a node per item)
   auto issue_gather = [&](const int* g_src) {
-    for (int it = tid; it < C::SQ; it += C::NT) {
-      const int node = it / F, p = it % F;
+    for (int node = tid; node < C::NODES; node += C::NT) {
       const int g = g_src[node];
+      double* dst = s_q + node * F;
       if (g < 0) {
-        s_q[it] = 0.0;
+#pragma unroll
+        for (int p = 0; p < F; ++p) dst[p] = 0.0;
+      } else if (q_contig) {
+        cp_async16cg(dst, A.q + (int64_t)g * 4);
+        cp_async16cg(dst + 2, A.q + (int64_t)g * 4 + 2);
       } else {
-        const int col = qf_contig ? qcol[0] + p : A.qf.f[p];
-        cp_async8(s_q + it, A.q + (int64_t)g * A.ldq + col);
+        const double* src = A.q + (int64_t)g * A.ldq;
+#pragma unroll
+        for (int p = 0; p < F; ++p) cp_async8(dst + p, src + qcol[p]);
       }
     }
     cp_async_commit();
