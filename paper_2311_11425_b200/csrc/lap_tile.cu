@@ -529,7 +529,7 @@ namespace hv {
 
 bool tile_supported(int N, int TX, int TY, int F) {
   if (F != 1 && F != 4 && F != 5) return false;
-  if (N == 7) return TX == 2 && TY == 1;
+  if (N == 7) return TX == 1 && TY == 1;
   return N >= 1 && N <= 6 && TX == 2 && TY == 2;
 }
 
@@ -546,7 +546,7 @@ int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStre
   HV_TILE_CASE(4, 2, 2)
   HV_TILE_CASE(5, 2, 2)
   HV_TILE_CASE(6, 2, 2)
-  HV_TILE_CASE(7, 2, 1)
+  HV_TILE_CASE(7, 1, 1)
 #undef HV_TILE_CASE
   HV_FAIL(HV_ERR_UNSUPPORTED, "tile kernel: no instantiation for N=%d TX=%d TY=%d F=%d", N, A.TX, A.TY, F);
 }

@@ -23,8 +23,9 @@ __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 def tile_shape(N, F=4):
     """(TX, TY) of the compiled sweep kernels: 2x2 columns for the line kernel
-    (lap_tile.cu) and the plane-owner kernel (lap_plane.cu), 2x1 for N = 7."""
-    return (2, 1) if N == 7 else (2, 2)
+    (lap_tile.cu) and the plane-owner kernel (lap_plane.cu); single columns for N = 7
+    (the 6-component metric of an N = 7 element is 24.6 KB: 1x1 tiles keep two CTAs per SM)."""
+    return (1, 1) if N == 7 else (2, 2)
 
 
 class TilePlan:
