@@ -394,7 +394,42 @@ def run_ours(args, rank, world, local):
 
     peak, peak_kind, _ = _peaks()
     alg = algorithmic_bytes_hnu(ng, nloc)
-    achieved = alg / (ms * 1e-3) / 1e9
+    achieved_op = alg / (ms * 1e-3) / 1e9
+    # dominant kernel alone: the tile sweep of one pass (pass 1, q -> L q), CUDA events on its stream
+    kern_ms, kern_name, traffic = None, None, None
+    if world == 1 and getattr(ops, "_plans", None):
+        import ctypes as C
+
+        plan = ops.lap_plan(vm)
+        if plan.d_gt:
+            nv_ = len(cfg.variables)
+            y = torch.empty((ng, nv_), dtype=torch.float64, device="cuda")
+            qa = (C.c_int32 * nv_)(*cfg.variables)
+            oa = (C.c_int32 * nv_)(*range(nv_))
+            L = _lib.lib()
+
+            def one_pass():
+                _lib.check(L.hv_lap_local(C.byref(plan), qd.data_ptr(), 5, nv_, qa, y.data_ptr(), nv_, oa, 1.0, 0, 0,
+                                          _lib.stream_handle()))
+
+            for _ in range(3):
+                one_pass()
+            torch.cuda.synchronize()
+            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nk = max(5, args.steps)
+            k0.record(stream)
+            for _ in range(nk):
+                one_pass()
+            k1.record(stream)
+            torch.cuda.synchronize()
+            kern_ms = k0.elapsed_time(k1) / nk
+            kern_name = "lap_plane_kernel" if plan.kernel == 1 else "lap_tile_kernel"
+            prof = ROOT / "profiles" / "r01_dominant_kernel.json"
+            if prof.exists():
+                traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            del y
+    alg_launch = alg / 2                       # one pass = one sweep launch
+    achieved = alg_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else achieved_op
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -420,9 +455,14 @@ def run_ours(args, rank, world, local):
                        "parallelism": (f"x-slabs x{world} of a ({w.nx}*{world})x{w.ny}x{w.nv} box, slab-face "
                                        "DSS over NCCL p2p" if world > 1 else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": None, "algorithmic_bytes_per_op": alg,
-                         "scope": "whole H_nu op (all kernels of the alpha=2 passes)"},
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
+                         "kernel": kern_name, "kernel_ms_per_launch": kern_ms,
+                         "algorithmic_bytes_per_launch": alg_launch, "algorithmic_bytes_per_op": alg,
+                         "op_achieved": achieved_op, "op_frac": achieved_op / peak,
+                         "kernel_share_of_step": (2 * kern_ms / ms) if kern_ms else None,
+                         "scope": "dominant kernel = tile sweep of one Laplacian pass (2 per H_nu op); "
+                                  "op_* = whole op incl. perimeter fix-ups; traffic = ncu dram bytes per "
+                                  "launch (profiles/r01_dominant_kernel.json)"},
             "cpu_baseline": cpu,
             "e2e": {"value": dof / (ms_e2e * 1e-3), "unit": "DOF-updates/s",
                     "h2d_bytes_per_step": ng * 5 * 8, "d2h_bytes_per_step": ng * 5 * 8,
