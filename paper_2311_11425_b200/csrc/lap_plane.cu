@@ -71,8 +71,14 @@ struct PlaneCfg {
   static constexpr int NODES = UV * n;
   static constexpr int GTS = (NODES + 3) & ~3;
   static constexpr int MTS = (NODES + 1) & ~1;
-  static constexpr int SQ = NODES * F;
-  static constexpr int SE = NE * n * n * n * F;
+  // field-major (SoA) shared arrays; plane strides padded to 4 (mod 16 doubles) so the lanes
+  // (element, eta plane, field) of a warp spread over the banks and node-granular lanes
+  // (gather / output) are conflict-free
+  static constexpr int pad16(int x) { return x + ((4 - (x % 16)) + 16) % 16; }
+  static constexpr int QP = pad16(NODES);                // s_q field-plane stride
+  static constexpr int SP = pad16(NE * n * n * n);       // scratch field-plane stride
+  static constexpr int SQ = QP * F;
+  static constexpr int SE = SP * F;
   static constexpr int WL = 6 * n * NE * n * n;          // packed metric doubles per tile-layer
   static constexpr int PN = (NODES + NT - 1) / NT;       // node items per thread
   // shared memory (doubles): q | W | scratch | Minv[2] | gid[3] (ints) | ctab (int4) | code | mbarrier[2]
@@ -87,10 +93,6 @@ struct PlaneCfg {
   static constexpr int BY_SMEM = (int)((227 * 1024) / (SMEM + 1024));
   static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);
 };
-
-__device__ __forceinline__ void cp_async16cg(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
 
 // Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
 // (w02,w11) (w12,w22)); the F field lanes of a plane broadcast one LDS.128.
@@ -126,10 +128,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     ocol[p] = A.of.f[p];
   }
   const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
-  const bool q_contig = (F == 4 && A.ldq == 4 && qcol[0] == 0 && qcol[1] == 1 && qcol[2] == 2 && qcol[3] == 3);
-  // element-private scratch index (this thread's field); tile-node index
-  auto sidx = [&](int ee, int a, int b, int c) { return (((ee * n + a) * n + b) * n + c) * F + f; };
-  auto tq = [&](int u, int v, int k) { return ((u * V + v) * n + k) * F + f; };
+  // element-private scratch index (this thread's field); tile-node index (field-major planes)
+  auto sidx = [&](int ee, int a, int b, int c) { return f * C::SP + ((ee * n + a) * n + b) * n + c; };
+  auto tq = [&](int u, int v, int k) { return f * C::QP + (u * V + v) * n + k; };
 
   auto issue_stage = [&](int l) {       // Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3] on bar[0]
     const int b = l & 1;
@@ -148,17 +149,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
   auto issue_gather = [&](const int* g_src) {
     for (int node = tid; node < C::NODES; node += C::NT) {
       const int g = g_src[node];
-      double* dst = s_q + node * F;
       if (g < 0) {
 #pragma unroll
-        for (int p = 0; p < F; ++p) dst[p] = 0.0;
-      } else if (q_contig) {
-        cp_async16cg(dst, A.q + (int64_t)g * 4);
-        cp_async16cg(dst + 2, A.q + (int64_t)g * 4 + 2);
+        for (int p = 0; p < F; ++p) s_q[p * C::QP + node] = 0.0;
       } else {
         const double* src = A.q + (int64_t)g * A.ldq;
 #pragma unroll
-        for (int p = 0; p < F; ++p) cp_async8(dst + p, src + qcol[p]);
+        for (int p = 0; p < F; ++p) cp_async8(s_q + p * C::QP + node, src + qcol[p]);
       }
     }
     cp_async_commit();
@@ -176,7 +173,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
     int o[4] = {-1, -1, -1, -1}, c = 0;
     for (int a = pu0; a <= pu1; ++a)
-      for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n * F;
+      for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n;
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
     s_code[uv] = A.code[t * UV + uv];
   }
@@ -347,13 +344,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         const int g = s_g[node];
         if (g < 0) continue;
         const int4 ct = s_ct[uv];
-        const int kof = k * F;
         double val[F];
 #pragma unroll
         for (int p = 0; p < F; ++p) {
-          double a = s_s[ct.x + kof + p];
-          if (ct.y >= 0) a += s_s[ct.y + kof + p];
-          if (ct.z >= 0) a += s_s[ct.z + kof + p] + s_s[ct.w + kof + p];
+          const double* sp = s_s + p * C::SP + k;
+          double a = sp[ct.x];
+          if (ct.y >= 0) a += sp[ct.y];
+          if (ct.z >= 0) a += sp[ct.z] + sp[ct.w];
           val[p] = a;
         }
         const int cd = s_code[uv];
