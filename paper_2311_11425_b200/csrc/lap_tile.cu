@@ -27,6 +27,9 @@
 
 #include <cstdlib>
 
+#ifndef HV_FP2_MAXN
+#define HV_FP2_MAXN 8   // two fields per thread below this n (N = 7 uses one: more warps per SM)
+#endif
 #ifndef HV_ABLATE
 #define HV_ABLATE 0   // timing experiments only: bit 1 skip S1, 2 skip W1, 4 skip O, 8 skip P
 #endif
@@ -82,7 +85,6 @@ struct TileCfg {
   static constexpr int SQ = NODES * F;
   static constexpr int SE = NE * n * n * n * F;
   static constexpr int WL = 6 * n * NE * NN;             // packed metric doubles per tile-layer
-  static constexpr int PQ = (NODES * FL + NT - 1) / NT;  // (node, lane) items per thread
   static constexpr int PN = (NODES + NT - 1) / NT;       // node items per thread (gather / output)
   static constexpr int UV = U * V;
   // shared memory (doubles): q | W[WB] | a | b | Minv[2] | gid[3] (ints) | ctab (ints) | mbarrier[2]
@@ -112,14 +114,6 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// one elected thread: expect `bytes` on the barrier and start the bulk copy global -> shared
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 __device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -512,7 +506,7 @@ __global__ void tile_pack_minv_kernel(int64_t rows, int gts, int mts, const int3
 
 template <int n, int TX, int TY, int F>
 int run_tile(const TileArgs& A, const double* Drow, cudaStream_t st) {
-  constexpr int FP = (F % 2 == 0) ? 2 : 1;
+  constexpr int FP = (F % 2 == 0 && n < HV_FP2_MAXN) ? 2 : 1;
   using C = TileCfg<n, TX, TY, F, FP>;
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
