@@ -203,6 +203,17 @@ int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int coriolis, d
                  const double* d_q, int64_t ldq, double* d_work, double* d_out, int64_t ldo, int accumulate,
                  void* stream);
 
+/* V(q), the vertical (zeta) operator of the HEVI split, column by column
+ * (EulerOps.rhs_vertical / column_apply / _col_acc, euler.py:61-94,138-144,231-272):
+ * per column of d_col_gid (ncol, n_z) int32 the layer accumulators, the zeta DSS
+ * along the column and the division by the column mass DSS(w_z J).  h_w: the
+ * (N+1) zeta quadrature weights.  out (nglobal, ldo) gets the 5 tendencies of
+ * every gridpoint (accumulate != 0: added). */
+int hv_euler_vertical(int N, const double* h_D, const double* h_w, int set_id, double P_A, double R, double gamma,
+                      int64_t ncol, int nlay, int n_z, const int32_t* d_col_gid, const double* d_Jg,
+                      const double* d_gz, const double* d_mask_g, const double* d_Phi_g, const double* d_q,
+                      int64_t ldq, double* d_out, int64_t ldo, int accumulate, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -315,3 +315,147 @@ extern "C" int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int 
   return hv::dss_minv_accumulate(d_work, nelem * n * n * n, d_off, d_idx, d_Minv, nglobal, d_out, ldo, 5,
                                  accumulate != 0, st);
 }
+
+// ---------------------------------------------------------------------------
+// V(q): the vertical (zeta) operator evaluated column by column
+// (EulerOps.rhs_vertical / column_apply / _col_acc, euler.py:61-94,138-144,231-272).
+// One thread per column walks its layers bottom to top with the layer's zeta
+// line in registers; the shared node between layers is summed as the
+// reference's _col_assemble does (previous top first), then divided by the
+// column mass DSS(w_z J).
+namespace {
+
+template <int n>
+__global__ void euler_vertical_kernel(hv::DTab<n> Dt, EulerConsts K, hv::DTab<n> Wz, int64_t ncol, int nlay, int n_z,
+                                      const int32_t* __restrict__ col_gid, const double* __restrict__ Jg,
+                                      const double* __restrict__ gz, const double* __restrict__ mask_g,
+                                      const double* __restrict__ Phi_g, const double* __restrict__ q, int64_t ldq,
+                                      double* __restrict__ out, int64_t ldo, int accumulate) {
+  constexpr int N = n - 1;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= ncol) return;
+  const int32_t* cg = col_gid + c * (int64_t)n_z;
+  double carry[5] = {0, 0, 0, 0, 0}, carry_m = 0.0;
+  auto emit = [&](int g, const double* a, double m) {
+    double* o = out + (int64_t)g * ldo;
+#pragma unroll
+    for (int f = 0; f < 5; ++f) o[f] = accumulate ? o[f] + a[f] / m : a[f] / m;
+  };
+  for (int l = 0; l < nlay; ++l) {
+    int g[n];
+    double qv[n][5], J[n], z[n][3], msk[n], phi[n], P[n], uz[n], tf[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      g[i] = cg[l * N + i];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) qv[i][f] = q[(int64_t)g[i] * ldq + f];
+      J[i] = Jg[g[i]];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) z[i][d] = gz[(int64_t)g[i] * 3 + d];
+      msk[i] = mask_g[g[i]];
+      phi[i] = Phi_g[g[i]];
+      const double rho = qv[i][0];
+      if (K.set == 0) {
+        P[i] = K.P_A * pow(qv[i][0] * K.R * qv[i][4] / K.P_A, K.gamma);
+        uz[i] = msk[i] * (qv[i][1] * z[i][0] + qv[i][2] * z[i][1] + qv[i][3] * z[i][2]);
+        tf[i] = 0.0;
+      } else {
+        if (K.set == 1) {
+          P[i] = K.P_A * pow(K.R * qv[i][4] / K.P_A, K.gamma);
+        } else {
+          const double ke = 0.5 * (qv[i][1] * qv[i][1] + qv[i][2] * qv[i][2] + qv[i][3] * qv[i][3]) / rho;
+          P[i] = (K.gamma - 1.0) * (qv[i][4] - ke - rho * phi[i]);
+        }
+        uz[i] = msk[i] * (qv[i][1] * z[i][0] + qv[i][2] * z[i][1] + qv[i][3] * z[i][2]) / rho;
+        tf[i] = (K.set == 1) ? qv[i][4] / rho : (qv[i][4] + P[i]) / rho;
+      }
+    }
+    double acc[n][5], ms[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const double wj = Wz.D[0][i] * J[i];
+      ms[i] = wj;
+      double dphi = 0.0;
+#pragma unroll
+      for (int a = 0; a < n; ++a) dphi += Dt.D[i][a] * phi[a];
+      if (K.set == 0) {
+        double a0 = 0.0, dP = 0.0, du[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < n; ++a) {
+          a0 += Dt.D[a][i] * (Wz.D[0][a] * (J[a] * qv[a][0] * uz[a]));
+          dP += Dt.D[i][a] * P[a];
+#pragma unroll
+          for (int f = 0; f < 4; ++f) du[f] += Dt.D[i][a] * qv[a][1 + f];
+        }
+        acc[i][0] = a0;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+          acc[i][1 + cc] = -wj * (uz[i] * du[cc] + (z[i][cc] / qv[i][0]) * dP + z[i][cc] * dphi);
+        acc[i][4] = -wj * uz[i] * du[3];
+      } else {
+        double a0 = 0.0, a4 = 0.0, dm[3] = {0, 0, 0};
+#pragma unroll
+        for (int a = 0; a < n; ++a) {
+          const double jru = J[a] * qv[a][0] * uz[a];
+          a0 += Dt.D[a][i] * (Wz.D[0][a] * jru);
+          a4 += Dt.D[a][i] * (Wz.D[0][a] * (jru * tf[a]));
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) dm[cc] += Dt.D[i][a] * (J[a] * (qv[a][1 + cc] * uz[a] + P[a] * z[a][cc]));
+        }
+        acc[i][0] = a0;
+        acc[i][4] = a4;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) acc[i][1 + cc] = -Wz.D[0][i] * dm[cc] - wj * qv[i][0] * dphi * z[i][cc];
+      }
+    }
+    // column DSS: node 0 of this layer is node N of the previous one
+    if (l > 0) {
+#pragma unroll
+      for (int f = 0; f < 5; ++f) acc[0][f] = carry[f] + acc[0][f];
+      ms[0] = carry_m + ms[0];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) emit(g[i], acc[i], ms[i]);
+#pragma unroll
+    for (int f = 0; f < 5; ++f) carry[f] = acc[N][f];
+    carry_m = ms[N];
+    if (l == nlay - 1) emit(g[N], acc[N], ms[N]);
+  }
+}
+
+template <int n>
+int run_vertical(const double* Drow, const double* w, const EulerConsts& K, int64_t ncol, int nlay, int n_z,
+                 const int32_t* col_gid, const double* Jg, const double* gz, const double* mask, const double* Phi,
+                 const double* q, int64_t ldq, double* out, int64_t ldo, int accumulate, cudaStream_t st) {
+  hv::DTab<n> Dt, Wz{};
+  hv::fill_dtab(Dt, Drow);
+  for (int i = 0; i < n; ++i) Wz.D[0][i] = w[i];
+  const int T = 128;
+  euler_vertical_kernel<n><<<(unsigned)((ncol + T - 1) / T), T, 0, st>>>(Dt, K, Wz, ncol, nlay, n_z, col_gid, Jg, gz,
+                                                                         mask, Phi, q, ldq, out, ldo, accumulate);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+}  // namespace
+
+extern "C" int hv_euler_vertical(int N, const double* h_D, const double* h_w, int set_id, double P_A, double R,
+                                 double gamma, int64_t ncol, int nlay, int n_z, const int32_t* d_col_gid,
+                                 const double* d_Jg, const double* d_gz, const double* d_mask_g,
+                                 const double* d_Phi_g, const double* d_q, int64_t ldq, double* d_out, int64_t ldo,
+                                 int accumulate, void* stream) {
+  if (N < 1 || N > 7 || !h_D || !h_w || set_id < 0 || set_id > 2 || ncol <= 0 || nlay <= 0 || n_z != nlay * N + 1 ||
+      !d_col_gid || !d_Jg || !d_gz || !d_mask_g || !d_Phi_g || !d_q || !d_out || ldq < 5 || ldo < 5)
+    HV_FAIL(HV_ERR_INVALID, "hv_euler_vertical: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  EulerConsts K{P_A, R, gamma, 0.0, set_id, 4, 0};
+  switch (N + 1) {
+    case 2: return run_vertical<2>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    case 3: return run_vertical<3>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    case 4: return run_vertical<4>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    case 5: return run_vertical<5>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    case 6: return run_vertical<6>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    case 7: return run_vertical<7>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+    default: return run_vertical<8>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
+  }
+}

@@ -219,6 +219,30 @@ class EulerOps:
         hyperdiffusion_apply(StateField(self.set_name, qd), cfg, viscous, self, out=o, accumulate=True)
         return o.cpu().numpy() if host else o
 
-    def rhs_vertical(self, state):
-        """V(q) column operator (euler.py:138-144): SURVEY §8(f) 'next', not in this build."""
-        raise NotImplementedError("rhs_vertical (column operator) is the next component, see DESIGN.md §8")
+    def _column_arrays(self):
+        if "cols" not in self._h:
+            phi = to_dev(np.ascontiguousarray(self.Phi_g, dtype=np.float64))
+            mask = to_dev(np.ascontiguousarray(self.mesh.flux_mask, dtype=np.float64))
+            cg = to_dev(np.ascontiguousarray(self.mesh.col_gid, dtype=np.int32))
+            self._h["cols"] = (cg, mask, phi)
+        return self._h["cols"]
+
+    def rhs_vertical(self, state, out=None, accumulate=False):
+        """V(q) assembled from the independent column evaluations (euler.py:138-144, 231-272)."""
+        from .hyperdiff import _as_device
+
+        torch = torch_mod()
+        data = state.data if hasattr(state, "data") else state
+        q, host = _as_device(data)
+        dev = self.mesh.device()
+        cg, mask, phi = self._column_arrays()
+        if out is None:
+            out = torch.empty_like(q)
+        wz = np.ascontiguousarray(self.mesh.bases[2].weights, dtype=np.float64)
+        k = self.c
+        _lib.check(_lib.lib().hv_euler_vertical(
+            dev.N, dev.D.ctypes.data, wz.ctypes.data, self._SETS[self.set_name], k.P_A, k.R, k.gamma,
+            self.mesh.ncol, self.mesh.cfg.n_elem_vertical, self.mesh.n_z, cg.data_ptr(), self.metrics.d_Jg.data_ptr(),
+            self.metrics.d_gz.data_ptr(), mask.data_ptr(), phi.data_ptr(), q.data_ptr(), 5, out.data_ptr(), 5,
+            int(bool(accumulate)), _lib.stream_handle()))
+        return out.cpu().numpy() if host else out

@@ -86,6 +86,7 @@ def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, l
         rs = random_state(m.nglobal, s, seed=7)
         out[f"rhs_full_{s}"] = o.rhs_full(rstate.StateField(s, rs))
         out[f"rhs_h_{s}"] = o.rhs_horizontal(rstate.StateField(s, rs), with_hyperdiff=False)
+        out[f"rhs_v_{s}"] = o.rhs_vertical(rstate.StateField(s, rs))
     if store_full:
         out["gid"] = m.gid.astype(np.int32)
         out["Jg"] = mets.Jg

@@ -212,3 +212,22 @@ def test_rhs_full_plus_hyperdiffusion(pair):
     ref_h = oe.rhs_horizontal_nohd(rs) + o.hyper(rs)
     got_h = ops.rhs_horizontal(state.StateField(s, rs), with_hyperdiff=True)
     assert rel_l2(got_h, ref_h) <= TOL
+
+
+def test_rhs_vertical_and_splitting(pair):
+    """V(q) per column vs the oracle and the reference goldens; H + V == S with omega = 0."""
+    name, p, o = pair
+    from cases import random_state
+    from paper_2311_11425_b200 import euler, state
+
+    g = golden(name)
+    for s in p.c["sets"]:
+        ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
+        rs = random_state(p.m.nglobal, s)
+        v = ops.rhs_vertical(state.StateField(s, rs))
+        assert rel_l2(v, o.euler(s).rhs_vertical(rs)) <= TOL, (s, rel_l2(v, o.euler(s).rhs_vertical(rs)))
+        assert rel_l2(v, g[f"rhs_v_{s}"]) <= TOL
+        if p.c["omega"] == 0.0:
+            h = ops.rhs_horizontal(state.StateField(s, rs), with_hyperdiff=False)
+            full = ops.rhs_full(state.StateField(s, rs))
+            assert rel_l2(h + v, full) <= 1e-12   # splitting completeness (SPEC.md:292)

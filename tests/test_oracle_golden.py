@@ -77,3 +77,4 @@ def test_rhs_bitwise(prob):
         rs = random_state(p.m.ng, s)
         assert np.array_equal(e.rhs_full(rs), g[f"rhs_full_{s}"]), s
         assert np.array_equal(e.rhs_horizontal_nohd(rs), g[f"rhs_h_{s}"]), s
+        assert np.array_equal(e.rhs_vertical(rs), g[f"rhs_v_{s}"]), s
