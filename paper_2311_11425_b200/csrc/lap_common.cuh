@@ -6,6 +6,12 @@
 
 namespace hv {
 
+template <int F>
+struct Vec {
+  double v[F];
+};
+
+
 // (n x n) LGL derivative matrix passed by value (kernel-parameter constant bank,
 // broadcast to every thread): D[i][a] = d psi_a / d xi at node i (basis.py:77-87).
 template <int n>

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#define HV_PLANE_ABLATE 1
 
 #include "hv_common.h"
 #include "lap_common.cuh"
@@ -62,7 +63,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-template <int n, int TX, int TY, int F>
+__device__ __forceinline__ void st_v2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ double2 ldg_stream2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+// WV: where the packed metric comes from in step c.
+//   0  TMA bulk copy of the tile-layer block into shared memory (mbarrier)
+//   1  straight from global memory (L2-prefetched one layer ahead), no shared staging
+template <int n, int TX, int TY, int F, int WV>
 struct PlaneCfg {
   static constexpr int N = n - 1;
   static constexpr int U = TX * N + 1, V = TY * N + 1, UV = U * V;
@@ -71,48 +84,57 @@ struct PlaneCfg {
   static constexpr int NODES = UV * n;
   static constexpr int GTS = (NODES + 3) & ~3;
   static constexpr int MTS = (NODES + 1) & ~1;
-  // field-major (SoA) shared arrays; plane strides padded to 4 (mod 16 doubles) so the lanes
-  // (element, eta plane, field) of a warp spread over the banks and node-granular lanes
-  // (gather / output) are conflict-free
+  // field-major (SoA) shared arrays with padded strides.  For the production shape (n = 5,
+  // 2x2 tiles, thread order (jp, e, f)) the strides come from an exhaustive bank-conflict
+  // search (ablate/bank_search.py): every plane / eta-line access of a half-warp then hits
+  // 16 distinct 8-byte banks.  Other shapes use the plain padded layout.
+  static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2);
   static constexpr int pad16(int x) { return x + ((4 - (x % 16)) + 16) % 16; }
-  static constexpr int QP = pad16(NODES);                // s_q field-plane stride
-  static constexpr int SP = pad16(NE * n * n * n);       // scratch field-plane stride
+  static constexpr int KS = n;                                   // node column (k) stride
+  static constexpr int US = TUNED ? 46 : V * n;                  // u stride of s_q
+  static constexpr int QP = TUNED ? 415 : pad16(NODES);          // s_q field-plane stride
+  static constexpr int BS = n;                                   // scratch: [f][e][a][b][c]
+  static constexpr int AS = TUNED ? 28 : n * n;
+  static constexpr int ES = TUNED ? 147 : n * n * n;
+  static constexpr int SP = TUNED ? 588 : pad16(NE * n * n * n);
   static constexpr int SQ = QP * F;
   static constexpr int SE = SP * F;
   static constexpr int WL = 6 * n * NE * n * n;          // packed metric doubles per tile-layer
-  static constexpr int PN = (NODES + NT - 1) / NT;       // node items per thread
-  // shared memory (doubles): q | W | scratch | Minv[2] | gid[3] (ints) | ctab (int4) | code | mbarrier[2]
+  static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
+  static constexpr int FI = UV * N;                      // output items per layer (k < N)
+  static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
+  // shared memory (doubles): q | W (WV 0) | scratch | ctab (int4) | code | mbarrier
   static constexpr int OFF_W = (SQ + 1) & ~1;
-  static constexpr int OFF_S = OFF_W + WL;
-  static constexpr int OFF_M = OFF_S + SE;
-  static constexpr int OFF_G = OFF_M + 2 * MTS;
-  static constexpr int OFF_T = OFF_G + 3 * GTS / 2;
+  static constexpr int OFF_S = OFF_W + (WV == 0 ? WL : 0);
+  static constexpr int OFF_T = (OFF_S + SE + 1) & ~1;
   static constexpr int OFF_C = OFF_T + 2 * UV;
-  static constexpr int OFF_BAR = OFF_C + (UV + 1) / 2 + 1;
+  static constexpr int OFF_BAR = (OFF_C + (UV + 1) / 2 + 1) & ~1;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
-  static constexpr int BY_SMEM = (int)((227 * 1024) / (SMEM + 1024));
-  static constexpr int MINB = BY_SMEM >= 3 ? 3 : (BY_SMEM >= 2 ? 2 : 1);
 };
 
 // Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
-// (w02,w11) (w12,w22)); the F field lanes of a plane broadcast one LDS.128.
-template <int n, int TX, int TY, int F, int MB>
-__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
-  using C = PlaneCfg<n, TX, TY, F>;
-  constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV;
+// (w02,w11) (w12,w22)); the F field lanes of a plane read one 16-byte pair together.
+//
+// Node items: thread tid handles the tile nodes tid + it*NT (it < PN) in the gather of the
+// next layer and in the final node-owner step; their gids live in registers (loaded one
+// layer ahead, coalesced from the tile-ordered map), Minv is read coalesced at step e.
+// AB: ablation bit mask for development timing only (0 in production): 1 = no node-owner
+// step (f), 2 = no q gather, 4 = no metric TMA, 8 = no plane arithmetic (steps b-e)
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0>
+__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
+  using C = PlaneCfg<n, TX, TY, F, WV>;
+  constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF;
   extern __shared__ __align__(16) double sm[];
-  double* s_q = sm;                                    // [NODES][F]
-  double* s_w = sm + C::OFF_W;                         // metric of the current layer (TMA)
-  double* s_s = sm + C::OFF_S;                         // [NE][n i][n j][n k][F] eta scratch / element acc
-  double* s_m0 = sm + C::OFF_M;                        // [2][MTS] Minv (TMA)
-  int* s_g0 = reinterpret_cast<int*>(sm + C::OFF_G);   // [3][GTS] gids (TMA)
+  double* s_q = sm;                                    // [F][QP] gathered q of the current layer
+  double* s_w = sm + C::OFF_W;                         // metric of the current layer (WV 0, TMA)
+  double* s_s = sm + C::OFF_S;                         // [F][NE][n i][n j][n k] eta scratch / element acc
   int4* s_ct = reinterpret_cast<int4*>(sm + C::OFF_T); // [UV] element-copy offsets
   int* s_code = reinterpret_cast<int*>(sm + C::OFF_C); // [UV] partial row or -1
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // [0] Minv/gid stage, [1] metric
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // metric stage (WV 0)
   const int tid = threadIdx.x;
   const int f = tid % F;
-  const int jp = (tid / F) % n;
-  const int e = tid / (F * n);
+  const int e = (tid / F) % NE;       // thread order (jp, e, f): f fastest (metric pairs broadcast)
+  const int jp = tid / (F * NE);
   const int px = e / TY, py = e % TY;
   const int64_t t = blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
@@ -128,44 +150,109 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     ocol[p] = A.of.f[p];
   }
   const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
-  // element-private scratch index (this thread's field); tile-node index (field-major planes)
-  auto sidx = [&](int ee, int a, int b, int c) { return f * C::SP + ((ee * n + a) * n + b) * n + c; };
-  auto tq = [&](int u, int v, int k) { return f * C::QP + (u * V + v) * n + k; };
+  auto sidx = [&](int ee, int a, int b, int c) { return f * C::SP + ee * C::ES + a * C::AS + b * C::BS + c; };
+  auto tq = [&](int u, int v, int k) { return f * C::QP + u * C::US + v * C::KS + k; };
+  // tile node (uv * n + k) -> s_q offset within a field plane
+  auto qnode = [&](int node) { const int uv = node / n; return (uv / V) * C::US + (uv % V) * C::KS + node % n; };
 
-  auto issue_stage = [&](int l) {       // Minv(l) -> M[l%2], gids(l+1) -> G[(l+1)%3] on bar[0]
-    const int b = l & 1;
-    const bool nextg = (l + 1 < nlay);
-    const uint32_t bytes = C::MTS * 8 + (nextg ? C::GTS * 4 : 0);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-    tma_copy(s_m0 + b * C::MTS, Mt_t + (int64_t)l * C::MTS, C::MTS * 8, bar);
-    if (nextg) tma_copy(s_g0 + ((l + 1) % 3) * C::GTS, gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4, bar);
-  };
-  auto issue_metric = [&](int l) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + 1)), "r"(C::WL * 8)
-                 : "memory");
-    tma_copy(s_w, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar + 1);
+  auto load_gids = [&](int l, int (&g)[PN]) {
+#pragma unroll
+    for (int it = 0; it < PN; ++it) {
+      const int node = tid + it * C::NT;
+      g[it] = (node < C::NODES) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
+    }
   };
   // node-granular async gather of one layer of q (all F fields of a node per item)
-  auto issue_gather = [&](const int* g_src) {
-    for (int node = tid; node < C::NODES; node += C::NT) {
-      const int g = g_src[node];
-      if (g < 0) {
+  auto issue_gather = [&](const int (&g)[PN]) {
+    if (AB & 2) return;
 #pragma unroll
-        for (int p = 0; p < F; ++p) s_q[p * C::QP + node] = 0.0;
-      } else {
-        const double* src = A.q + (int64_t)g * A.ldq;
+    for (int it = 0; it < PN; ++it) {
+      const int node = tid + it * C::NT;
+      if (node < C::NODES) {
+        if (g[it] < 0) {
 #pragma unroll
-        for (int p = 0; p < F; ++p) cp_async8(s_q + p * C::QP + node, src + qcol[p]);
+          for (int p = 0; p < F; ++p) s_q[p * C::QP + qnode(node)] = 0.0;
+        } else {
+          const double* src = A.q + (int64_t)g[it] * A.ldq;
+#pragma unroll
+          const int qo = qnode(node);
+#pragma unroll
+          for (int p = 0; p < F; ++p) cp_async8(s_q + p * C::QP + qo, src + qcol[p]);
+        }
       }
     }
     cp_async_commit();
   };
+  auto issue_metric = [&](int l) {
+    if (AB & 4) return;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(C::WL * 8)
+                 : "memory");
+    tma_copy(s_w, Wt_t + (int64_t)l * C::WL, C::WL * 8, bar);
+  };
 
-  if (tid == 0) {
+  // one output item: final value scale * Minv * sum (row store, 16-byte stores where the row
+  // alignment allows) or the raw sum into the item's partial row (perimeter slot)
+  const bool vec4 = (F == 4 && A.ldo == 4 && !A.accumulate && !A.zero_mask && ocol[0] == 0 && ocol[1] == 1 &&
+                     ocol[2] == 2 && ocol[3] == 3);
+  auto emit = [&](int g, double mi, hv::Vec<F> val, int cd, int z) {
+    if (cd < 0) {
+      double* o = A.out + (int64_t)g * A.ldo;
+      const double m = A.scale * mi;
+      if constexpr (F == 4) {
+        if (vec4) {
+          st_v2(o, m * val.v[0], m * val.v[1]);
+          st_v2(o + 2, m * val.v[2], m * val.v[3]);
+          return;
+        }
+        if (row5 && !A.accumulate) {
+          if ((g & 1) == 0) {
+            st_v2(o, 0.0, m * val.v[0]);
+            st_v2(o + 2, m * val.v[1], m * val.v[2]);
+            o[4] = m * val.v[3];
+          } else {
+            o[0] = 0.0;
+            st_v2(o + 1, m * val.v[0], m * val.v[1]);
+            st_v2(o + 3, m * val.v[2], m * val.v[3]);
+          }
+          return;
+        }
+      }
+      if (A.accumulate) {
+#pragma unroll
+        for (int p = 0; p < F; ++p) o[ocol[p]] += m * val.v[p];
+      } else {
+#pragma unroll
+        for (int p = 0; p < F; ++p) o[ocol[p]] = m * val.v[p];
+        if (A.zero_mask)
+          for (int zc = 0; zc < A.ldo; ++zc)
+            if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+      }
+    } else {
+      const int64_t r = (int64_t)cd * A.n_z + z;
+      double* o = A.part + r * 5;
+      if constexpr (F == 4) {
+        if ((r & 1) == 0) {
+          st_v2(o, val.v[0], val.v[1]);
+          st_v2(o + 2, val.v[2], val.v[3]);
+        } else {
+          o[0] = val.v[0];
+          st_v2(o + 1, val.v[1], val.v[2]);
+          o[3] = val.v[3];
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < F; ++p) o[p] = val.v[p];
+      }
+    }
+  };
+
+  int gcur[PN], gnext[PN];
+  load_gids(0, gcur);
+  if (WV == 0 && tid == 0) {
     mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
+  if (WV == 1 && tid == 0) l2_prefetch(Wt_t, C::WL * 8);
   for (int uv = tid; uv < UV; uv += C::NT) {
     const int u = uv / V, v = uv % V;
     const int pu1 = min(u / N, TX - 1), pv1 = min(v / N, TY - 1);
@@ -173,36 +260,30 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
     const int pv0 = (v % N == 0 && v > 0) ? v / N - 1 : pv1;
     int o[4] = {-1, -1, -1, -1}, c = 0;
     for (int a = pu0; a <= pu1; ++a)
-      for (int b = pv0; b <= pv1; ++b) o[c++] = (((a * TY + b) * n + (u - a * N)) * n + (v - b * N)) * n;
+      for (int b = pv0; b <= pv1; ++b) o[c++] = (a * TY + b) * C::ES + (u - a * N) * C::AS + (v - b * N) * C::BS;
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
     s_code[uv] = A.code[t * UV + uv];
   }
-  for (int node = tid; node < C::NODES; node += C::NT) s_g0[node] = gt_t[node];
+  issue_gather(gcur);
+  if (nlay > 1) load_gids(1, gnext);
   __syncthreads();
-  if (tid == 0) {
-    issue_stage(0);
-    issue_metric(0);
-  }
-  issue_gather(s_g0);
+  if (WV == 0 && tid == 0) issue_metric(0);
   double carry[n];
 #pragma unroll
   for (int i = 0; i < n; ++i) carry[i] = 0.0;
 
   for (int l = 0; l < nlay; ++l) {
-    const int b = l & 1;
-    // ---- a: q(l) and stage l have landed; start Minv / gids of l+1
+    // ---- a: q(l) has landed
     cp_async_wait_all();
-    mbar_wait(bar, (uint32_t)(l & 1));
     __syncthreads();
-    if (tid == 0 && l + 1 < nlay) {
-      fence_proxy_async();
-      issue_stage(l + 1);
+    if (WV == 1 && tid == 0 && l + 1 < nlay) l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
+    if (tid == C::NT - 1 && l + 1 < nlay) {   // output-item gid / Minv of the next layer -> L2
+      l2_prefetch(Mt_t + (int64_t)(l + 1) * C::MTS, C::MTS * 8);
+      l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
     }
-    const double* s_mi = s_m0 + b * C::MTS;
-    const int* s_g = s_g0 + (l % 3) * C::GTS;
     // ---- b: plane derivatives in registers, eta lines (i = jp) strong
     double p0[n][n], p2[n][n];   // [i][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
-    if (act) {
+    if (act && !(AB & 8)) {
 #pragma unroll
       for (int i = 0; i < n; ++i) {
         double ql[n];
@@ -247,26 +328,45 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
       }
     }
     __syncthreads();
-    // s_q of layer l is dead: gather q(l+1) (addresses arrived with stage l)
-    if (l + 1 < nlay) issue_gather(s_g0 + ((l + 1) % 3) * C::GTS);
-    // ---- c: flux at the plane nodes, weak xi / zeta in registers
-    mbar_wait(bar + 1, (uint32_t)(l & 1));
-    if (act) {
-      const double* W = s_w + (e * n + jp) * 2;
+    // s_q of layer l is dead: gather q(l+1)
+    if (l + 1 < nlay) issue_gather(gnext);
+    if (AB & 8) {
 #pragma unroll
       for (int i = 0; i < n; ++i)
 #pragma unroll
+        for (int k = 0; k < n; ++k) p0[i][k] = p2[i][k] = s_q[tq(i, jp, k)];
+    }
+    // ---- c: flux at the plane nodes, weak xi / zeta in registers
+    if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)(l & 1));
+    if (act) {
+      const double* W = (WV == 0) ? s_w + (e * n + jp) * 2 : Wt_t + (int64_t)l * C::WL + (e * n + jp) * 2;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        // all loads of the row first: one shared-memory round trip per row, not per node
+        double d1[n];
+        double2 wa[n], wb[n], wc[n];   // (w00 w01) (w02 w11) (w12 w22)
+#pragma unroll
         for (int k = 0; k < n; ++k) {
           const int wo = (i * n + k) * NE * n * 2;
-          const double2 wa = *reinterpret_cast<const double2*>(W + 0 * n * n * NE * n * 2 + wo);   // w00 w01
-          const double2 wb = *reinterpret_cast<const double2*>(W + 1 * n * n * NE * n * 2 + wo);   // w02 w11
-          const double2 wc = *reinterpret_cast<const double2*>(W + 2 * n * n * NE * n * 2 + wo);   // w12 w22
-          const int id = sidx(e, i, jp, k);
-          const double d0 = p0[i][k], d1 = s_s[id], d2 = p2[i][k];
-          p0[i][k] = wa.x * d0 + wa.y * d1 + wb.x * d2;
-          s_s[id] = wa.y * d0 + wb.y * d1 + wc.x * d2;
-          p2[i][k] = wb.x * d0 + wc.x * d1 + wc.y * d2;
+          if (WV == 0) {
+            wa[k] = *reinterpret_cast<const double2*>(W + 0 * n * n * NE * n * 2 + wo);
+            wb[k] = *reinterpret_cast<const double2*>(W + 1 * n * n * NE * n * 2 + wo);
+            wc[k] = *reinterpret_cast<const double2*>(W + 2 * n * n * NE * n * 2 + wo);
+          } else {
+            wa[k] = ldg_stream2(W + 0 * n * n * NE * n * 2 + wo);
+            wb[k] = ldg_stream2(W + 1 * n * n * NE * n * 2 + wo);
+            wc[k] = ldg_stream2(W + 2 * n * n * NE * n * 2 + wo);
+          }
+          d1[k] = s_s[sidx(e, i, jp, k)];
         }
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const double d0 = p0[i][k], d2 = p2[i][k];
+          p0[i][k] = wa[k].x * d0 + wa[k].y * d1[k] + wb[k].x * d2;
+          s_s[sidx(e, i, jp, k)] = wa[k].y * d0 + wb[k].y * d1[k] + wc[k].x * d2;
+          p2[i][k] = wb[k].x * d0 + wc[k].x * d1[k] + wc[k].y * d2;
+        }
+      }
       // weak xi (columns of p0, in place): p0[i][k] <- -sum_a D[a][i] f_xi[a][k]
 #pragma unroll
       for (int k = 0; k < n; ++k) {
@@ -293,7 +393,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         }
     }
     __syncthreads();
-    if (tid == 0 && l + 1 < nlay) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
+    if (WV == 0 && tid == 0 && l + 1 < nlay) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
       fence_proxy_async();
       issue_metric(l + 1);
     }
@@ -314,7 +414,16 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
       }
     }
     __syncthreads();
-    // ---- e: element accumulator (+ vertical carry) -> scratch
+    // ---- e: element accumulator (+ vertical carry) -> scratch; gid / Minv of the output items
+    int gf[PF];
+    double mf[PF];
+#pragma unroll
+    for (int it = 0; it < PF; ++it) {
+      const int qi = tid + it * C::NT;
+      const int node = (qi / N) * n + qi % N;
+      gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
+      mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
+    }
     if (act) {
 #pragma unroll
       for (int i = 0; i < n; ++i) {
@@ -332,52 +441,49 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F>::NT, MB) lap_plane_kern
         for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = 0.0;
     }
     __syncthreads();
-    // ---- f: node owners sum the element copies (all F fields per item); whole-row stores
-    {
-      const int kmax = (l == nlay - 1) ? n : N;
+    // ---- f: node owners (items (column, k < N); k = N only on the top layer) sum the
+    // element copies of all F fields (predicated loads, fixed order (c0 + c1) + (c2 + c3)),
+    // then one row store per item
+    if (!(AB & 1)) {
 #pragma unroll
-      for (int it = 0; it < C::PN; ++it) {
-        const int node = tid + it * C::NT;   // = uv * n + k
-        if (node >= C::NODES) break;
-        const int k = node % n, uv = node / n;
-        if (k >= kmax) continue;
-        const int g = s_g[node];
-        if (g < 0) continue;
+      for (int it = 0; it < PF; ++it) {
+        const int qi = tid + it * C::NT;
+        if (gf[it] < 0) continue;
+        const int uv = qi / N, k = qi % N;
         const int4 ct = s_ct[uv];
-        double val[F];
+        hv::Vec<F> val;
 #pragma unroll
         for (int p = 0; p < F; ++p) {
           const double* sp = s_s + p * C::SP + k;
-          double a = sp[ct.x];
-          if (ct.y >= 0) a += sp[ct.y];
-          if (ct.z >= 0) a += sp[ct.z] + sp[ct.w];
-          val[p] = a;
+          const double c0 = sp[ct.x];
+          const double c1 = (ct.y >= 0) ? sp[ct.y] : 0.0;
+          const double c2 = (ct.z >= 0) ? sp[ct.z] : 0.0;
+          const double c3 = (ct.z >= 0) ? sp[ct.w] : 0.0;
+          val.v[p] = (c0 + c1) + (c2 + c3);
         }
-        const int cd = s_code[uv];
-        if (cd < 0) {
-          double* o = A.out + (int64_t)g * A.ldo;
-          const double m = A.scale * s_mi[node];
-          if (A.accumulate) {
+        emit(gf[it], mf[it], val, s_code[uv], l * N + k);
+      }
+      if (l == nlay - 1) {        // top nodes of the columns
+        for (int uv = tid; uv < UV; uv += C::NT) {
+          const int node = uv * n + N;
+          const int g = __ldg(gt_t + (int64_t)l * C::GTS + node);
+          if (g < 0) continue;
+          const int4 ct = s_ct[uv];
+          hv::Vec<F> v;
 #pragma unroll
-            for (int p = 0; p < F; ++p) o[ocol[p]] += m * val[p];
-          } else if (row5) {
-            o[0] = 0.0;
-#pragma unroll
-            for (int p = 0; p < F; ++p) o[1 + p] = m * val[p];
-          } else {
-#pragma unroll
-            for (int p = 0; p < F; ++p) o[ocol[p]] = m * val[p];
-            if (A.zero_mask)
-              for (int zc = 0; zc < A.ldo; ++zc)
-                if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
+          for (int p = 0; p < F; ++p) {
+            const double* sp = s_s + p * C::SP + N;
+            const double c0 = sp[ct.x];
+            const double c1 = (ct.y >= 0) ? sp[ct.y] : 0.0;
+            const double c2 = (ct.z >= 0) ? sp[ct.z] : 0.0;
+            const double c3 = (ct.z >= 0) ? sp[ct.w] : 0.0;
+            v.v[p] = (c0 + c1) + (c2 + c3);
           }
-        } else {
-          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5;
-#pragma unroll
-          for (int p = 0; p < F; ++p) o[p] = val[p];
+          emit(g, __ldg(Mt_t + (int64_t)l * C::MTS + node), v, s_code[uv], l * N + N);
         }
       }
     }
+    if (l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
     // the next step's barrier (a) orders these reads before the scratch is rewritten
   }
 }
@@ -403,16 +509,44 @@ __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const
   }
 }
 
-template <int n, int TX, int TY, int F>
-int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
-  using C = PlaneCfg<n, TX, TY, F>;
-  hv::DTab<n> Dt;
-  hv::fill_dtab(Dt, Drow);
-  auto kern = lap_plane_kernel<n, TX, TY, F, C::MINB>;
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0>
+int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
+  using C = PlaneCfg<n, TX, TY, F, WV>;
+  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   return HV_OK;
+}
+
+// variant (HV_PLANE_VARIANT, development sweeps): 0 = W via TMA, 3 CTAs/SM; 1 = TMA, 4;
+// 2 = W from global, 4; 3 = global, 5; 4 = global, 6
+template <int n, int TX, int TY, int F>
+int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
+  hv::DTab<n> Dt;
+  hv::fill_dtab(Dt, Drow);
+  if constexpr (n == 5 && F == 4) {
+    const char* v = getenv("HV_PLANE_VARIANT");
+    switch (v ? atoi(v) : 0) {
+      case 1: return run_plane_v<n, TX, TY, F, 0, 4>(A, Dt, st);
+      case 2: return run_plane_v<n, TX, TY, F, 1, 4>(A, Dt, st);
+      case 3: return run_plane_v<n, TX, TY, F, 1, 5>(A, Dt, st);
+      case 4: return run_plane_v<n, TX, TY, F, 1, 6>(A, Dt, st);
+#ifdef HV_PLANE_ABLATE
+      case 11: return run_plane_v<n, TX, TY, F, 0, 3, 1>(A, Dt, st);
+      case 12: return run_plane_v<n, TX, TY, F, 0, 3, 2>(A, Dt, st);
+      case 14: return run_plane_v<n, TX, TY, F, 0, 3, 4>(A, Dt, st);
+      case 18: return run_plane_v<n, TX, TY, F, 0, 3, 8>(A, Dt, st);
+      case 13: return run_plane_v<n, TX, TY, F, 0, 3, 3>(A, Dt, st);
+      case 17: return run_plane_v<n, TX, TY, F, 0, 3, 7>(A, Dt, st);
+      case 25: return run_plane_v<n, TX, TY, F, 0, 3, 15>(A, Dt, st);
+#endif
+      default: break;
+    }
+  }
+  switch (0) {
+    default: return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
+  }
 }
 
 }  // namespace
