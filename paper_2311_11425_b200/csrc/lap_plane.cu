@@ -20,7 +20,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
-#define HV_PLANE_ABLATE 1
 
 #include "hv_common.h"
 #include "lap_common.cuh"
