@@ -65,6 +65,8 @@ class LapPlan(C.Structure):
         ("face", C.c_int),
         ("d_send", _P),
         ("d_recv", _P),
+        ("d_row_slot", _P),
+        ("d_slot_cnt", _P),
     ]
 
 
@@ -100,6 +102,7 @@ _SIGS = {
 }
 
 _lib = None
+ABI_VERSION = 2          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
 
 
 def lib():
@@ -115,6 +118,8 @@ def lib():
             fn = getattr(h, name)
             fn.restype = res
             fn.argtypes = args
+        if h.hv_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{LIB_PATH}: ABI {h.hv_abi_version()} != {ABI_VERSION}: rebuild the library")
         _lib = h
     return _lib
 
