@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(512) euler_setup_kernel(hv::DTab<n> Dt, int64_
 }
 
 template <int n>
-__global__ void __launch_bounds__(512) euler_elem_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
+__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
                                                          const int32_t* __restrict__ gid, const double* __restrict__ w3,
                                                          const double* __restrict__ Mt, const double* __restrict__ q,
                                                          int64_t ldq, double* __restrict__ work) {
