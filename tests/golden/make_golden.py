@@ -32,6 +32,7 @@ os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
 from hevicore import basis as rbasis  # noqa: E402
 from hevicore import euler as reuler  # noqa: E402
 from hevicore import hyperdiff as rhd  # noqa: E402
+from hevicore import linalg as rlinalg  # noqa: E402
 from hevicore import mesh as rmesh  # noqa: E402
 from hevicore import metrics as rmet  # noqa: E402
 from hevicore import state as rstate  # noqa: E402
@@ -54,7 +55,11 @@ def ref_mesh_lattice(nx, ny, nv, N, extents, perturb):
     return rmesh.Mesh(cfg, coords, (b, b, b), layer, hcol)
 
 
-def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, lap_fields=None):
+JAC_COLS = 24
+JAC_LAM = 0.37
+
+
+def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, lap_fields=None, jac=False):
     """Reference outputs for one mesh; inputs are regenerated from the seeds by the tests."""
     out = {}
     mets0 = rmet.curl_invariant_metrics(m)
@@ -87,6 +92,18 @@ def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, l
         out[f"rhs_full_{s}"] = o.rhs_full(rstate.StateField(s, rs))
         out[f"rhs_h_{s}"] = o.rhs_horizontal(rstate.StateField(s, rs), with_hyperdiff=False)
         out[f"rhs_v_{s}"] = o.rhs_vertical(rstate.StateField(s, rs))
+        if jac:
+            # LHEVI column system (euler.py:274-306, linalg.py:112-194) on a column subset
+            band = np.ascontiguousarray(o.column_jacobian(rs[m.col_gid], JAC_LAM)[:JAC_COLS])
+            out[f"jac_sha_{s}"] = np.array(sha(band))
+            out[f"jac_cols_{s}"] = band[:, :, :2 * o.nvar * o.nzl].copy()
+            bf = band.copy()
+            ipiv, _ = rlinalg.banded_lu_factor_batch(bf, o.kl, o.ku)
+            out[f"lu_sha_{s}"] = np.array(sha(bf))
+            out[f"ipiv_{s}"] = ipiv.astype(np.int32)
+            rhs = np.random.default_rng(11).standard_normal((band.shape[0], o.Mdim))
+            x, _ = rlinalg.banded_solve_batch(bf, ipiv, o.kl, o.ku, rhs)
+            out[f"solve_{s}"] = x
     if store_full:
         out["gid"] = m.gid.astype(np.int32)
         out["Jg"] = mets.Jg
@@ -113,7 +130,7 @@ def main():
     for name, c in CASES.items():
         m = ref_mesh(c)
         case(name, m, rhd.HyperDiffConfig(**c["hd"]), c["dt"], make_state(c, m.xg), sets=c["sets"],
-             omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"])
+             omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"], jac=(name != "c1"))
     # basis constants
     np.savez_compressed(HERE / "basis.npz", **{f"D{N}": rbasis.lobatto(N).diff_matrix for N in range(1, 9)},
                         **{f"w{N}": rbasis.lobatto(N).weights for N in range(1, 9)},

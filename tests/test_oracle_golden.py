@@ -78,3 +78,22 @@ def test_rhs_bitwise(prob):
         assert np.array_equal(e.rhs_full(rs), g[f"rhs_full_{s}"]), s
         assert np.array_equal(e.rhs_horizontal_nohd(rs), g[f"rhs_h_{s}"]), s
         assert np.array_equal(e.rhs_vertical(rs), g[f"rhs_v_{s}"]), s
+
+
+def test_column_system_bitwise(prob):
+    """LHEVI column Jacobian band, its pivoted band LU and the back-solve (euler.py:274-417,
+    linalg.py:112-194) against the reference on the first golden columns."""
+    p, g = prob
+    if p.name == "c1":
+        pytest.skip("no column-system fixture for c1")
+    for s in p.c["sets"]:
+        e = p.euler(s)
+        rs = random_state(p.m.ng, s)
+        band, kl, ku = O.column_jacobian(e, rs[p.m.col_gid], 0.37)
+        band = np.ascontiguousarray(band[:24])
+        assert sha(band) == str(g[f"jac_sha_{s}"]), s
+        ipiv = O.band_lu_factor(band, kl, ku)
+        assert sha(band) == str(g[f"lu_sha_{s}"]), s
+        assert np.array_equal(ipiv, g[f"ipiv_{s}"]), s
+        rhs = np.random.default_rng(11).standard_normal((band.shape[0], band.shape[2]))
+        assert np.array_equal(O.band_solve(band, ipiv, kl, ku, rhs), g[f"solve_{s}"]), s
