@@ -219,6 +219,25 @@ int hv_euler_vertical(int N, const double* h_D, const double* h_w, int set_id, d
                       const double* d_gz, const double* d_mask_g, const double* d_Phi_g, const double* d_q,
                       int64_t ldq, double* d_out, int64_t ldo, int accumulate, void* stream);
 
+/* LHEVI column systems.
+ * hv_column_jacobian: band batch of I - lam dV/dq for the columns of d_qcol
+ *   (ncol, n_z, 5) (EulerOps.column_jacobian, euler.py:274-417), written to d_band
+ *   (ncol, 2kl+ku+1, 5 n_z), kl = ku = 5 (N+1) - 1, LAPACK band layout.  d_col_gid
+ *   (ncol, n_z) int32 maps the column nodes to gridpoints (J_g, grad zeta, mask, Phi).
+ * hv_band_lu_factor: in-place batched band LU with partial pivoting
+ *   (linalg.banded_lu_factor_batch, linalg.py:112-163); d_ipiv (nb, M) int32 pivot
+ *   rows, d_info (nb) 0 or 1 + the first column with a zero pivot (SingularMatrixError).
+ * hv_band_solve: d_x (nb, M) <- solution of the factored systems for the right-hand
+ *   sides in d_x (linalg.banded_solve_batch, linalg.py:166-194). */
+int hv_column_jacobian(int N, const double* h_D, const double* h_w, int set_id, double P_A, double R, double gamma,
+                       double lam, int64_t ncol, int nlay, int n_z, const int32_t* d_col_gid, const double* d_qcol,
+                       const double* d_Jg, const double* d_gz, const double* d_mask_g, const double* d_Phi_g,
+                       double* d_band, void* stream);
+int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int M, int32_t* d_ipiv, int32_t* d_info,
+                      void* stream);
+int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_t nb, int kl, int ku, int M, double* d_x,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,6 +95,10 @@ _SIGS = {
     "hv_euler_setup": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P]),
     "hv_euler_vertical": (C.c_int, [C.c_int, _P, _P, C.c_int, _D, _D, _D, _I64, C.c_int, C.c_int, _P, _P, _P, _P, _P,
                                     _P, _I64, _P, _I64, C.c_int, _P]),
+    "hv_column_jacobian": (C.c_int, [C.c_int, _P, _P, C.c_int, _D, _D, _D, _D, _I64, C.c_int, C.c_int, _P, _P,
+                                     _P, _P, _P, _P, _P, _P]),
+    "hv_band_lu_factor": (C.c_int, [_P, _I64, C.c_int, C.c_int, C.c_int, _P, _P, _P]),
+    "hv_band_solve": (C.c_int, [_P, _P, _I64, C.c_int, C.c_int, C.c_int, _P, _P]),
     "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, _P,
                                _P, _P, _P, _P, _I64, _P, _P, _I64, C.c_int, _P]),
     # test hook (host build of the metric arithmetic); never used by the product path

@@ -1,0 +1,421 @@
+// LHEVI column systems on the device.
+//
+// hv_column_jacobian  band batch of I - lam dV/dq (EulerOps.column_jacobian /
+//                     _col_dacc, euler.py:274-417): one CTA per column walks its
+//                     layers bottom to top; the layer's node data go to shared
+//                     memory, then every thread adds its block entries
+//                     (-lam dacc / Mrow) into the LAPACK band (ncol, 2kl+ku+1, M).
+//                     Layers run in order, so the node shared by two layers
+//                     accumulates exactly as the reference's loop does.
+// hv_band_lu_factor   batched band LU with partial pivoting (linalg.py:112-163):
+//                     one warp per system, a sliding window of band columns in
+//                     shared memory (kl+ku+1 live columns + a chunk being
+//                     retired), chunked coalesced row loads / stores.  Same
+//                     elementary operations as the reference (multiplier =
+//                     a / pivot; update = a - (m * u), no FMA contraction), so
+//                     the pivots and factors follow the reference bit for bit
+//                     for a bitwise-equal input band.
+// hv_band_solve       forward (pivot swaps + L) and backward (U) substitution
+//                     (linalg.py:166-194), one warp per system.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "hv_common.h"
+#include "lap_common.cuh"
+
+namespace {
+
+struct ColConsts {
+  double P_A, R, gamma, lam;
+  int set;  // 0 = 2NC, 1 = 2C, 2 = 3C
+};
+
+// per layer node data in shared memory
+template <int n>
+struct LayerNodes {
+  double q[5][n], J[n], z[3][n], mask[n], phi[n], P[n], dP[5][n], mass[n];
+  double dphi[n], dPz[n], dfld[3][n], dth[n];   // Dz contractions along the layer
+};
+
+template <int n>
+__global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv::DTab<n> Wz, ColConsts K,
+                                                              int nlay, int n_z, const int32_t* __restrict__ col_gid,
+                                                              const double* __restrict__ qcol,
+                                                              const double* __restrict__ Jg,
+                                                              const double* __restrict__ gz,
+                                                              const double* __restrict__ mask_g,
+                                                              const double* __restrict__ Phi_g,
+                                                              double* __restrict__ band) {
+  constexpr int N = n - 1;
+  constexpr int NV = 5;
+  constexpr int KL = NV * n - 1, KU = KL, D0 = KL + KU, R = 2 * KL + KU + 1;
+  __shared__ LayerNodes<n> L;
+  const int64_t c = blockIdx.x;
+  const int t = threadIdx.x;
+  const int64_t M = (int64_t)NV * n_z;
+  double* bc = band + c * R * M;
+  const double* w = Wz.D[0];
+  // band = I (zeros elsewhere)
+  for (int64_t e = t; e < R * M; e += blockDim.x) bc[e] = ((e / M) == D0) ? 1.0 : 0.0;
+  __syncthreads();
+  const int32_t* cg = col_gid + c * (int64_t)n_z;
+  const double* qc = qcol + c * (int64_t)n_z * NV;
+  for (int l = 0; l < nlay; ++l) {
+    if (t < n) {
+      const int i = t;
+      const int z = l * N + i;
+      const int g = cg[z];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) L.q[v][i] = qc[(int64_t)z * NV + v];
+      const double J = Jg[g];
+      L.J[i] = J;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) L.z[d][i] = gz[(int64_t)g * 3 + d];
+      L.mask[i] = mask_g[g];
+      L.phi[i] = Phi_g[g];
+      // column mass DSS(w_z J) at this node (euler.py:76-78): previous layer's top first
+      double m = 0.0;
+      if (i == 0 && l > 0) m = m + w[N] * J;
+      m = m + w[i] * J;
+      if (i == N && l < nlay - 1) m = m + w[0] * J;
+      L.mass[i] = m;
+      const double rho = L.q[0][i];
+      double P;
+      if (K.set == 0) P = K.P_A * pow(rho * K.R * L.q[4][i] / K.P_A, K.gamma);
+      else if (K.set == 1) P = K.P_A * pow(K.R * L.q[4][i] / K.P_A, K.gamma);
+      else {
+        const double ke = 0.5 * (L.q[1][i] * L.q[1][i] + L.q[2][i] * L.q[2][i] + L.q[3][i] * L.q[3][i]) / rho;
+        P = (K.gamma - 1.0) * (L.q[4][i] - ke - rho * L.phi[i]);
+      }
+      L.P[i] = P;
+      // dP/dq (state.py:104-125)
+      if (K.set == 0) {
+        L.dP[0][i] = K.gamma * P / rho;
+        L.dP[1][i] = L.dP[2][i] = L.dP[3][i] = 0.0;
+        L.dP[4][i] = K.gamma * P / L.q[4][i];
+      } else if (K.set == 1) {
+        L.dP[0][i] = L.dP[1][i] = L.dP[2][i] = L.dP[3][i] = 0.0;
+        L.dP[4][i] = K.gamma * P / L.q[4][i];
+      } else {
+        const double g1 = K.gamma - 1.0;
+        const double ke2 = L.q[1][i] * L.q[1][i] + L.q[2][i] * L.q[2][i] + L.q[3][i] * L.q[3][i];
+        L.dP[0][i] = g1 * (0.5 * ke2 / (rho * rho) - L.phi[i]);
+        L.dP[1][i] = -g1 * L.q[1][i] / rho;
+        L.dP[2][i] = -g1 * L.q[2][i] / rho;
+        L.dP[3][i] = -g1 * L.q[3][i] / rho;
+        L.dP[4][i] = g1;
+      }
+    }
+    __syncthreads();
+    if (t < n) {   // strong zeta derivatives along the layer
+      const int i = t;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
+#pragma unroll
+      for (int a = 0; a < n; ++a) {
+        const double d = Dt.D[i][a];
+        a0 += d * L.phi[a];
+        a1 += d * L.P[a];
+        a2 += d * L.q[1][a];
+        a3 += d * L.q[2][a];
+        a4 += d * L.q[3][a];
+        a5 += d * L.q[4][a];
+      }
+      L.dphi[i] = a0;
+      L.dPz[i] = a1;
+      L.dfld[0][i] = a2;
+      L.dfld[1][i] = a3;
+      L.dfld[2][i] = a4;
+      L.dth[i] = a5;
+    }
+    __syncthreads();
+    // block entries (i, vi, a, va)
+    for (int e = t; e < NV * n * NV * n; e += blockDim.x) {
+      const int va = e % NV, a = (e / NV) % n, vi = (e / (NV * n)) % NV, i = e / (NV * n * NV);
+      const double rho_i = L.q[0][i], rho_a = L.q[0][a];
+      const double wj_i = w[i] * L.J[i];
+      double B = 0.0;
+      if (K.set == 0) {
+        const double uz_i = L.mask[i] * (L.q[1][i] * L.z[0][i] + L.q[2][i] * L.z[1][i] + L.q[3][i] * L.z[2][i]);
+        const double uz_a = L.mask[a] * (L.q[1][a] * L.z[0][a] + L.q[2][a] * L.z[1][a] + L.q[3][a] * L.z[2][a]);
+        if (vi == 0) {
+          if (va == 0) B = (w[a] * Dt.D[a][i]) * (L.J[a] * uz_a);
+          else if (va <= 3) B = (w[a] * Dt.D[a][i]) * (L.J[a] * (L.mask[a] * rho_a * L.z[va - 1][a]));
+        } else if (vi <= 3) {
+          const double zc = L.z[vi - 1][i];
+          if (va == 0) {
+            const double dg = (i == a) ? (wj_i * (-zc / (rho_i * rho_i)) * L.dPz[i]) : 0.0;
+            B = -(dg + ((wj_i * zc / rho_i) * Dt.D[i][a]) * L.dP[0][a]);
+          } else if (va <= 3) {
+            const double dg = (i == a) ? (wj_i * L.mask[i] * L.z[va - 1][i] * L.dfld[vi - 1][i]) : 0.0;
+            B = (va == vi) ? -(dg + (wj_i * uz_i) * Dt.D[i][a]) : -dg;
+          } else {
+            B = -(((wj_i * zc / rho_i) * Dt.D[i][a]) * L.dP[4][a]);
+          }
+        } else {
+          if (va >= 1 && va <= 3) B = (i == a) ? -(wj_i * L.mask[i] * L.z[va - 1][i] * L.dth[i]) : 0.0;
+          else if (va == 4) B = -((wj_i * uz_i) * Dt.D[i][a]);
+        }
+      } else {
+        const bool three = (K.set == 2);
+        const double Uz_a = L.mask[a] * (L.q[1][a] * L.z[0][a] + L.q[2][a] * L.z[1][a] + L.q[3][a] * L.z[2][a]);
+        const double uz_a = Uz_a / rho_a;
+        const double dUz_a = (va >= 1 && va <= 3) ? L.mask[a] * L.z[va - 1][a] : 0.0;
+        if (vi == 0) {
+          B = (w[a] * Dt.D[a][i]) * (L.J[a] * dUz_a);
+        } else if (vi == 4) {
+          const double T5 = L.q[4][a];
+          double dF;
+          if (!three) {
+            if (va == 0) dF = -T5 * Uz_a / (rho_a * rho_a);
+            else if (va <= 3) dF = L.mask[a] * L.z[va - 1][a] * T5 / rho_a;
+            else dF = uz_a;
+          } else {
+            const double EP = T5 + L.P[a];
+            if (va == 0) dF = -EP * Uz_a / (rho_a * rho_a) + uz_a * L.dP[0][a];
+            else if (va <= 3) dF = L.mask[a] * L.z[va - 1][a] * EP / rho_a + uz_a * L.dP[va][a];
+            else dF = uz_a * (1.0 + L.dP[4][a]);
+          }
+          B = (w[a] * Dt.D[a][i]) * (L.J[a] * dF);
+        } else {
+          const int comp = vi;
+          const double zc_a = L.z[comp - 1][a];
+          const double Uc = L.q[comp][a];
+          double df;
+          if (va == 0) df = L.J[a] * (-Uc * Uz_a / (rho_a * rho_a) + zc_a * L.dP[0][a]);
+          else if (va == 4) df = L.J[a] * zc_a * L.dP[4][a];
+          else {
+            double d = Uc * dUz_a / rho_a + zc_a * L.dP[va][a];
+            if (va == comp) d = d + uz_a;
+            df = L.J[a] * d;
+          }
+          B = -((w[i] * Dt.D[i][a]) * df);
+          if (va == 0 && i == a) B = B + -(wj_i * L.dphi[i] * L.z[comp - 1][i]);
+        }
+      }
+      const double contrib = (-K.lam * B) / L.mass[i];
+      const int64_t row = (int64_t)NV * (l * N + i) + vi, col = (int64_t)NV * (l * N + a) + va;
+      double* p = bc + (D0 + row - col) * M + col;
+      *p = *p + contrib;
+    }
+    __syncthreads();
+  }
+}
+
+template <int n>
+int run_jacobian(const double* hD, const double* hw, const ColConsts& K, int64_t ncol, int nlay, int n_z,
+                 const int32_t* col_gid, const double* qcol, const double* Jg, const double* gz, const double* mask,
+                 const double* Phi, double* band, cudaStream_t st) {
+  hv::DTab<n> Dt, Wz{};
+  hv::fill_dtab(Dt, hD);
+  for (int i = 0; i < n; ++i) Wz.D[0][i] = hw[i];
+  column_jacobian_kernel<n><<<(unsigned)ncol, 256, 0, st>>>(Dt, Wz, K, nlay, n_z, col_gid, qcol, Jg, gz, mask, Phi,
+                                                             band);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+// ---------------------------------------------------------------- band LU / solve
+constexpr int CH = 16;   // columns per retire / load chunk
+
+struct BandDims {
+  int kl, ku, R, M, WC, RS;   // window columns WC = kl + ku + 1 + CH, padded row stride RS (even)
+};
+
+__device__ __forceinline__ double dsub_mul(double a, double m, double u) { return __dsub_rn(a, __dmul_rn(m, u)); }
+
+__global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data, int32_t* __restrict__ ipiv,
+                               int32_t* __restrict__ info) {
+  extern __shared__ double win_all[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+  if (s >= nb) return;
+  double* win = win_all + (size_t)warp * B.R * B.RS;
+  double* mult = win_all + (size_t)(blockDim.x / 32) * B.R * B.RS + warp * 64;
+  double* g = data + s * (int64_t)B.R * B.M;
+  const int d = B.kl + B.ku;
+  auto slot = [&](int col) { return col % B.WC; };
+  auto load_cols = [&](int c0, int c1) {     // columns [c0, c1) -> window
+    for (int r = 0; r < B.R; ++r)
+      for (int col = c0 + lane; col < c1; col += 32) win[r * B.RS + slot(col)] = g[(int64_t)r * B.M + col];
+  };
+  auto store_cols = [&](int c0, int c1) {
+    for (int r = 0; r < B.R; ++r)
+      for (int col = c0 + lane; col < c1; col += 32) g[(int64_t)r * B.M + col] = win[r * B.RS + slot(col)];
+  };
+  int loaded = min(B.M, B.WC);
+  load_cols(0, loaded);
+  int stored = 0;
+  __syncwarp();
+  for (int j = 0; j < B.M; ++j) {
+    const int jmax = min(B.M - 1, j + B.ku + B.kl);
+    if (jmax >= loaded) {   // retire finished columns [stored, j) and bring in the next chunk
+      store_cols(stored, j);
+      stored = j;
+      const int nl = min(B.M, loaded + CH);
+      __syncwarp();
+      load_cols(loaded, nl);
+      loaded = nl;
+      __syncwarp();
+    }
+    const int lm = min(B.kl, B.M - 1 - j);
+    // pivot: first index of the largest |candidate| (np.argmax)
+    double best = -1.0;
+    int bi = 0;
+    for (int r = lane; r <= lm; r += 32) {
+      const double v = fabs(win[(d + r) * B.RS + slot(j)]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int prel = bi;
+    const double piv = win[(d + prel) * B.RS + slot(j)];
+    if (piv == 0.0) {
+      if (lane == 0) info[s] = j + 1;
+      store_cols(stored, loaded);
+      return;
+    }
+    if (lane == 0) ipiv[s * B.M + j] = j + prel;
+    if (prel != 0) {
+      for (int col = j + lane; col <= jmax; col += 32) {
+        const int off = d + j - col;
+        double* a = win + off * B.RS + slot(col);
+        double* b = win + (off + prel) * B.RS + slot(col);
+        const double tmp = *a;
+        *a = *b;
+        *b = tmp;
+      }
+    }
+    __syncwarp();
+    if (lm > 0) {
+      const double pv = win[d * B.RS + slot(j)];
+      for (int i = lane; i < lm; i += 32) {
+        const double m = win[(d + 1 + i) * B.RS + slot(j)] / pv;
+        win[(d + 1 + i) * B.RS + slot(j)] = m;
+        mult[i] = m;
+      }
+      __syncwarp();
+      for (int col = j + 1 + lane; col <= jmax; col += 32) {
+        const int off = d + j - col;
+        const double u = win[off * B.RS + slot(col)];
+        for (int i = 0; i < lm; ++i) {
+          double* a = win + (off + 1 + i) * B.RS + slot(col);
+          *a = dsub_mul(*a, mult[i], u);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  store_cols(stored, B.M);
+  if (lane == 0) info[s] = 0;
+}
+
+__global__ void band_solve_kernel(BandDims B, int64_t nb, const double* __restrict__ data,
+                                  const int32_t* __restrict__ ipiv, double* __restrict__ x) {
+  extern __shared__ double xs_all[];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+  if (s >= nb) return;
+  double* xs = xs_all + (size_t)warp * B.M;
+  const double* g = data + s * (int64_t)B.R * B.M;
+  double* xg = x + s * (int64_t)B.M;
+  const int d = B.kl + B.ku;
+  for (int i = lane; i < B.M; i += 32) xs[i] = xg[i];
+  __syncwarp();
+  for (int j = 0; j < B.M - 1; ++j) {
+    const int p = ipiv[s * B.M + j];
+    if (p != j && lane == 0) {
+      const double tmp = xs[j];
+      xs[j] = xs[p];
+      xs[p] = tmp;
+    }
+    __syncwarp();
+    const int lm = min(B.kl, B.M - 1 - j);
+    const double xj = xs[j];
+    for (int i = lane; i < lm; i += 32)
+      xs[j + 1 + i] = dsub_mul(xs[j + 1 + i], g[(int64_t)(d + 1 + i) * B.M + j], xj);
+    __syncwarp();
+  }
+  for (int i = B.M - 1; i >= 0; --i) {
+    const int jmax = min(B.M - 1, i + B.ku + B.kl);
+    double acc = 0.0;
+    for (int c = i + 1 + lane; c <= jmax; c += 32) acc = fma(g[(int64_t)(d + i - c) * B.M + c], xs[c], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) xs[i] = (xs[i] - acc) / g[(int64_t)d * B.M + i];
+    __syncwarp();
+  }
+  for (int i = lane; i < B.M; i += 32) xg[i] = xs[i];
+}
+
+BandDims band_dims(int kl, int ku, int M) {
+  BandDims B;
+  B.kl = kl;
+  B.ku = ku;
+  B.R = 2 * kl + ku + 1;
+  B.M = M;
+  B.WC = kl + ku + 1 + CH;
+  B.RS = (B.WC + 1) & ~1;
+  if (((B.RS - 1) & 1) == 0) B.RS += 1;   // odd (RS - 1): the diagonal update walks distinct banks
+  return B;
+}
+
+}  // namespace
+
+extern "C" int hv_column_jacobian(int N, const double* h_D, const double* h_w, int set_id, double P_A, double R,
+                                  double gamma, double lam, int64_t ncol, int nlay, int n_z,
+                                  const int32_t* d_col_gid, const double* d_qcol, const double* d_Jg,
+                                  const double* d_gz, const double* d_mask_g, const double* d_Phi_g, double* d_band,
+                                  void* stream) {
+  if (N < 1 || N > 7 || !h_D || !h_w || set_id < 0 || set_id > 2 || ncol <= 0 || nlay <= 0 || n_z != nlay * N + 1 ||
+      !d_col_gid || !d_qcol || !d_Jg || !d_gz || !d_mask_g || !d_Phi_g || !d_band)
+    HV_FAIL(HV_ERR_INVALID, "hv_column_jacobian: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  ColConsts K{P_A, R, gamma, lam, set_id};
+#define HV_JAC(NN_) \
+  case NN_: return run_jacobian<NN_>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_qcol, d_Jg, d_gz, d_mask_g, d_Phi_g, d_band, st);
+  switch (N + 1) {
+    HV_JAC(2) HV_JAC(3) HV_JAC(4) HV_JAC(5) HV_JAC(6) HV_JAC(7) HV_JAC(8)
+  }
+#undef HV_JAC
+  HV_FAIL(HV_ERR_UNSUPPORTED, "hv_column_jacobian: N=%d", N);
+}
+
+extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int M, int32_t* d_ipiv, int32_t* d_info,
+                                 void* stream) {
+  if (!d_data || !d_ipiv || !d_info || nb <= 0 || kl < 0 || ku < 0 || M <= 0)
+    HV_FAIL(HV_ERR_INVALID, "hv_band_lu_factor: bad arguments");
+  const BandDims B = band_dims(kl, ku, M);
+  int wpb = 4;
+  size_t smem = 0;
+  for (; wpb >= 1; --wpb) {
+    smem = sizeof(double) * ((size_t)wpb * B.R * B.RS + (size_t)wpb * 64);
+    if (smem <= 200 * 1024) break;
+  }
+  if (wpb < 1 || kl > 64) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
+  HV_CUDA_CHECK(cudaFuncSetAttribute(band_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  band_lu_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
+                                                                                              d_info);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+extern "C" int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_t nb, int kl, int ku, int M,
+                             double* d_x, void* stream) {
+  if (!d_data || !d_ipiv || !d_x || nb <= 0 || kl < 0 || ku < 0 || M <= 0)
+    HV_FAIL(HV_ERR_INVALID, "hv_band_solve: bad arguments");
+  const BandDims B = band_dims(kl, ku, M);
+  const int wpb = 4;
+  const size_t smem = sizeof(double) * (size_t)wpb * M;
+  if (smem > 200 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_solve: system too large (M=%d)", M);
+  HV_CUDA_CHECK(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  band_solve_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
+                                                                                                d_x);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}

@@ -227,6 +227,51 @@ class EulerOps:
             self._h["cols"] = (cg, mask, phi)
         return self._h["cols"]
 
+    # ------------------------------------------------------------ LHEVI column systems
+    @property
+    def nzl(self):
+        return self.mesh.device().N + 1
+
+    nvar = 5
+
+    @property
+    def kl(self):
+        """Half bandwidth nvar * nzl - 1 (euler.py:84-85)."""
+        return self.nvar * self.nzl - 1
+
+    ku = kl
+
+    @property
+    def Mdim(self):
+        return self.nvar * self.mesh.n_z
+
+    @property
+    def ncol(self):
+        return self.mesh.ncol
+
+    def column_jacobian(self, qcol, lam):
+        """Band batch of I - lam dV/dq about the column state qcol (ncol, n_z, 5)
+        (euler.py:274-306), LAPACK band layout (ncol, 2 kl + ku + 1, 5 n_z)."""
+        from .hyperdiff import _as_device
+
+        torch = torch_mod()
+        q, host = _as_device(qcol)
+        q = q.contiguous()
+        ncol = q.shape[0]
+        if tuple(q.shape[1:]) != (self.mesh.n_z, 5) or ncol > self.mesh.ncol:
+            raise ValueError("qcol must be (ncol, n_z, 5)")
+        dev = self.mesh.device()
+        cg, mask, phi = self._column_arrays()
+        band = torch.empty((ncol, 2 * self.kl + self.ku + 1, self.Mdim), dtype=torch.float64, device="cuda")
+        wz = np.ascontiguousarray(self.mesh.bases[2].weights, dtype=np.float64)
+        k = self.c
+        _lib.check(_lib.lib().hv_column_jacobian(
+            dev.N, dev.D.ctypes.data, wz.ctypes.data, self._SETS[self.set_name], k.P_A, k.R, k.gamma, float(lam),
+            ncol, self.mesh.cfg.n_elem_vertical, self.mesh.n_z, cg.data_ptr(), q.data_ptr(),
+            self.metrics.d_Jg.data_ptr(), self.metrics.d_gz.data_ptr(), mask.data_ptr(), phi.data_ptr(),
+            band.data_ptr(), _lib.stream_handle()))
+        return band.cpu().numpy() if host else band
+
     def rhs_vertical(self, state, out=None, accumulate=False):
         """V(q) assembled from the independent column evaluations (euler.py:138-144, 231-272)."""
         from .hyperdiff import _as_device

@@ -15,6 +15,12 @@ from conftest import golden
 
 pytestmark = pytest.mark.gpu
 
+
+def sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
 TOL = 1e-12
 
 
@@ -237,3 +243,51 @@ def test_rhs_vertical_and_splitting(pair):
             ref_defect = oe.rhs_horizontal_nohd(rs) + oe.rhs_vertical(rs) - oe.rhs_full(rs)
             err = np.linalg.norm((h + v - full) - ref_defect) / np.linalg.norm(full)
             assert err <= 1e-11, (s, err)
+
+
+def test_column_system(pair):
+    """LHEVI column Jacobian band (hv_column_jacobian), band LU (hv_band_lu_factor) and
+    back-solve (hv_band_solve) against the oracle and the reference fixtures."""
+    name, p, o = pair
+    if name == "c1":
+        pytest.skip("no column-system fixture for c1")
+    from cases import random_state
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import euler, linalg
+
+    g = golden(name)
+    for s in p.c["sets"]:
+        ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
+        rs = random_state(p.m.nglobal, s)
+        qcol = np.ascontiguousarray(rs[p.m.col_gid][:24])
+        band = ops.column_jacobian(qcol, 0.37)
+        ob, kl, ku = O.column_jacobian(o.euler(s), rs[p.m.col_gid], 0.37)
+        ob = np.ascontiguousarray(ob[:24])
+        assert (kl, ku) == (ops.kl, ops.ku) and band.shape == ob.shape
+        assert np.abs(band - ob).max() <= 1e-13 * np.abs(ob).max(), (s, np.abs(band - ob).max())
+        assert rel_l2(band[:, :, :g[f"jac_cols_{s}"].shape[2]], g[f"jac_cols_{s}"]) <= 1e-13
+        # the factorisation repeats the reference's elementary operations: bitwise on the same band
+        ref_band = ob.copy()
+        ipiv, flops = linalg.banded_lu_factor_batch(ref_band, kl, ku)
+        assert sha(ref_band) == str(g[f"lu_sha_{s}"]), s
+        assert np.array_equal(ipiv, g[f"ipiv_{s}"]), s
+        rhs = np.random.default_rng(11).standard_normal((24, ops.Mdim))
+        x, _ = linalg.banded_solve_batch(ref_band, ipiv, kl, ku, rhs)
+        assert rel_l2(x, g[f"solve_{s}"]) <= 1e-12, (s, rel_l2(x, g[f"solve_{s}"]))
+        # our own band end to end: same pivots, solution within tolerance
+        ip2, _ = linalg.banded_lu_factor_batch(band, kl, ku)
+        assert np.array_equal(ip2, g[f"ipiv_{s}"]), s
+        x2, _ = linalg.banded_solve_batch(band, ip2, kl, ku, rhs)
+        assert rel_l2(x2, g[f"solve_{s}"]) <= 1e-12, (s, rel_l2(x2, g[f"solve_{s}"]))
+
+
+def test_band_lu_singular_and_wide():
+    from paper_2311_11425_b200 import linalg
+
+    kl = ku = 2
+    data = np.zeros((2, 2 * kl + ku + 1, 6))
+    data[:, kl + ku, :] = 1.0
+    data[1, kl + ku, 3] = 0.0     # system 1: zero pivot at column 3 (nothing below to swap in)
+    with pytest.raises(linalg.SingularMatrixError) as e:
+        linalg.banded_lu_factor_batch(data, kl, ku)
+    assert e.value.j == 3 and e.value.batch == 1
