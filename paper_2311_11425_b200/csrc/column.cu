@@ -57,7 +57,15 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
   double* bc = band + c * R * M;
   const double* w = Wz.D[0];
   // band = I (zeros elsewhere)
-  for (int64_t e = t; e < R * M; e += blockDim.x) bc[e] = ((e / M) == D0) ? 1.0 : 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double v = (r == D0) ? 1.0 : 0.0;
+    double* br = bc + (int64_t)r * M;
+    if ((M & 1) == 0 && ((reinterpret_cast<uintptr_t>(br) & 15) == 0)) {
+      for (int64_t e = t; e < M / 2; e += blockDim.x) reinterpret_cast<double2*>(br)[e] = make_double2(v, v);
+    } else {
+      for (int64_t e = t; e < M; e += blockDim.x) br[e] = v;
+    }
+  }
   __syncthreads();
   const int32_t* cg = col_gid + c * (int64_t)n_z;
   const double* qc = qcol + c * (int64_t)n_z * NV;
@@ -231,17 +239,30 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
   const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
   if (s >= nb) return;
   double* win = win_all + (size_t)warp * B.R * B.RS;
-  double* mult = win_all + (size_t)(blockDim.x / 32) * B.R * B.RS + warp * 64;
   double* g = data + s * (int64_t)B.R * B.M;
   const int d = B.kl + B.ku;
   auto slot = [&](int col) { return col % B.WC; };
+  // chunk transfers: the (row, column) elements of the chunk spread over the lanes, eight
+  // independent loads in flight per lane
   auto load_cols = [&](int c0, int c1) {     // columns [c0, c1) -> window
-    for (int r = 0; r < B.R; ++r)
-      for (int col = c0 + lane; col < c1; col += 32) win[r * B.RS + slot(col)] = g[(int64_t)r * B.M + col];
+    const int w = c1 - c0, tot = B.R * w;
+    for (int e0 = 0; e0 < tot; e0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 32 + lane;
+        v[u] = (e < tot) ? g[(int64_t)(e / w) * B.M + c0 + e % w] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 32 + lane;
+        if (e < tot) win[(e / w) * B.RS + slot(c0 + e % w)] = v[u];
+      }
+    }
   };
   auto store_cols = [&](int c0, int c1) {
-    for (int r = 0; r < B.R; ++r)
-      for (int col = c0 + lane; col < c1; col += 32) g[(int64_t)r * B.M + col] = win[r * B.RS + slot(col)];
+    const int w = c1 - c0, tot = B.R * w;
+    for (int e = lane; e < tot; e += 32) g[(int64_t)(e / w) * B.M + c0 + e % w] = win[(e / w) * B.RS + slot(c0 + e % w)];
   };
   int loaded = min(B.M, B.WC);
   load_cols(0, loaded);
@@ -259,11 +280,13 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
       __syncwarp();
     }
     const int lm = min(B.kl, B.M - 1 - j);
+    const int sj = j % B.WC;                                          // window slot of column j
+    auto sl = [&](int col) { const int t = sj + (col - j); return t >= B.WC ? t - B.WC : t; };
     // pivot: first index of the largest |candidate| (np.argmax)
     double best = -1.0;
     int bi = 0;
     for (int r = lane; r <= lm; r += 32) {
-      const double v = fabs(win[(d + r) * B.RS + slot(j)]);
+      const double v = fabs(win[(d + r) * B.RS + sj]);
       if (v > best) { best = v; bi = r; }
     }
 #pragma unroll
@@ -273,7 +296,7 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
     const int prel = bi;
-    const double piv = win[(d + prel) * B.RS + slot(j)];
+    const double piv = win[(d + prel) * B.RS + sj];
     if (piv == 0.0) {
       if (lane == 0) info[s] = j + 1;
       store_cols(stored, loaded);
@@ -283,8 +306,8 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
     if (prel != 0) {
       for (int col = j + lane; col <= jmax; col += 32) {
         const int off = d + j - col;
-        double* a = win + off * B.RS + slot(col);
-        double* b = win + (off + prel) * B.RS + slot(col);
+        double* a = win + off * B.RS + sl(col);
+        double* b = win + (off + prel) * B.RS + sl(col);
         const double tmp = *a;
         *a = *b;
         *b = tmp;
@@ -292,19 +315,32 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
     }
     __syncwarp();
     if (lm > 0) {
-      const double pv = win[d * B.RS + slot(j)];
-      for (int i = lane; i < lm; i += 32) {
-        const double m = win[(d + 1 + i) * B.RS + slot(j)] / pv;
-        win[(d + 1 + i) * B.RS + slot(j)] = m;
-        mult[i] = m;
-      }
-      __syncwarp();
-      for (int col = j + 1 + lane; col <= jmax; col += 32) {
-        const int off = d + j - col;
-        const double u = win[off * B.RS + slot(col)];
-        for (int i = 0; i < lm; ++i) {
-          double* a = win + (off + 1 + i) * B.RS + slot(col);
-          *a = dsub_mul(*a, mult[i], u);
+      // lanes own the rows below the pivot: multiplier in a register, then the row update
+      // in batches of 8 columns (all loads of a batch before its stores)
+      const double pv = win[d * B.RS + sj];
+      for (int i0 = 0; i0 < lm; i0 += 32) {
+        const int i = i0 + lane;
+        const bool act = i < lm;
+        double m = 0.0;
+        if (act) {
+          m = win[(d + 1 + i) * B.RS + sj] / pv;
+          win[(d + 1 + i) * B.RS + sj] = m;
+        }
+        for (int c0 = j + 1; c0 <= jmax; c0 += 8) {
+          double u[8], a[8];
+          int so[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int col = c0 + k;
+            const int off = d + j - col;
+            const bool ok = act && col <= jmax;
+            so[k] = off * B.RS + sl(col);
+            u[k] = ok ? win[so[k]] : 0.0;
+            a[k] = ok ? win[so[k] + (1 + i) * B.RS] : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (act && c0 + k <= jmax) win[so[k] + (1 + i) * B.RS] = dsub_mul(a[k], m, u[k]);
         }
       }
       __syncwarp();
@@ -360,8 +396,10 @@ BandDims band_dims(int kl, int ku, int M) {
   B.R = 2 * kl + ku + 1;
   B.M = M;
   B.WC = kl + ku + 1 + CH;
-  B.RS = (B.WC + 1) & ~1;
-  if (((B.RS - 1) & 1) == 0) B.RS += 1;   // odd (RS - 1): the diagonal update walks distinct banks
+  // row stride = 3 (mod 4): odd, so the row-update lanes (one row each) hit distinct banks,
+  // and RS - 1 = 2 (mod 4), so the column-walking swaps (stride 1 - RS) are at most 2-way
+  B.RS = B.WC;
+  while ((B.RS & 3) != 3) ++B.RS;
   return B;
 }
 
@@ -394,10 +432,10 @@ extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int
   int wpb = 4;
   size_t smem = 0;
   for (; wpb >= 1; --wpb) {
-    smem = sizeof(double) * ((size_t)wpb * B.R * B.RS + (size_t)wpb * 64);
+    smem = sizeof(double) * (size_t)wpb * B.R * B.RS;
     if (smem <= 200 * 1024) break;
   }
-  if (wpb < 1 || kl > 64) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
+  if (wpb < 1) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
   HV_CUDA_CHECK(cudaFuncSetAttribute(band_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   band_lu_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
                                                                                               d_info);

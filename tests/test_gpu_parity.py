@@ -291,3 +291,27 @@ def test_band_lu_singular_and_wide():
     with pytest.raises(linalg.SingularMatrixError) as e:
         linalg.banded_lu_factor_batch(data, kl, ku)
     assert e.value.j == 3 and e.value.batch == 1
+
+
+@pytest.mark.parametrize("kl,M,nb", [(4, 9, 3), (24, 85, 5), (24, 165, 7), (24, 645, 3), (39, 232, 4), (2, 300, 9)])
+def test_band_lu_random_vs_oracle(kl, M, nb):
+    """Random (pivoting) band systems of the column-system shapes, incl. M far beyond the
+    kernel's column window: factors bitwise equal to the oracle, solve within tolerance."""
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import linalg
+
+    ku = kl
+    rng = np.random.default_rng(kl * 1000 + M)
+    data = np.zeros((nb, 2 * kl + ku + 1, M))
+    for j in range(M):                     # random entries inside the band, zero fill-in rows
+        lo, hi = max(0, j - ku), min(M - 1, j + kl)
+        data[:, kl + ku + lo - j:kl + ku + hi - j + 1, j] = rng.standard_normal((nb, hi - lo + 1))
+    ref = data.copy()
+    ip_ref = O.band_lu_factor(ref, kl, ku)
+    got = data.copy()
+    ip, _ = linalg.banded_lu_factor_batch(got, kl, ku)
+    assert np.array_equal(ip, ip_ref)
+    assert np.array_equal(got, ref)
+    b = rng.standard_normal((nb, M))
+    x, _ = linalg.banded_solve_batch(got, ip, kl, ku, b)
+    assert rel_l2(x, O.band_solve(ref, ip_ref, kl, ku, b)) <= 1e-12
