@@ -76,3 +76,22 @@ def rel_l2(a, b):
     b = np.asarray(b, dtype=float)
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+
+
+# LHEVI step parity case (hevi.step_lhevi, hevi.py:317-362): set 2C on the box_p_n4 mesh,
+# warm-bubble state with seeded momenta, two steps sharing one cached factorisation
+LHEVI = dict(case="box_p_n4", tabs=("ARK2", "ARS3"), dt=0.05, steps=2, update_interval=5,
+             hd=dict(alpha=2, c=(1e-4, 1e-4, 0.0)))   # explicit-stable hyper-diffusion strength
+
+
+def lhevi_state(xg, seed=5):
+    from paper_2311_11425_b200.synthetic import bubble_state_2c
+
+    q = bubble_state_2c(xg, centre=(4000.0, 3000.0, 1000.0), radius=1500.0)
+    rng = np.random.default_rng(seed)
+    x, y, z = xg[:, 0] / 8000.0, xg[:, 1] / 6000.0, xg[:, 2] / 2000.0
+    s2 = lambda a: np.sin(2.0 * np.pi * a)  # noqa: E731
+    q[:, 1] = q[:, 0] * (2.0 * s2(x) * np.cos(np.pi * y) + 0.01 * rng.standard_normal(xg.shape[0]))
+    q[:, 2] = q[:, 0] * (1.5 * s2(y) * np.cos(np.pi * x) + 0.01 * rng.standard_normal(xg.shape[0]))
+    q[:, 3] = q[:, 0] * (0.5 * np.sin(np.pi * z) * s2(x) + 0.01 * rng.standard_normal(xg.shape[0]))
+    return q

@@ -33,6 +33,8 @@ from hevicore import basis as rbasis  # noqa: E402
 from hevicore import euler as reuler  # noqa: E402
 from hevicore import hyperdiff as rhd  # noqa: E402
 from hevicore import linalg as rlinalg  # noqa: E402
+from hevicore import ark as rark  # noqa: E402
+from hevicore import hevi as rhevi  # noqa: E402
 from hevicore import mesh as rmesh  # noqa: E402
 from hevicore import metrics as rmet  # noqa: E402
 from hevicore import state as rstate  # noqa: E402
@@ -40,7 +42,7 @@ from hevicore import state as rstate  # noqa: E402
 from paper_2311_11425_b200 import synthetic  # noqa: E402
 
 sys.path.insert(0, str(HERE.parent))
-from cases import CASES, make_state, random_state  # noqa: E402
+from cases import CASES, LHEVI, lhevi_state, make_state, random_state  # noqa: E402
 
 
 def sha(a):
@@ -126,7 +128,33 @@ def ref_mesh(c):
     return rmesh.build_box(cfg)
 
 
+def lhevi_fixture():
+    """IMEX tableaux (ark.py) and reference LHEVI steps (hevi.step_lhevi) for the device driver."""
+    out = {}
+    for name in rark.tableau_names():
+        t = rark.tableau(name)
+        for f in ("A", "b", "c", "A_im", "b_im", "c_im"):
+            out[f"tab_{name}_{f}"] = np.asarray(getattr(t, f), dtype=np.float64)
+        out[f"tab_{name}_order"] = np.array(t.order)
+    c = CASES[LHEVI["case"]]
+    m = ref_mesh(c)
+    mets = rmet.project_metrics_to_columns(rmet.curl_invariant_metrics(m), m)
+    hd = rhd.HyperDiffConfig(**LHEVI["hd"])
+    vm = rhd.build_viscous_metric(m, mets, hd, dt=LHEVI["dt"])
+    ops = reuler.EulerOps(m, mets, rstate.PhysConstants(omega=0.0), "2C", hyper=(hd, vm))
+    q0 = lhevi_state(m.xg)
+    for name in LHEVI["tabs"]:
+        ls = rhevi.LheviState(update_interval=LHEVI["update_interval"], mode="PS")
+        q = q0.copy()
+        for k in range(LHEVI["steps"]):
+            q = rhevi.step_lhevi(ops, rark.tableau(name), q, LHEVI["dt"], ls)
+            out[f"step_{name}_{k}"] = q
+    np.savez_compressed(HERE / "lhevi.npz", **out)
+    print("lhevi", "bytes", (HERE / "lhevi.npz").stat().st_size)
+
+
 def main():
+    lhevi_fixture()
     for name, c in CASES.items():
         m = ref_mesh(c)
         case(name, m, rhd.HyperDiffConfig(**c["hd"]), c["dt"], make_state(c, m.xg), sets=c["sets"],

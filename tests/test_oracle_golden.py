@@ -97,3 +97,31 @@ def test_column_system_bitwise(prob):
         assert np.array_equal(ipiv, g[f"ipiv_{s}"]), s
         rhs = np.random.default_rng(11).standard_normal((band.shape[0], band.shape[2]))
         assert np.array_equal(O.band_solve(band, ipiv, kl, ku, rhs), g[f"solve_{s}"]), s
+
+
+class _Tab:
+    def __init__(self, z, name):
+        for f in ("A", "b", "c", "A_im", "b_im", "c_im"):
+            setattr(self, f, z[f"tab_{name}_{f}"])
+
+
+def test_lhevi_step_bitwise():
+    """Two LHEVI steps (ark tableaux ARK2 / ARS3) with one cached factorisation, against
+    hevi.step_lhevi run by the reference (tests/golden/lhevi.npz)."""
+    from cases import LHEVI, lhevi_state
+
+    z = golden("lhevi")
+    p = OracleProblem(LHEVI["case"])
+    e = p.euler("2C", omega=0.0)
+    # H_nu of this case at the LHEVI dt (the viscous metric depends on dt)
+    hd = dict(LHEVI["hd"])
+    alpha = hd.pop("alpha")
+    Gnu, _, _ = O.viscous_metric(p.m, p.grad, alpha, dt=LHEVI["dt"], **hd)
+    hyper = lambda q: O.hyperdiffusion(p.m, Gnu, p.Jg_e, p.Minv, q, alpha)  # noqa: E731
+    q0 = lhevi_state(p.m.xg)
+    for name in LHEVI["tabs"]:
+        cache = O.LheviCache(LHEVI["update_interval"])
+        q = q0.copy()
+        for k in range(LHEVI["steps"]):
+            q = O.lhevi_step(e, hyper, _Tab(z, name), q, LHEVI["dt"], cache)
+            assert np.array_equal(q, z[f"step_{name}_{k}"]), (name, k, np.abs(q - z[f"step_{name}_{k}"]).max())
