@@ -1,0 +1,93 @@
+"""LHEVI steps on the device (hevi.step_lhevi, hevi.py:317-362) against the reference.
+
+The fixture tests/golden/lhevi.npz holds the reference's own tableaux and two
+reference steps per tableau (make_golden.py); the oracle reproduces them bit
+for bit (test_oracle_golden.py), the device driver within the fp64 bar.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from cases import LHEVI, lhevi_state, rel_l2
+from conftest import golden
+
+
+class Tab:
+    def __init__(self, z, name):
+        for f in ("A", "b", "c", "A_im", "b_im", "c_im"):
+            setattr(self, f, z[f"tab_{name}_{f}"])
+
+
+def test_lhevi_state_rebuild_logic():
+    from paper_2311_11425_b200.hevi import LheviState
+
+    s = LheviState(update_interval=2)
+    assert s.needs_rebuild(0.1)
+    s.band, s.lam, s.age = object(), 0.1, 0
+    assert not s.needs_rebuild(0.1) and s.needs_rebuild(0.2)
+    s.age = 2
+    assert s.needs_rebuild(0.1)
+    rs = LheviState(update_interval=1, mode="RS")
+    rs.band, rs.lam, rs.age = object(), 0.1, 9
+    assert not rs.needs_rebuild(0.1)
+    with pytest.raises(ValueError):
+        LheviState(mode="XX")
+    with pytest.raises(ValueError):
+        LheviState(update_interval=0)
+
+
+@pytest.fixture(scope="module")
+def lhevi_ops():
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import euler, hyperdiff, state
+
+    p = ProductProblem(LHEVI["case"])
+    cfg = hyperdiff.HyperDiffConfig(**LHEVI["hd"])
+    vm = hyperdiff.build_viscous_metric(p.m, p.mets, cfg, dt=LHEVI["dt"])
+    ops = euler.EulerOps(p.m, p.mets, state.PhysConstants(omega=0.0), "2C", hyper=(cfg, vm))
+    return p, ops
+
+
+@pytest.mark.gpu
+def test_step_lhevi_device(lhevi_ops):
+    import torch
+
+    from paper_2311_11425_b200.hevi import LheviGraph, LheviState, step_lhevi
+
+    p, ops = lhevi_ops
+    z = golden("lhevi")
+    q0 = lhevi_state(p.m.xg)
+    for name in LHEVI["tabs"]:
+        tab = Tab(z, name)
+        ls = LheviState(update_interval=LHEVI["update_interval"])
+        q = torch.from_numpy(q0).cuda()
+        eager = []
+        for k in range(LHEVI["steps"]):
+            q = step_lhevi(ops, tab, q, LHEVI["dt"], ls)
+            eager.append(q.clone())
+            ref = z[f"step_{name}_{k}"]
+            # the step changes q by ~1e-3 relative: hold the increment to the bar too
+            q0_k = q0 if k == 0 else z[f"step_{name}_{k - 1}"]
+            assert rel_l2(q.cpu().numpy(), ref) <= 1e-12, (name, k)
+            assert rel_l2(q.cpu().numpy() - q0_k, ref - q0_k) <= 1e-9, (name, k)
+        assert ls.age == LHEVI["steps"]
+        # the same steps replayed from one captured CUDA graph: bitwise the eager result
+        ls2 = LheviState(update_interval=LHEVI["update_interval"])
+        g = LheviGraph(ops, tab, LHEVI["dt"], ls2, torch.from_numpy(q0).cuda())
+        q = torch.from_numpy(q0).cuda()
+        for k in range(LHEVI["steps"]):
+            q = g.step(q).clone()
+            assert torch.equal(q, eager[k]), (name, k)
+
+
+@pytest.mark.gpu
+def test_step_lhevi_numpy_io(lhevi_ops):
+    from paper_2311_11425_b200.hevi import LheviState, step_lhevi
+
+    p, ops = lhevi_ops
+    z = golden("lhevi")
+    q1 = step_lhevi(ops, Tab(z, "ARK2"), lhevi_state(p.m.xg), LHEVI["dt"], LheviState())
+    assert isinstance(q1, np.ndarray)
+    assert rel_l2(q1, z["step_ARK2_0"]) <= 1e-12
