@@ -145,11 +145,6 @@ typedef struct hv_lap_plan {
   int face;                    /* column nodes per slab face                                   */
   double* d_send;              /* (2*face, n_z, 5) local interface sums (NCCL send payload)    */
   double* d_recv;              /* (2*face, n_z, 5) neighbour sums (NCCL receive buffer)        */
-  /* in-sweep fix-up (plane kernel): the last tile to write a shared node's partial row sums
-   * the slot's rows (fixed order) and writes the final value, so no separate fix-up pass runs
-   * for slots that do not cross a slab interface.  NULL d_slot_cnt disables it. */
-  const int32_t* d_row_slot;   /* (rows) slot of each partial row                              */
-  int32_t* d_slot_cnt;         /* (nslot, n_z) arrival counters, zero between launches         */
 } hv_lap_plan;
 
 /* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the

@@ -65,8 +65,6 @@ class LapPlan(C.Structure):
         ("face", C.c_int),
         ("d_send", _P),
         ("d_recv", _P),
-        ("d_row_slot", _P),
-        ("d_slot_cnt", _P),
     ]
 
 

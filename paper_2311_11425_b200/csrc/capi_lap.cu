@@ -36,7 +36,6 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.zero_mask = zero_mask; A.accumulate = accumulate; A.scale = scale; A.out = out; A.part = P->d_part;
   A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
-  A.row_slot = P->d_row_slot; A.slot_cnt = P->d_slot_cnt;
   return A;
 }
 
@@ -47,13 +46,10 @@ bool use_tiles(const hv_lap_plan* P, int nf) {
   return use_plane(P, nf) || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf));
 }
 
-bool fused_fixup(const hv_lap_plan* P, int nf) { return use_plane(P, nf) && P->d_slot_cnt && P->d_row_slot; }
-
 // tile sweep + packing of the interface sums (no-op on one GPU)
 int lap_local(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
               int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st, int accumulate) {
-  hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
-  if (!fused_fixup(P, nf)) A.slot_cnt = nullptr;
+  const hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
   const int rc = use_plane(P, nf) ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
   if (rc) return rc;
   return hv::slot_pack(A, nf, st);
@@ -62,7 +58,7 @@ int lap_local(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const 
 int lap_finish(const hv_lap_plan* P, int nf, double* out, int64_t ldo, const hv::FieldMap& of, double scale,
                unsigned zero_mask, cudaStream_t st, int accumulate) {
   const hv::TileArgs A = tile_args(P, nullptr, 0, hv::FieldMap{}, out, ldo, of, scale, zero_mask, accumulate);
-  return fused_fixup(P, nf) ? hv::slot_fixup_ext(A, nf, st) : hv::slot_fixup(A, nf, st);
+  return hv::slot_fixup(A, nf, st);
 }
 
 // Run one whole Laplacian pass (single GPU) with the best available kernel for this plan.

@@ -115,13 +115,4 @@ int slot_fixup(const TileArgs& A, int F, cudaStream_t st) {
   }
 }
 
-int slot_fixup_ext(const TileArgs& A, int F, cudaStream_t st) {
-  switch (F) {
-    case 1: return fixup_f<1, true>(A, st);
-    case 4: return fixup_f<4, true>(A, st);
-    case 5: return fixup_f<5, true>(A, st);
-    default: HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup_ext: F=%d", F);
-  }
-}
-
 }  // namespace hv

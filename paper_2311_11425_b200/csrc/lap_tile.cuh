@@ -34,15 +34,11 @@ struct TileArgs {
   int face;                 // column nodes per slab face
   double* send;             // (2 * face, n_z, 5) local sums for the neighbours
   const double* recv;       // (2 * face, n_z, 5) neighbours' sums
-  // in-sweep fix-up (plane kernel); slot_cnt == nullptr: partial rows only, separate fix-up
-  const int32_t* row_slot;  // (rows) slot of each partial row
-  int32_t* slot_cnt;        // (nslot, n_z) arrival counters
 };
 
 bool tile_supported(int N, int TX, int TY, int F);
 int slot_pack(const TileArgs& A, int F, cudaStream_t st);
 int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
-int slot_fixup_ext(const TileArgs& A, int F, cudaStream_t st);   // interface slots only
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
