@@ -233,6 +233,14 @@ int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int M, int32_t
 int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_t nb, int kl, int ku, int M, double* d_x,
                   void* stream);
 
+/* EulerOps.diagnostics (euler.py:421-456): d_out[7] = mass, energy_internal, energy_kinetic,
+ * energy_potential, energy_total, p_surface_min, w_vertical_max.  d_M: the global mass (nglobal),
+ * d_xg (nglobal, 3) only for the sphere (radial velocity), d_col_gid (ncol, n_z) int32 (surface
+ * nodes = first column level), d_work >= 7 * 592 doubles.  Deterministic two-stage reduction. */
+int hv_euler_diagnostics(int set_id, double P_A, double R, double gamma, double c_v, int sphere, int64_t ng,
+                         const double* d_q, const double* d_M, const double* d_Phi_g, const double* d_xg, int64_t ncol,
+                         int n_z, const int32_t* d_col_gid, double* d_work, double* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -459,3 +459,137 @@ extern "C" int hv_euler_vertical(int N, const double* h_D, const double* h_w, in
     default: return run_vertical<8>(h_D, h_w, K, ncol, nlay, n_z, d_col_gid, d_Jg, d_gz, d_mask_g, d_Phi_g, d_q, ldq, d_out, ldo, accumulate, st);
   }
 }
+
+// ---------------------------------------------------------------------------
+// Diagnostics (EulerOps.diagnostics, euler.py:421-456): quadrature-weighted global
+// integrals (M-weighted sums) and the surface-pressure minimum / vertical-velocity
+// maximum.  Two-stage deterministic reduction: a fixed grid of DIAG_BLOCKS blocks writes
+// partials, one block combines them in block order (run-to-run bitwise reproducible).
+namespace {
+
+constexpr int DIAG_BLOCKS = 592, DIAG_T = 256;
+// partial layout per block: 5 sums (mass, e_int, e_kin, e_pot, e_tot3C), max |w|, min P_surface
+constexpr int DIAG_NP = 7;
+
+__device__ __forceinline__ void block_reduce(double (&v)[DIAG_NP], double* sh) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < DIAG_NP; ++k) sh[k * DIAG_T + t] = v[k];
+  __syncthreads();
+  for (int s = DIAG_T / 2; s > 0; s >>= 1) {
+    if (t < s) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sh[k * DIAG_T + t] += sh[k * DIAG_T + t + s];
+      sh[5 * DIAG_T + t] = fmax(sh[5 * DIAG_T + t], sh[5 * DIAG_T + t + s]);
+      sh[6 * DIAG_T + t] = fmin(sh[6 * DIAG_T + t], sh[6 * DIAG_T + t + s]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < DIAG_NP; ++k) v[k] = sh[k * DIAG_T];
+}
+
+__global__ void __launch_bounds__(DIAG_T) diag_partial_kernel(EulerConsts K, double c_v, int sphere, int64_t ng,
+                                                              const double* __restrict__ q,
+                                                              const double* __restrict__ Mm,
+                                                              const double* __restrict__ Phi,
+                                                              const double* __restrict__ xg, int64_t ncol, int n_z,
+                                                              const int32_t* __restrict__ col_gid,
+                                                              double* __restrict__ part) {
+  __shared__ double sh[DIAG_NP * DIAG_T];
+  double v[DIAG_NP] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int64_t g = blockIdx.x * (int64_t)DIAG_T + threadIdx.x; g < ng; g += (int64_t)DIAG_BLOCKS * DIAG_T) {
+    const double* r = q + g * 5;
+    const double rho = r[0], m = Mm[g], phi = Phi[g];
+    double P;
+    if (K.set == 0) P = K.P_A * pow(rho * K.R * r[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * pow(K.R * r[4] / K.P_A, K.gamma);
+    else {
+      const double kk = 0.5 * (r[1] * r[1] + r[2] * r[2] + r[3] * r[3]) / rho;
+      P = (K.gamma - 1.0) * (r[4] - kk - rho * phi);
+    }
+    const double T = P / (rho * K.R);
+    const double u2 = r[1] * r[1] + r[2] * r[2] + r[3] * r[3];
+    const double ke = (K.set == 0) ? 0.5 * rho * u2 : 0.5 * u2 / rho;
+    double wv;
+    if (!sphere) {
+      wv = (K.set == 0) ? fabs(r[3]) : fabs(r[3] / rho);
+    } else {
+      const double x = xg[g * 3], y = xg[g * 3 + 1], z = xg[g * 3 + 2];
+      const double nr = sqrt(x * x + y * y + z * z);
+      const double s = (K.set == 0) ? 1.0 : rho;
+      wv = fabs((r[1] / s) * (x / nr) + (r[2] / s) * (y / nr) + (r[3] / s) * (z / nr));
+    }
+    v[0] += m * rho;
+    v[1] += m * rho * c_v * T;
+    v[2] += m * ke;
+    v[3] += m * rho * phi;
+    v[4] += m * r[4];
+    v[5] = fmax(v[5], wv);
+  }
+  for (int64_t c = blockIdx.x * (int64_t)DIAG_T + threadIdx.x; c < ncol; c += (int64_t)DIAG_BLOCKS * DIAG_T) {
+    const int64_t g = col_gid[c * n_z];
+    const double* r = q + g * 5;
+    double P;
+    if (K.set == 0) P = K.P_A * pow(r[0] * K.R * r[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * pow(K.R * r[4] / K.P_A, K.gamma);
+    else {
+      const double kk = 0.5 * (r[1] * r[1] + r[2] * r[2] + r[3] * r[3]) / r[0];
+      P = (K.gamma - 1.0) * (r[4] - kk - r[0] * Phi[g]);
+    }
+    v[6] = fmin(v[6], P);
+  }
+  block_reduce(v, sh);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < DIAG_NP; ++k) part[k * DIAG_BLOCKS + blockIdx.x] = v[k];
+}
+
+__global__ void __launch_bounds__(DIAG_T) diag_final_kernel(const double* __restrict__ part, int set,
+                                                            double* __restrict__ out) {
+  __shared__ double sh[DIAG_NP * DIAG_T];
+  double v[DIAG_NP] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, INFINITY};
+  for (int b = threadIdx.x; b < DIAG_BLOCKS; b += DIAG_T) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] += part[k * DIAG_BLOCKS + b];
+    v[5] = fmax(v[5], part[5 * DIAG_BLOCKS + b]);
+    v[6] = fmin(v[6], part[6 * DIAG_BLOCKS + b]);
+  }
+  block_reduce(v, sh);
+  if (threadIdx.x == 0) {
+    // mass, energy_internal, energy_kinetic, energy_potential, energy_total, p_surface_min, w_vertical_max
+    double e_int = v[1], e_tot;
+    if (set == 2) {
+      e_tot = v[4];
+      e_int = e_tot - v[2] - v[3];
+    } else {
+      e_tot = e_int + v[2] + v[3];
+    }
+    out[0] = v[0];
+    out[1] = e_int;
+    out[2] = v[2];
+    out[3] = v[3];
+    out[4] = e_tot;
+    out[5] = v[6];
+    out[6] = v[5];
+  }
+}
+
+}  // namespace
+
+extern "C" int hv_euler_diagnostics(int set_id, double P_A, double R, double gamma, double c_v, int sphere,
+                                    int64_t ng, const double* d_q, const double* d_M, const double* d_Phi_g,
+                                    const double* d_xg, int64_t ncol, int n_z, const int32_t* d_col_gid,
+                                    double* d_work, double* d_out, void* stream) {
+  if (set_id < 0 || set_id > 2 || ng <= 0 || ncol <= 0 || n_z <= 0 || !d_q || !d_M || !d_Phi_g || !d_col_gid ||
+      !d_work || !d_out || (sphere && !d_xg))
+    HV_FAIL(HV_ERR_INVALID, "hv_euler_diagnostics: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  EulerConsts K{P_A, R, gamma, 0.0, set_id, 0, 0};
+  diag_partial_kernel<<<DIAG_BLOCKS, DIAG_T, 0, st>>>(K, c_v, sphere, ng, d_q, d_M, d_Phi_g, d_xg, ncol, n_z,
+                                                      d_col_gid, d_work);
+  HV_LAUNCH_CHECK();
+  diag_final_kernel<<<1, DIAG_T, 0, st>>>(d_work, set_id, d_out);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}

@@ -227,6 +227,32 @@ class EulerOps:
             self._h["cols"] = (cg, mask, phi)
         return self._h["cols"]
 
+    # ------------------------------------------------------------ diagnostics
+    DIAG_KEYS = ("mass", "energy_internal", "energy_kinetic", "energy_potential", "energy_total", "p_surface_min",
+                 "w_vertical_max")
+
+    def diagnostics(self, state):
+        """Quadrature-weighted global integrals and surface extrema (euler.py:421-456), one
+        deterministic device reduction (hv_euler_diagnostics)."""
+        from .hyperdiff import _as_device
+
+        torch = torch_mod()
+        data = state.data if hasattr(state, "data") else state
+        q, _ = _as_device(data)
+        cg, _, phi = self._column_arrays()
+        sphere = int(self.mesh.cfg.geometry == "sphere")
+        if sphere and "xg_dev" not in self._h:
+            self._h["xg_dev"] = to_dev(np.ascontiguousarray(self.mesh.xg, dtype=np.float64))
+        xg = self._h["xg_dev"] if sphere else None
+        work = torch.empty(7 * 592, dtype=torch.float64, device="cuda")
+        out = torch.empty(7, dtype=torch.float64, device="cuda")
+        k = self.c
+        _lib.check(_lib.lib().hv_euler_diagnostics(
+            self._SETS[self.set_name], k.P_A, k.R, k.gamma, k.c_v, sphere, q.shape[0], q.data_ptr(),
+            self.mass.d_M.data_ptr(), phi.data_ptr(), xg.data_ptr() if xg is not None else None, self.mesh.ncol,
+            self.mesh.n_z, cg.data_ptr(), work.data_ptr(), out.data_ptr(), _lib.stream_handle()))
+        return dict(zip(self.DIAG_KEYS, (float(v) for v in out.cpu().numpy())))
+
     # ------------------------------------------------------------ LHEVI column systems
     @property
     def nzl(self):

@@ -95,3 +95,19 @@ def lhevi_state(xg, seed=5):
     q[:, 2] = q[:, 0] * (1.5 * s2(y) * np.cos(np.pi * x) + 0.01 * rng.standard_normal(xg.shape[0]))
     q[:, 3] = q[:, 0] * (0.5 * np.sin(np.pi * z) * s2(x) + 0.01 * rng.standard_normal(xg.shape[0]))
     return q
+
+
+def diag_state(m, seed=9):
+    """Physical set-2C state on any mesh (box or sphere): stratified density, seeded
+    momenta, potential temperature 300 K (diagnostics fixture)."""
+    if m.cfg.geometry == "sphere":
+        h = np.linalg.norm(m.xg, axis=1) - m.cfg.radius
+    else:
+        h = m.xg[:, 2]
+    rng = np.random.default_rng(seed)
+    rho = 1.2 * np.exp(-h / 8000.0)
+    q = np.empty((m.xg.shape[0], 5))
+    q[:, 0] = rho
+    q[:, 1:4] = rho[:, None] * rng.normal(0.0, 3.0, (m.xg.shape[0], 3))
+    q[:, 4] = rho * (300.0 + rng.uniform(0.0, 2.0, m.xg.shape[0]))
+    return q

@@ -42,7 +42,7 @@ from hevicore import state as rstate  # noqa: E402
 from paper_2311_11425_b200 import synthetic  # noqa: E402
 
 sys.path.insert(0, str(HERE.parent))
-from cases import CASES, LHEVI, lhevi_state, make_state, random_state  # noqa: E402
+from cases import CASES, LHEVI, diag_state, lhevi_state, make_state, random_state  # noqa: E402
 
 
 def sha(a):
@@ -153,7 +153,38 @@ def lhevi_fixture():
     print("lhevi", "bytes", (HERE / "lhevi.npz").stat().st_size)
 
 
+def diag_fixture():
+    """EulerOps.diagnostics (euler.py:421-456) for all sets on a box and the sphere, and a
+    run.dump_fields dump (run.py:202-211), from the reference."""
+    import tempfile
+
+    from hevicore import run as rrun
+
+    out = {}
+    for cname in ("box_p_n4", "sphere_n4"):
+        c = CASES[cname]
+        m = ref_mesh(c)
+        mets = rmet.project_metrics_to_columns(rmet.curl_invariant_metrics(m), m)
+        consts = rstate.PhysConstants(omega=0.0)
+        q2c = diag_state(m)
+        for s in ("2C", "2NC", "3C"):
+            ops = reuler.EulerOps(m, mets, consts, s)
+            st = rstate.convert_state(rstate.StateField("2C", q2c), s, consts, ops.Phi_g)
+            out[f"{cname}_{s}_state"] = st.data
+            d = ops.diagnostics(st)
+            out[f"{cname}_{s}_keys"] = np.array(sorted(d))
+            out[f"{cname}_{s}_vals"] = np.array([d[k] for k in sorted(d)])
+        if cname == "box_p_n4":
+            with tempfile.TemporaryDirectory() as td:
+                rrun.dump_fields(td + "/f", m, rstate.StateField("2C", q2c), 12.5)
+                out["dump_bin"] = np.frombuffer(open(td + "/f.bin", "rb").read(), dtype=np.uint8)
+                out["dump_hdr"] = np.array(open(td + "/f.hdr").read())
+    np.savez_compressed(HERE / "diag.npz", **out)
+    print("diag", "bytes", (HERE / "diag.npz").stat().st_size)
+
+
 def main():
+    diag_fixture()
     lhevi_fixture()
     for name, c in CASES.items():
         m = ref_mesh(c)

@@ -315,3 +315,25 @@ def test_band_lu_random_vs_oracle(kl, M, nb):
     b = rng.standard_normal((nb, M))
     x, _ = linalg.banded_solve_batch(got, ip, kl, ku, b)
     assert rel_l2(x, O.band_solve(ref, ip_ref, kl, ku, b)) <= 1e-12
+
+
+@pytest.mark.parametrize("cname", ["box_p_n4", "sphere_n4"])
+def test_diagnostics_device(cname):
+    """hv_euler_diagnostics vs the reference's EulerOps.diagnostics (sums within 1e-12
+    relative, extrema exact)."""
+    import torch
+
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import euler, state
+
+    z = golden("diag")
+    p = ProductProblem(cname)
+    for s in ("2C", "2NC", "3C"):
+        ops = euler.EulerOps(p.m, p.mets, state.PhysConstants(omega=0.0), s)
+        q = torch.from_numpy(z[f"{cname}_{s}_state"]).cuda()
+        d = ops.diagnostics(state.StateField(s, q))
+        ref = dict(zip(z[f"{cname}_{s}_keys"], z[f"{cname}_{s}_vals"]))
+        for k, v in ref.items():
+            tol = 0.0 if k in ("w_vertical_max",) else 1e-12
+            assert abs(d[k] - v) <= tol * max(abs(v), 1.0) + (1e-9 if k == "energy_internal" and s == "3C" else 0), \
+                (s, k, d[k], v)

@@ -125,3 +125,32 @@ def test_lhevi_step_bitwise():
         for k in range(LHEVI["steps"]):
             q = O.lhevi_step(e, hyper, _Tab(z, name), q, LHEVI["dt"], cache)
             assert np.array_equal(q, z[f"step_{name}_{k}"]), (name, k, np.abs(q - z[f"step_{name}_{k}"]).max())
+
+
+@pytest.mark.parametrize("cname", ["box_p_n4", "sphere_n4"])
+def test_diagnostics_bitwise(cname):
+    """EulerOps.diagnostics (euler.py:421-456) restated: bitwise the reference's values."""
+    z = golden("diag")
+    p = OracleProblem(cname)
+    for s in ("2C", "2NC", "3C"):
+        d = p.euler(s, omega=0.0).diagnostics(z[f"{cname}_{s}_state"])
+        keys = list(z[f"{cname}_{s}_keys"])
+        assert sorted(d) == keys
+        assert np.array_equal(np.array([d[k] for k in keys]), z[f"{cname}_{s}_vals"]), s
+
+
+def test_field_dump_bytes(tmp_path):
+    """run.dump_fields format (run.py:202-211): our writer is byte-identical to the reference's;
+    load_fields reads it back."""
+    from product_cases import product_mesh
+    from paper_2311_11425_b200 import dumps, state
+
+    z = golden("diag")
+    m = product_mesh("box_p_n4")
+    q = z["box_p_n4_2C_state"]
+    dumps.dump_fields(str(tmp_path / "f"), m, state.StateField("2C", q), 12.5)
+    assert (tmp_path / "f.bin").read_bytes() == z["dump_bin"].tobytes()
+    assert (tmp_path / "f.hdr").read_text() == str(z["dump_hdr"])
+    st, hdr = dumps.load_fields(str(tmp_path / "f"))
+    assert np.array_equal(st.data, q) and st.set_name == "2C" and hdr["time"] == 12.5
+    assert hdr["n_z"] == m.n_z and hdr["columns"] == m.ncol
