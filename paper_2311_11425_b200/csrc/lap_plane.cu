@@ -74,12 +74,17 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {
 // WV: where the packed metric comes from in step c.
 //   0  TMA bulk copy of the tile-layer block into shared memory (mbarrier)
 //   1  straight from global memory (L2-prefetched one layer ahead), no shared staging
-template <int n, int TX, int TY, int F, int WV>
+// H: plane split.  H = 1: a thread owns the whole (xi, zeta) plane of its (element, eta
+// index, field).  H = 2 (N = 7: a 64-node plane does not fit in registers): the plane's xi
+// rows are split over two lanes (ih = 0, 1) that exchange the other half of every xi line
+// with warp shuffles; the eta lines of the line-owner role are split by zeta halves.
+template <int n, int TX, int TY, int F, int WV, int H = 1>
 struct PlaneCfg {
   static constexpr int N = n - 1;
   static constexpr int U = TX * N + 1, V = TY * N + 1, UV = U * V;
   static constexpr int NE = TX * TY;
-  static constexpr int NT = NE * n * F;                  // threads: (element, eta plane, field)
+  static constexpr int NR = n / H, NK = n / H;           // xi rows / eta-line zeta levels per thread
+  static constexpr int NT = NE * n * F * H;              // threads: (eta plane, element, half, field)
   static constexpr int NODES = UV * n;
   static constexpr int GTS = (NODES + 3) & ~3;
   static constexpr int MTS = (NODES + 1) & ~1;
@@ -87,7 +92,7 @@ struct PlaneCfg {
   // 2x2 tiles, thread order (jp, e, f)) the strides come from an exhaustive bank-conflict
   // search (ablate/bank_search.py): every plane / eta-line access of a half-warp then hits
   // 16 distinct 8-byte banks.  Other shapes use the plain padded layout.
-  static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2);
+  static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2 && H == 1);
   static constexpr int pad16(int x) { return x + ((4 - (x % 16)) + 16) % 16; }
   static constexpr int KS = n;                                   // node column (k) stride
   static constexpr int US = TUNED ? 46 : V * n;                  // u stride of s_q
@@ -119,10 +124,10 @@ struct PlaneCfg {
 // layer ahead, coalesced from the tile-ordered map), Minv is read coalesced at step e.
 // AB: ablation bit mask for development timing only (0 in production): 1 = no node-owner
 // step (f), 2 = no q gather, 4 = no metric TMA, 8 = no plane arithmetic (steps b-e)
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0>
-__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
-  using C = PlaneCfg<n, TX, TY, F, WV>;
-  constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF;
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1>
+__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
+  using C = PlaneCfg<n, TX, TY, F, WV, H>;
+  constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                                    // [F][QP] gathered q of the current layer
   double* s_w = sm + C::OFF_W;                         // metric of the current layer (WV 0, TMA)
@@ -132,8 +137,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // metric stage (WV 0)
   const int tid = threadIdx.x;
   const int f = tid % F;
-  const int e = (tid / F) % NE;       // thread order (jp, e, f): f fastest (metric pairs broadcast)
-  const int jp = tid / (F * NE);
+  const int ih = (tid / F) % H;       // thread order (jp, e, ih, f): f fastest (metric pairs broadcast),
+  const int e = (tid / (F * H)) % NE; // the two halves of a plane in lanes 4 apart (shuffle partner)
+  const int jp = tid / (F * H * NE);
+  const int I0 = ih * NR, K0 = ih * NK;
   const int px = e / TY, py = e % TY;
   const int64_t t = blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
@@ -267,9 +274,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
   if (nlay > 1) load_gids(1, gnext);
   __syncthreads();
   if (WV == 0 && tid == 0) issue_metric(0);
-  double carry[n];
+  double carry[NR];
 #pragma unroll
-  for (int i = 0; i < n; ++i) carry[i] = 0.0;
+  for (int r = 0; r < NR; ++r) carry[r] = 0.0;
+  // H = 2: inactive elements of ragged tiles run the plane steps on zeros so that shuffle
+  // partners stay converged (their scratch is zeroed in step e)
+  const bool run = (H == 1) ? act : true;
 
   for (int l = 0; l < nlay; ++l) {
     // ---- a: q(l) has landed
@@ -281,39 +291,64 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
       l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
     }
     // ---- b: plane derivatives in registers, eta lines (i = jp) strong
-    double p0[n][n], p2[n][n];   // [i][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
-    if (act && !(AB & 8)) {
+    double p0[NR][n], p2[NR][n];   // [row][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
+    if (run && !(AB & 8)) {
 #pragma unroll
-      for (int i = 0; i < n; ++i) {
+      for (int r = 0; r < NR; ++r) {
         double ql[n];
 #pragma unroll
-        for (int k = 0; k < n; ++k) ql[k] = s_q[tq(px * N + i, py * N + jp, k)];
+        for (int k = 0; k < n; ++k) ql[k] = s_q[tq(px * N + I0 + r, py * N + jp, k)];
 #pragma unroll
         for (int k = 0; k < n; ++k) {
           double s = 0.0;
 #pragma unroll
           for (int a = 0; a < n; ++a) s = fma(Dt.D[k][a], ql[a], s);
-          p2[i][k] = s;
+          p2[r][k] = s;
         }
 #pragma unroll
-        for (int k = 0; k < n; ++k) p0[i][k] = ql[k];   // q plane, xi-differentiated below
+        for (int k = 0; k < n; ++k) p0[r][k] = ql[k];   // q plane, xi-differentiated below
       }
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        double ql[n];
+        if constexpr (H == 1) {
+          double ql[n];
 #pragma unroll
-        for (int i = 0; i < n; ++i) ql[i] = p0[i][k];
+          for (int i = 0; i < n; ++i) ql[i] = p0[i][k];
 #pragma unroll
-        for (int i = 0; i < n; ++i) {
-          double s = 0.0;
+          for (int i = 0; i < n; ++i) {
+            double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[i][a], ql[a], s);
-          p0[i][k] = s;
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[i][a], ql[a], s);
+            p0[i][k] = s;
+          }
+        } else {
+          // own rows, then the other H - 1 blocks of the xi line from the shuffle partners
+          double co[NR], cp[H - 1][NR];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) co[r] = p0[r][k];
+#pragma unroll
+          for (int m = 1; m < H; ++m)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) cp[m - 1][r] = __shfl_xor_sync(0xffffffffu, co[r], F * m);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + r][I0 + a], co[a], s);
+#pragma unroll
+            for (int m = 1; m < H; ++m) {
+              const int pb = (ih ^ m) * NR;
+#pragma unroll
+              for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + r][pb + a], cp[m - 1][a], s);
+            }
+            p0[r][k] = s;
+          }
         }
       }
-      // eta lines of element e with i = jp: dq_eta(e, jp, a', k)
+      // eta lines of element e with i = jp (zeta levels K0 .. K0 + NK): dq_eta(e, jp, a', k)
 #pragma unroll
-      for (int k = 0; k < n; ++k) {
+      for (int kk = 0; kk < NK; ++kk) {
+        const int k = K0 + kk;
         double ql[n];
 #pragma unroll
         for (int a = 0; a < n; ++a) ql[a] = s_q[tq(px * N + jp, py * N + a, k)];
@@ -331,64 +366,93 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
     if (l + 1 < nlay) issue_gather(gnext);
     if (AB & 8) {
 #pragma unroll
-      for (int i = 0; i < n; ++i)
+      for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int k = 0; k < n; ++k) p0[i][k] = p2[i][k] = s_q[tq(i, jp, k)];
+        for (int k = 0; k < n; ++k) p0[r][k] = p2[r][k] = s_q[tq(r, jp, k)];
     }
     // ---- c: flux at the plane nodes, weak xi / zeta in registers
     if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)(l & 1));
-    if (act) {
+    if (run) {
       const double* W = (WV == 0) ? s_w + (e * n + jp) * 2 : Wt_t + (int64_t)l * C::WL + (e * n + jp) * 2;
 #pragma unroll
-      for (int i = 0; i < n; ++i) {
-        // all loads of the row first: one shared-memory round trip per row, not per node
-        double d1[n];
-        double2 wa[n], wb[n], wc[n];   // (w00 w01) (w02 w11) (w12 w22)
+      for (int r = 0; r < NR; ++r) {
+        const int i = I0 + r;
+        // all loads of a row chunk first: one shared-memory round trip per chunk, not per node
+        constexpr int KB = (n > 5) ? n / 2 : n;
 #pragma unroll
-        for (int k = 0; k < n; ++k) {
-          const int wo = (i * n + k) * NE * n * 2;
-          if (WV == 0) {
-            wa[k] = *reinterpret_cast<const double2*>(W + 0 * n * n * NE * n * 2 + wo);
-            wb[k] = *reinterpret_cast<const double2*>(W + 1 * n * n * NE * n * 2 + wo);
-            wc[k] = *reinterpret_cast<const double2*>(W + 2 * n * n * NE * n * 2 + wo);
-          } else {
-            wa[k] = ldg_stream2(W + 0 * n * n * NE * n * 2 + wo);
-            wb[k] = ldg_stream2(W + 1 * n * n * NE * n * 2 + wo);
-            wc[k] = ldg_stream2(W + 2 * n * n * NE * n * 2 + wo);
+        for (int k0 = 0; k0 < n; k0 += KB) {
+          double d1[KB];
+          double2 wa[KB], wb[KB], wc[KB];   // (w00 w01) (w02 w11) (w12 w22)
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const int wo = (i * n + k0 + kk) * NE * n * 2;
+            if (WV == 0) {
+              wa[kk] = *reinterpret_cast<const double2*>(W + 0 * n * n * NE * n * 2 + wo);
+              wb[kk] = *reinterpret_cast<const double2*>(W + 1 * n * n * NE * n * 2 + wo);
+              wc[kk] = *reinterpret_cast<const double2*>(W + 2 * n * n * NE * n * 2 + wo);
+            } else {
+              wa[kk] = ldg_stream2(W + 0 * n * n * NE * n * 2 + wo);
+              wb[kk] = ldg_stream2(W + 1 * n * n * NE * n * 2 + wo);
+              wc[kk] = ldg_stream2(W + 2 * n * n * NE * n * 2 + wo);
+            }
+            d1[kk] = s_s[sidx(e, i, jp, k0 + kk)];
           }
-          d1[k] = s_s[sidx(e, i, jp, k)];
-        }
 #pragma unroll
-        for (int k = 0; k < n; ++k) {
-          const double d0 = p0[i][k], d2 = p2[i][k];
-          p0[i][k] = wa[k].x * d0 + wa[k].y * d1[k] + wb[k].x * d2;
-          s_s[sidx(e, i, jp, k)] = wa[k].y * d0 + wb[k].y * d1[k] + wc[k].x * d2;
-          p2[i][k] = wb[k].x * d0 + wc[k].x * d1[k] + wc[k].y * d2;
+          for (int kk = 0; kk < KB; ++kk) {
+            const int k = k0 + kk;
+            const double d0 = p0[r][k], d2 = p2[r][k];
+            p0[r][k] = wa[kk].x * d0 + wa[kk].y * d1[kk] + wb[kk].x * d2;
+            s_s[sidx(e, i, jp, k)] = wa[kk].y * d0 + wb[kk].y * d1[kk] + wc[kk].x * d2;
+            p2[r][k] = wb[kk].x * d0 + wc[kk].x * d1[kk] + wc[kk].y * d2;
+          }
         }
       }
       // weak xi (columns of p0, in place): p0[i][k] <- -sum_a D[a][i] f_xi[a][k]
 #pragma unroll
       for (int k = 0; k < n; ++k) {
-        double c[n];
+        if constexpr (H == 1) {
+          double c[n];
 #pragma unroll
-        for (int a = 0; a < n; ++a) c[a] = p0[a][k];
+          for (int a = 0; a < n; ++a) c[a] = p0[a][k];
 #pragma unroll
-        for (int i = 0; i < n; ++i) {
-          double s = 0.0;
+          for (int i = 0; i < n; ++i) {
+            double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][i], c[a], s);
-          p0[i][k] = -s;
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[a][i], c[a], s);
+            p0[i][k] = -s;
+          }
+        } else {
+          double co[NR], cp[H - 1][NR];
+#pragma unroll
+          for (int r = 0; r < NR; ++r) co[r] = p0[r][k];
+#pragma unroll
+          for (int m = 1; m < H; ++m)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) cp[m - 1][r] = __shfl_xor_sync(0xffffffffu, co[r], F * m);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + a][I0 + r], co[a], s);
+#pragma unroll
+            for (int m = 1; m < H; ++m) {
+              const int pb = (ih ^ m) * NR;
+#pragma unroll
+              for (int a = 0; a < NR; ++a) s = fma(Dt.D[pb + a][I0 + r], cp[m - 1][a], s);
+            }
+            p0[r][k] = -s;
+          }
         }
       }
       // weak zeta (rows of p2) accumulated into p0
 #pragma unroll
-      for (int i = 0; i < n; ++i)
+      for (int r = 0; r < NR; ++r)
 #pragma unroll
         for (int k = 0; k < n; ++k) {
           double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], p2[i][a], s);
-          p0[i][k] -= s;
+          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], p2[r][a], s);
+          p0[r][k] -= s;
         }
     }
     __syncthreads();
@@ -396,10 +460,11 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
       fence_proxy_async();
       issue_metric(l + 1);
     }
-    // ---- d: eta lines weak, in place (line i = jp of element e)
-    if (act) {
+    // ---- d: eta lines weak, in place (line i = jp of element e, zeta levels K0 .. K0 + NK)
+    if (run) {
 #pragma unroll
-      for (int k = 0; k < n; ++k) {
+      for (int kk = 0; kk < NK; ++kk) {
+        const int k = K0 + kk;
         double ql[n];
 #pragma unroll
         for (int a = 0; a < n; ++a) ql[a] = s_s[sidx(e, jp, a, k)];
@@ -425,19 +490,20 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV>::NT, MB) lap_plane_
     }
     if (act) {
 #pragma unroll
-      for (int i = 0; i < n; ++i) {
+      for (int r = 0; r < NR; ++r) {
+        const int i = I0 + r;
 #pragma unroll
-        for (int k = 0; k < n; ++k) p0[i][k] -= s_s[sidx(e, i, jp, k)];
-        p0[i][0] += carry[i];
-        carry[i] = p0[i][N];
+        for (int k = 0; k < n; ++k) p0[r][k] -= s_s[sidx(e, i, jp, k)];
+        p0[r][0] += carry[r];
+        carry[r] = p0[r][N];
 #pragma unroll
-        for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = p0[i][k];
+        for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = p0[r][k];
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < n; ++i)
+      for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = 0.0;
+        for (int k = 0; k < n; ++k) s_s[sidx(e, I0 + r, jp, k)] = 0.0;
     }
     __syncthreads();
     // ---- f: node owners (items (column, k < N); k = N only on the top layer) sum the
@@ -508,10 +574,10 @@ __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const
   }
 }
 
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0>
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1>
 int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
-  using C = PlaneCfg<n, TX, TY, F, WV>;
-  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB>;
+  using C = PlaneCfg<n, TX, TY, F, WV, H>;
+  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
@@ -524,6 +590,11 @@ template <int n, int TX, int TY, int F>
 int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
+  if constexpr (n == 8) {
+    const char* hv = getenv("HV_N7_SPLIT");
+    if (hv && atoi(hv) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2>(A, Dt, st);
+    return run_plane_v<n, TX, TY, F, 0, 1, 0, 4>(A, Dt, st);
+  } else {
   if constexpr (n == 5 && F == 4) {
     const char* v = getenv("HV_PLANE_VARIANT");
     switch (v ? atoi(v) : 0) {
@@ -546,6 +617,7 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   switch (0) {
     default: return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
   }
+  }
 }
 
 }  // namespace
@@ -553,6 +625,7 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
 namespace hv {
 
 bool plane_supported(int N, int TX, int TY, int F) {
+  if (N == 7) return F == 4 && TX == 2 && TY == 2;     // split planes (H = 2)
   return (F == 1 || F == 4 || F == 5) && TX == 2 && TY == 2 && N >= 1 && N <= 4;
 }
 
@@ -563,6 +636,7 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
     if (F == 4) return run_plane<NN_ + 1, 2, 2, 4>(A, Drow, st);  \
     if (F == 5) return run_plane<NN_ + 1, 2, 2, 5>(A, Drow, st);  \
   }
+  if (N == 7 && F == 4) return run_plane<8, 2, 2, 4>(A, Drow, st);
   HV_PLANE_CASE(1)
   HV_PLANE_CASE(2)
   HV_PLANE_CASE(3)

@@ -16,16 +16,22 @@ mesh) the plan is rejected and the operators use the element-parallel path.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 
 def tile_shape(N, F=4):
-    """(TX, TY) of the compiled sweep kernels: 2x2 columns for the line kernel
-    (lap_tile.cu) and the plane-owner kernel (lap_plane.cu); single columns for N = 7
-    (the 6-component metric of an N = 7 element is 24.6 KB: 1x1 tiles keep two CTAs per SM)."""
-    return (1, 1) if N == 7 else (2, 2)
+    """(TX, TY) of the compiled sweep kernels: 2x2 columns for the plane-owner kernel
+    (lap_plane.cu) and the line kernel (lap_tile.cu); single columns for the N = 7 line
+    kernel (the 6-component metric of an N = 7 element is 24.6 KB: 1x1 tiles keep two CTAs
+    per SM).  ``HV_N7_KERNEL=plane`` selects 2x2 tiles and the split-plane kernel at N = 7
+    (measured slower on c4)."""
+    if N == 7 and os.environ.get("HV_N7_KERNEL", "") != "plane":
+        return (1, 1)
+    return (2, 2)
 
 
 class TilePlan:
