@@ -136,7 +136,7 @@ typedef struct hv_lap_plan {
   const int32_t* d_col_gid;    /* (ncol, n_z) int32 column gids                       */
   const double* d_Wt;          /* tiled packed metric                                 */
   const double* d_Mt;          /* Minv in tile order (ntiles, nlay, MTS)              */
-  double* d_part;              /* partial rows (rows, n_z, 5)                         */
+  double* d_part;              /* partial rows (rows, n_z, F), >= rows*n_z*5 doubles   */
   int kernel;                  /* 0: line-tile kernel (lap_tile.cu), 1: plane-owner kernel (lap_plane.cu) */
   /* multi-GPU slab interface (parallel.py); d_slot_ext == NULL on one GPU */
   const int32_t* d_slot_ext;   /* (nslot) -1 or side*face + jf, side 0 = lower rank, 1 = upper   */

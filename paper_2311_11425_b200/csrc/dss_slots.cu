@@ -26,7 +26,7 @@ __device__ __forceinline__ void local_sum(const TileArgs& A, int64_t s, int z, d
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
   for (int r = 0; r < nc; ++r) {
-    const double* p = A.part + ((int64_t)(r0 + r) * A.n_z + z) * 5;
+    const double* p = A.part + ((int64_t)(r0 + r) * A.n_z + z) * F;   // partial rows: F doubles
 #pragma unroll
     for (int ff = 0; ff < F; ++ff) acc[ff] += p[ff];
   }

@@ -235,16 +235,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
       }
     } else {
       const int64_t r = (int64_t)cd * A.n_z + z;
-      double* o = A.part + r * 5;
+      double* o = A.part + r * F;                       // partial rows: F doubles
       if constexpr (F == 4) {
-        if ((r & 1) == 0) {
-          st_v2(o, val.v[0], val.v[1]);
-          st_v2(o + 2, val.v[2], val.v[3]);
-        } else {
-          o[0] = val.v[0];
-          st_v2(o + 1, val.v[1], val.v[2]);
-          o[3] = val.v[3];
-        }
+        st_v2(o, val.v[0], val.v[1]);
+        st_v2(o + 2, val.v[2], val.v[3]);
       } else {
 #pragma unroll
         for (int p = 0; p < F; ++p) o[p] = val.v[p];

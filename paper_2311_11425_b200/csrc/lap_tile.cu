@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
               if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
         }
       } else {
-        double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * 5;
+        double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * F;
 #pragma unroll
         for (int p = 0; p < F; ++p) o[p] = val[p];
       }
