@@ -216,9 +216,11 @@ class EulerOps:
 
         data = state.data if hasattr(state, "data") else state
         qd, host = _as_device(data)
-        o, _ = self._rhs(qd, 7, 0, out=out)
+        # H_nu first (plain row writes from the sweep), then S accumulated by the streaming
+        # DSS kernel: S + H == H + S bitwise, and the read-modify-write moves out of the sweep
         cfg, viscous = self.hyper
-        hyperdiffusion_apply(StateField(self.set_name, qd), cfg, viscous, self, out=o, accumulate=True)
+        o = hyperdiffusion_apply(StateField(self.set_name, qd), cfg, viscous, self, out=out)
+        self._rhs(qd, 7, 0, out=o, accumulate=True)
         return o.cpu().numpy() if host else o
 
     def _column_arrays(self):
