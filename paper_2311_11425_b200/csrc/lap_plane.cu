@@ -84,7 +84,8 @@ struct PlaneCfg {
   static constexpr int U = TX * N + 1, V = TY * N + 1, UV = U * V;
   static constexpr int NE = TX * TY;
   static constexpr int NR = n / H, NK = n / H;           // xi rows / eta-line zeta levels per thread
-  static constexpr int NT = NE * n * F * H;              // threads: (eta plane, element, half, field)
+  static constexpr int NP = NE * n * F * H;              // plane threads: (eta plane, element, half, field)
+  static constexpr int NT = (NP + 31) & ~31;             // + helper lanes filling the last warp (gather / output)
   static constexpr int NODES = UV * n;
   static constexpr int GTS = (NODES + 3) & ~3;
   static constexpr int MTS = (NODES + 1) & ~1;
@@ -112,7 +113,8 @@ struct PlaneCfg {
   static constexpr int OFF_S = OFF_W + (WV == 0 ? WL : 0);
   static constexpr int OFF_T = (OFF_S + SE + 1) & ~1;
   static constexpr int OFF_C = OFF_T + 2 * UV;
-  static constexpr int OFF_BAR = (OFF_C + (UV + 1) / 2 + 1) & ~1;
+  static constexpr int OFF_P = OFF_C + (UV + 1) / 2;
+  static constexpr int OFF_BAR = (OFF_P + (UV + 1) / 2 + 1) & ~1;
   static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
 };
 
@@ -134,17 +136,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
   double* s_s = sm + C::OFF_S;                         // [F][NE][n i][n j][n k] eta scratch / element acc
   int4* s_ct = reinterpret_cast<int4*>(sm + C::OFF_T); // [UV] element-copy offsets
   int* s_code = reinterpret_cast<int*>(sm + C::OFF_C); // [UV] partial row or -1
+  int* s_perm = reinterpret_cast<int*>(sm + C::OFF_P); // [UV] output column order: tile-owned first
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // metric stage (WV 0)
   const int tid = threadIdx.x;
   const int f = tid % F;
   const int ih = (tid / F) % H;       // thread order (jp, e, ih, f): f fastest (metric pairs broadcast),
   const int e = (tid / (F * H)) % NE; // the two halves of a plane in lanes 4 apart (shuffle partner)
-  const int jp = tid / (F * H * NE);
+  const int jp = min(tid / (F * H * NE), n - 1);
   const int I0 = ih * NR, K0 = ih * NK;
   const int px = e / TY, py = e % TY;
   const int64_t t = blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
-  const bool act = (px < tx) && (py < ty);
+  const bool pth = tid < C::NP;       // plane thread (the rest: helper lanes for the node-granular steps)
+  const bool act = pth && (px < tx) && (py < ty);
   const int nlay = A.nlay;
   const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::GTS;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
@@ -267,13 +271,20 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
   issue_gather(gcur);
   if (nlay > 1) load_gids(1, gnext);
   __syncthreads();
+  if (tid == 0) {   // output items walk the tile-owned columns first (uniform warps in step f)
+    int c = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int uv = 0; uv < UV; ++uv)
+        if ((s_code[uv] < 0) == (pass == 0)) s_perm[c++] = uv;
+  }
+  __syncthreads();
   if (WV == 0 && tid == 0) issue_metric(0);
   double carry[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) carry[r] = 0.0;
   // H = 2: inactive elements of ragged tiles run the plane steps on zeros so that shuffle
   // partners stay converged (their scratch is zeroed in step e)
-  const bool run = (H == 1) ? act : true;
+  const bool run = (H == 1) ? act : pth;
 
   for (int l = 0; l < nlay; ++l) {
     // ---- a: q(l) has landed
@@ -478,7 +489,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
 #pragma unroll
     for (int it = 0; it < PF; ++it) {
       const int qi = tid + it * C::NT;
-      const int node = (qi / N) * n + qi % N;
+      const int node = (qi < C::FI) ? s_perm[qi / N] * n + qi % N : 0;
       gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
       mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
     }
@@ -493,7 +504,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
 #pragma unroll
         for (int k = 0; k < n; ++k) s_s[sidx(e, i, jp, k)] = p0[r][k];
       }
-    } else {
+    } else if (pth) {
 #pragma unroll
       for (int r = 0; r < NR; ++r)
 #pragma unroll
@@ -508,7 +519,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
         if (gf[it] < 0) continue;
-        const int uv = qi / N, k = qi % N;
+        const int uv = s_perm[qi / N], k = qi % N;
         const int4 ct = s_ct[uv];
         hv::Vec<F> val;
 #pragma unroll
