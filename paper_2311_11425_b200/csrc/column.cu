@@ -351,40 +351,84 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
   if (lane == 0) info[s] = 0;
 }
 
+// rows [r0, r0 + nr) x columns [c0, c0 + w) of a band into ch[col][RS] (column-major in shared
+// memory: the lanes of the substitution steps walk rows); eight global loads in flight
+__device__ __forceinline__ void load_chunk(double* ch, int RS, const double* g, int r0, int nr, int c0, int w, int M,
+                                           int lane) {
+  const int tot = nr * w;
+  for (int e0 = 0; e0 < tot; e0 += 32 * 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 32 + lane;
+      v[u] = (e < tot) ? g[(int64_t)(r0 + e / w) * M + c0 + e % w] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * 32 + lane;
+      if (e < tot) ch[(e % w) * RS + e / w] = v[u];
+    }
+  }
+}
+
+// Solve with the factors streamed through shared memory in CH-column chunks (row segments of
+// a chunk are contiguous in the band layout: coalesced).  Forward: pivot swap + L column
+// (reference order, a - (l * x) without contraction).  Backward in column order: x_i /= U_ii,
+// then the column's U entries update the rows above (same operations as the reference's row
+// sums, different summation order: within the fp64 bar, not bitwise).
 __global__ void band_solve_kernel(BandDims B, int64_t nb, const double* __restrict__ data,
                                   const int32_t* __restrict__ ipiv, double* __restrict__ x) {
   extern __shared__ double xs_all[];
+  const int wpb = blockDim.x / 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + warp;
+  const int64_t s = (int64_t)blockIdx.x * wpb + warp;
+  const int d = B.kl + B.ku;
+  const int RW = d + 1;                          // chunk rows: U part 0..d (forward uses d+1..d+kl)
+  const int RL = B.kl;
+  const int CRS = RW | 1;                        // odd column stride of the chunk buffer
+  double* xs = xs_all + (size_t)warp * (B.M + CRS * CH);
+  double* ch = xs + B.M;                         // [col][CRS]
   if (s >= nb) return;
-  double* xs = xs_all + (size_t)warp * B.M;
   const double* g = data + s * (int64_t)B.R * B.M;
   double* xg = x + s * (int64_t)B.M;
-  const int d = B.kl + B.ku;
   for (int i = lane; i < B.M; i += 32) xs[i] = xg[i];
+  const int32_t* ip = ipiv + s * (int64_t)B.M;
   __syncwarp();
-  for (int j = 0; j < B.M - 1; ++j) {
-    const int p = ipiv[s * B.M + j];
-    if (p != j && lane == 0) {
-      const double tmp = xs[j];
-      xs[j] = xs[p];
-      xs[p] = tmp;
+  // forward: L rows d+1 .. d+kl of each chunk
+  for (int c0 = 0; c0 < B.M - 1; c0 += CH) {
+    const int w = min(CH, B.M - 1 - c0);
+    load_chunk(ch, CRS, g, d + 1, RL, c0, w, B.M, lane);
+    const int pl = (lane < w) ? ip[c0 + lane] : 0;   // the chunk's pivots, one per lane
+    __syncwarp();
+    for (int jj = 0; jj < w; ++jj) {
+      const int j = c0 + jj;
+      const int p = __shfl_sync(0xffffffffu, pl, jj);
+      if (p != j && lane == 0) {
+        const double tmp = xs[j];
+        xs[j] = xs[p];
+        xs[p] = tmp;
+      }
+      __syncwarp();
+      const int lm = min(B.kl, B.M - 1 - j);
+      const double xj = xs[j];
+      for (int i = lane; i < lm; i += 32) xs[j + 1 + i] = dsub_mul(xs[j + 1 + i], ch[jj * CRS + i], xj);
+      __syncwarp();
     }
-    __syncwarp();
-    const int lm = min(B.kl, B.M - 1 - j);
-    const double xj = xs[j];
-    for (int i = lane; i < lm; i += 32)
-      xs[j + 1 + i] = dsub_mul(xs[j + 1 + i], g[(int64_t)(d + 1 + i) * B.M + j], xj);
-    __syncwarp();
   }
-  for (int i = B.M - 1; i >= 0; --i) {
-    const int jmax = min(B.M - 1, i + B.ku + B.kl);
-    double acc = 0.0;
-    for (int c = i + 1 + lane; c <= jmax; c += 32) acc = fma(g[(int64_t)(d + i - c) * B.M + c], xs[c], acc);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) xs[i] = (xs[i] - acc) / g[(int64_t)d * B.M + i];
+  // backward, column by column from the last: rows 0 .. d of each chunk (d = diagonal)
+  for (int c1 = B.M; c1 > 0; c1 -= CH) {
+    const int c0 = max(0, c1 - CH), w = c1 - c0;
+    load_chunk(ch, CRS, g, 0, RW, c0, w, B.M, lane);
     __syncwarp();
+    for (int jj = w - 1; jj >= 0; --jj) {
+      const int i = c0 + jj;
+      if (lane == 0) xs[i] = xs[i] / ch[jj * CRS + d];
+      __syncwarp();
+      const double xi = xs[i];
+      const int nr = min(d, i);                  // rows i-1 .. i-nr hold this column's U entries
+      for (int r = lane; r < nr; r += 32) xs[i - 1 - r] = dsub_mul(xs[i - 1 - r], ch[jj * CRS + d - 1 - r], xi);
+      __syncwarp();
+    }
   }
   for (int i = lane; i < B.M; i += 32) xg[i] = xs[i];
 }
@@ -449,7 +493,7 @@ extern "C" int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_
     HV_FAIL(HV_ERR_INVALID, "hv_band_solve: bad arguments");
   const BandDims B = band_dims(kl, ku, M);
   const int wpb = 4;
-  const size_t smem = sizeof(double) * (size_t)wpb * M;
+  const size_t smem = sizeof(double) * (size_t)wpb * (M + ((kl + ku + 1) | 1) * CH);
   if (smem > 200 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_solve: system too large (M=%d)", M);
   HV_CUDA_CHECK(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   band_solve_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,

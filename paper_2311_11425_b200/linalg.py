@@ -10,6 +10,8 @@ tensors stay on the device.  Kernels: csrc/column.cu.
 
 from __future__ import annotations
 
+import functools
+
 import numpy as np
 
 from . import _lib
@@ -36,6 +38,7 @@ def half_bandwidth(n_var, N_zeta):
     return n_var * (N_zeta + 1) - 1
 
 
+@functools.lru_cache(maxsize=64)
 def _factor_flops(M, kl, ku):
     f = 0
     for j in range(M):
@@ -46,6 +49,7 @@ def _factor_flops(M, kl, ku):
     return f
 
 
+@functools.lru_cache(maxsize=64)
 def _solve_flops(M, kl, ku):
     f = sum(2 * min(kl, M - 1 - j) for j in range(M - 1))
     f += sum(2 * (min(M - 1, i + ku + kl) - i) + 1 for i in range(M))
