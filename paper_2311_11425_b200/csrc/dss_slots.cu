@@ -4,8 +4,7 @@
 //
 // slot_pack   per interface slot and level: the fixed-order sum of the local
 //             partial rows -> the send buffer of that side (ncclSend payload).
-// slot_fixup  per slot (all, or only the slab-interface ones when the plane kernel has
-//             finished the others in-sweep) and level: the fixed-order sum of the local partial rows,
+// slot_fixup  per slot and level: the fixed-order sum of the local partial rows,
 //             plus the neighbour's sum (received) in global rank order
 //             (lower rank first) so both ranks produce bitwise identical values;
 //             times scale * Minv, written to the output row (reference DSS
@@ -45,11 +44,11 @@ __global__ void slot_pack_kernel(TileArgs A) {
   for (int ff = 0; ff < F; ++ff) o[ff] = acc[ff];
 }
 
-template <int F, bool EXT_ONLY>
+template <int F>
 __global__ void slot_fixup_kernel(TileArgs A) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (id >= (EXT_ONLY ? A.next : A.nslot) * A.n_z) return;
-  const int64_t s = EXT_ONLY ? (int64_t)A.ext_slots[id / A.n_z] : id / A.n_z;
+  if (id >= A.nslot * A.n_z) return;
+  const int64_t s = id / A.n_z;
   const int z = (int)(id % A.n_z);
   const int c = A.slot_col[s];
   const int g = A.col_gid[(int64_t)c * A.n_z + z];
@@ -83,12 +82,11 @@ int pack_f(const TileArgs& A, cudaStream_t st) {
   return HV_OK;
 }
 
-template <int F, bool EXT_ONLY>
+template <int F>
 int fixup_f(const TileArgs& A, cudaStream_t st) {
-  const int64_t ns = EXT_ONLY ? (A.slot_ext ? A.next : 0) : A.nslot;
-  if (ns <= 0) return HV_OK;
-  const int64_t tot = ns * A.n_z;
-  slot_fixup_kernel<F, EXT_ONLY><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+  if (A.nslot <= 0) return HV_OK;
+  const int64_t tot = A.nslot * A.n_z;
+  slot_fixup_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
@@ -108,9 +106,9 @@ int slot_pack(const TileArgs& A, int F, cudaStream_t st) {
 
 int slot_fixup(const TileArgs& A, int F, cudaStream_t st) {
   switch (F) {
-    case 1: return fixup_f<1, false>(A, st);
-    case 4: return fixup_f<4, false>(A, st);
-    case 5: return fixup_f<5, false>(A, st);
+    case 1: return fixup_f<1>(A, st);
+    case 4: return fixup_f<4>(A, st);
+    case 5: return fixup_f<5>(A, st);
     default: HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: F=%d", F);
   }
 }

@@ -589,39 +589,39 @@ int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
   return HV_OK;
 }
 
-// variant (HV_PLANE_VARIANT, development sweeps): 0 = W via TMA, 3 CTAs/SM; 1 = TMA, 4;
-// 2 = W from global, 4; 3 = global, 5; 4 = global, 6
+// Production: W by TMA into shared memory, 3 CTAs/SM (N <= 4); split planes H = 4 at N = 7
+// (HV_N7_SPLIT=2 for H = 2).  Building with -DHV_PLANE_ABLATE adds the development variants
+// selected by HV_PLANE_VARIANT (metric from global memory, other occupancy targets, ablations
+// of single steps; tools_time_plane.py).
 template <int n, int TX, int TY, int F>
 int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   if constexpr (n == 8) {
-    const char* hv = getenv("HV_N7_SPLIT");
-    if (hv && atoi(hv) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2>(A, Dt, st);
+    const char* hs = getenv("HV_N7_SPLIT");
+    if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2>(A, Dt, st);
     return run_plane_v<n, TX, TY, F, 0, 1, 0, 4>(A, Dt, st);
   } else {
-  if constexpr (n == 5 && F == 4) {
-    const char* v = getenv("HV_PLANE_VARIANT");
-    switch (v ? atoi(v) : 0) {
-      case 1: return run_plane_v<n, TX, TY, F, 0, 4>(A, Dt, st);
-      case 2: return run_plane_v<n, TX, TY, F, 1, 4>(A, Dt, st);
-      case 3: return run_plane_v<n, TX, TY, F, 1, 5>(A, Dt, st);
-      case 4: return run_plane_v<n, TX, TY, F, 1, 6>(A, Dt, st);
 #ifdef HV_PLANE_ABLATE
-      case 11: return run_plane_v<n, TX, TY, F, 0, 3, 1>(A, Dt, st);
-      case 12: return run_plane_v<n, TX, TY, F, 0, 3, 2>(A, Dt, st);
-      case 14: return run_plane_v<n, TX, TY, F, 0, 3, 4>(A, Dt, st);
-      case 18: return run_plane_v<n, TX, TY, F, 0, 3, 8>(A, Dt, st);
-      case 13: return run_plane_v<n, TX, TY, F, 0, 3, 3>(A, Dt, st);
-      case 17: return run_plane_v<n, TX, TY, F, 0, 3, 7>(A, Dt, st);
-      case 25: return run_plane_v<n, TX, TY, F, 0, 3, 15>(A, Dt, st);
-#endif
-      default: break;
+    if constexpr (n == 5 && F == 4) {
+      const char* v = getenv("HV_PLANE_VARIANT");
+      switch (v ? atoi(v) : 0) {
+        case 1: return run_plane_v<n, TX, TY, F, 0, 4>(A, Dt, st);
+        case 2: return run_plane_v<n, TX, TY, F, 1, 4>(A, Dt, st);
+        case 3: return run_plane_v<n, TX, TY, F, 1, 5>(A, Dt, st);
+        case 4: return run_plane_v<n, TX, TY, F, 1, 6>(A, Dt, st);
+        case 11: return run_plane_v<n, TX, TY, F, 0, 3, 1>(A, Dt, st);
+        case 12: return run_plane_v<n, TX, TY, F, 0, 3, 2>(A, Dt, st);
+        case 14: return run_plane_v<n, TX, TY, F, 0, 3, 4>(A, Dt, st);
+        case 18: return run_plane_v<n, TX, TY, F, 0, 3, 8>(A, Dt, st);
+        case 13: return run_plane_v<n, TX, TY, F, 0, 3, 3>(A, Dt, st);
+        case 17: return run_plane_v<n, TX, TY, F, 0, 3, 7>(A, Dt, st);
+        case 25: return run_plane_v<n, TX, TY, F, 0, 3, 15>(A, Dt, st);
+        default: break;
+      }
     }
-  }
-  switch (0) {
-    default: return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
-  }
+#endif
+    return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
   }
 }
 

@@ -337,3 +337,22 @@ def test_diagnostics_device(cname):
             tol = 0.0 if k in ("w_vertical_max",) else 1e-12
             assert abs(d[k] - v) <= tol * max(abs(v), 1.0) + (1e-9 if k == "energy_internal" and s == "3C" else 0), \
                 (s, k, d[k], v)
+
+
+@pytest.mark.parametrize("split", ["4", "2"])
+def test_n7_split_plane_kernel(monkeypatch, split):
+    """The opt-in split-plane sweep at N = 7 (HV_N7_KERNEL=plane, 2x2 tiles, H lanes per plane
+    exchanging xi lines by shuffles) against the oracle and the reference golden."""
+    monkeypatch.setenv("HV_N7_KERNEL", "plane")
+    monkeypatch.setenv("HV_N7_SPLIT", split)
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    p = ProductProblem("box_n7")
+    plan = p.ops.lap_plan(p.vm)
+    assert plan.kernel == 1 and (plan.TX, plan.TY) == (2, 2)
+    o = OracleProblem("box_n7")
+    got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
+    assert rel_l2(got, o.hyper()) <= TOL
+    assert rel_l2(got, golden("box_n7")["hyper"]) <= TOL
