@@ -241,6 +241,11 @@ int hv_euler_diagnostics(int set_id, double P_A, double R, double gamma, double 
                          const double* d_q, const double* d_M, const double* d_Phi_g, const double* d_xg, int64_t ncol,
                          int n_z, const int32_t* d_col_gid, double* d_work, double* d_out, void* stream);
 
+/* assembly.elem_deriv / weak_deriv_acc (assembly.py:29-51) on (nelem, n, n, n) element data:
+ * weak = 0: sum_a D[i,a] f_a along axis; weak = 1: -sum_a D[a,i] (w3 f)_a (d_w3: n^3 weights). */
+int hv_elem_deriv(int N, const double* h_D, const double* d_w3, int64_t nelem, const double* d_f, int axis, int weak,
+                  double* d_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

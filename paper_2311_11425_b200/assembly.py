@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib
 from .device import torch_mod
 
-__all__ = ["weights3", "gather", "dss", "GlobalMass"]
+__all__ = ["weights3", "gather", "dss", "elem_deriv", "weak_deriv_acc", "GlobalMass"]
 
 
 def weights3(mesh):
@@ -47,6 +47,31 @@ def dss(mesh, field_e):
                                      dev.nglobal, out.data_ptr(), _lib.stream_handle()))
     out = out.reshape((dev.nglobal,) + extra)
     return out.cpu().numpy() if host else out
+
+
+def _deriv(mesh, f, axis, weak):
+    torch = torch_mod()
+    if axis not in (0, 1, 2):
+        raise ValueError("axis must be 0, 1 or 2")
+    host = isinstance(f, np.ndarray)
+    fe = torch.from_numpy(np.ascontiguousarray(f, dtype=np.float64)).cuda() if host else f.contiguous()
+    dev = mesh.device()
+    if tuple(fe.shape) != (dev.nelem, dev.n, dev.n, dev.n):
+        raise ValueError("element data must be (nelem, n, n, n)")
+    out = torch.empty_like(fe)
+    _lib.check(_lib.lib().hv_elem_deriv(dev.N, dev.D.ctypes.data, dev.w3.data_ptr(), dev.nelem, fe.data_ptr(),
+                                        axis, int(weak), out.data_ptr(), _lib.stream_handle()))
+    return out.cpu().numpy() if host else out
+
+
+def elem_deriv(mesh, f, axis):
+    """Reference-coordinate derivative along one axis: sum_a D[i, a] f_a (assembly.py:29-36)."""
+    return _deriv(mesh, f, axis, False)
+
+
+def weak_deriv_acc(mesh, f, axis):
+    """Weak-form accumulator -sum_a D[a, i] (w3 f)_a (assembly.py:39-51)."""
+    return _deriv(mesh, f, axis, True)
 
 
 class GlobalMass:

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "hv_common.h"
+#include "lap_common.cuh"
 #include "metric_math.h"
 
 namespace {
@@ -419,4 +420,62 @@ extern "C" int hv_mass_proj_finalize(int64_t nglobal, const double* d_S, double*
   if (d_Jg && f[3]) HV_FAIL(HV_ERR_DEGENERATE, "zero mass-matrix entry in projection");
   if (f[2]) HV_FAIL(HV_ERR_DEGENERATE, "non-positive mass-matrix entry (inverted element?)");
   return HV_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Element derivative primitives (assembly.elem_deriv / weak_deriv_acc, assembly.py:29-51):
+// strong: out[e, .., i, ..] = sum_a D[i, a] f[e, .., a, ..] along axis;
+// weak:   out[e, .., i, ..] = -sum_a D[a, i] (w3 f)[e, .., a, ..]   (w3 multiplied first, as the
+// reference's wf = weights3 * f).  One thread per element node.
+namespace {
+
+template <int n>
+__global__ void elem_deriv_kernel(hv::DTab<n> Dt, const double* __restrict__ w3, int64_t nelem,
+                                  const double* __restrict__ f, int axis, int weak, double* __restrict__ out) {
+  constexpr int nn = n * n * n;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= nelem * nn) return;
+  const int64_t e = id / nn;
+  const int t = (int)(id % nn);
+  const int i = t / (n * n), j = (t / n) % n, k = t % n;
+  const int ii = (axis == 0) ? i : (axis == 1) ? j : k;
+  const int stride = (axis == 0) ? n * n : (axis == 1) ? n : 1;
+  const double* fe = f + e * nn + (t - ii * stride);
+  double s = 0.0;
+#pragma unroll
+  for (int a = 0; a < n; ++a) {
+    const double v = fe[a * stride];
+    if (weak) s += Dt.D[a][ii] * (w3[t - ii * stride + a * stride] * v);
+    else s += Dt.D[ii][a] * v;
+  }
+  out[id] = weak ? -s : s;
+}
+
+template <int n>
+int run_elem_deriv(const double* hD, const double* w3, int64_t nelem, const double* f, int axis, int weak,
+                   double* out, cudaStream_t st) {
+  hv::DTab<n> Dt;
+  hv::fill_dtab(Dt, hD);
+  const int64_t tot = nelem * n * n * n;
+  elem_deriv_kernel<n><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(Dt, w3, nelem, f, axis, weak, out);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
+}  // namespace
+
+extern "C" int hv_elem_deriv(int N, const double* h_D, const double* d_w3, int64_t nelem, const double* d_f, int axis,
+                             int weak, double* d_out, void* stream) {
+  if (N < 1 || N > 7 || !h_D || nelem <= 0 || !d_f || !d_out || axis < 0 || axis > 2 || (weak && !d_w3))
+    HV_FAIL(HV_ERR_INVALID, "hv_elem_deriv: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (N + 1) {
+    case 2: return run_elem_deriv<2>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    case 3: return run_elem_deriv<3>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    case 4: return run_elem_deriv<4>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    case 5: return run_elem_deriv<5>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    case 6: return run_elem_deriv<6>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    case 7: return run_elem_deriv<7>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+    default: return run_elem_deriv<8>(h_D, d_w3, nelem, d_f, axis, weak, d_out, st);
+  }
 }

@@ -356,3 +356,16 @@ def test_n7_split_plane_kernel(monkeypatch, split):
     got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
     assert rel_l2(got, o.hyper()) <= TOL
     assert rel_l2(got, golden("box_n7")["hyper"]) <= TOL
+
+
+def test_elem_deriv_primitives(pair):
+    """assembly.elem_deriv / weak_deriv_acc (assembly.py:29-51) on random element data."""
+    name, p, o = pair
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import assembly
+
+    dev = p.m.device()
+    f = np.random.default_rng(3).standard_normal((dev.nelem, dev.n, dev.n, dev.n))
+    for axis in range(3):
+        assert rel_l2(assembly.elem_deriv(p.m, f, axis), O.dstrong(o.m.D, f, axis)) <= 1e-13
+        assert rel_l2(assembly.weak_deriv_acc(p.m, f, axis), O.dweak(o.m.D, o.m.w3, f, axis)) <= 1e-13

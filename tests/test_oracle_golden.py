@@ -154,3 +154,25 @@ def test_field_dump_bytes(tmp_path):
     st, hdr = dumps.load_fields(str(tmp_path / "f"))
     assert np.array_equal(st.data, q) and st.set_name == "2C" and hdr["time"] == 12.5
     assert hdr["n_z"] == m.n_z and hdr["columns"] == m.ncol
+
+
+def test_state_helpers_match_reference():
+    """convert_state / temperature / pressure_derivatives (state.py:104-165): the package's host
+    helpers reproduce the reference's converted fixture states bit for bit."""
+    from product_cases import product_mesh
+    from paper_2311_11425_b200 import state
+
+    z = golden("diag")
+    m = product_mesh("box_p_n4")
+    k = state.PhysConstants(omega=0.0)
+    phi = k.g * m.xg[:, 2]
+    q2c = state.StateField("2C", z["box_p_n4_2C_state"])
+    for s in ("2NC", "3C"):
+        got = state.convert_state(q2c, s, k, phi)
+        assert got.set_name == s and np.array_equal(got.data, z[f"box_p_n4_{s}_state"]), s
+        back = state.convert_state(got, "2C", k, phi)
+        assert np.allclose(back.data, q2c.data, rtol=1e-12, atol=1e-12)
+    d = state.pressure_derivatives("3C", z["box_p_n4_3C_state"], k, Phi=phi)
+    assert set(d) == {"rho", "U", "V", "W", "E"}
+    T = state.temperature("2C", q2c.data, k)
+    assert np.allclose(T, state.pressure("2C", q2c.data, k) / (q2c.data[:, 0] * k.R))
