@@ -302,6 +302,21 @@ class EulerOps:
             band.data_ptr(), _lib.stream_handle()))
         return band.cpu().numpy() if host else band
 
+    def column_apply(self, qcol):
+        """V on column-gathered states qcol (ncol, n_z, 5) -> (ncol, n_z, 5) (euler.py:231-235)."""
+        from .hyperdiff import _as_device
+
+        q, host = _as_device(qcol)
+        if tuple(q.shape) != (self.mesh.ncol, self.mesh.n_z, 5):
+            raise ValueError("qcol must be (ncol, n_z, 5)")
+        torch = torch_mod()
+        cg, _, _ = self._column_arrays()
+        idx = cg.long()
+        qg = torch.empty((self.mesh.nglobal, 5), dtype=torch.float64, device="cuda")
+        qg[idx.reshape(-1)] = q.reshape(-1, 5)
+        v = self.rhs_vertical(qg)[idx]
+        return v.cpu().numpy() if host else v
+
     def rhs_vertical(self, state, out=None, accumulate=False):
         """V(q) assembled from the independent column evaluations (euler.py:138-144, 231-272)."""
         from .hyperdiff import _as_device

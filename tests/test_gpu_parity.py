@@ -369,3 +369,17 @@ def test_elem_deriv_primitives(pair):
     for axis in range(3):
         assert rel_l2(assembly.elem_deriv(p.m, f, axis), O.dstrong(o.m.D, f, axis)) <= 1e-13
         assert rel_l2(assembly.weak_deriv_acc(p.m, f, axis), O.dweak(o.m.D, o.m.w3, f, axis)) <= 1e-13
+
+
+def test_column_apply(pair):
+    """EulerOps.column_apply (euler.py:231-235): V on column-gathered states."""
+    name, p, o = pair
+    from cases import random_state
+    from paper_2311_11425_b200 import euler
+
+    for s in p.c["sets"]:
+        ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
+        rs = random_state(p.m.nglobal, s)
+        got = ops.column_apply(rs[p.m.col_gid])
+        ref = o.euler(s).rhs_vertical(rs)[p.m.col_gid]
+        assert rel_l2(got, ref) <= TOL, s
