@@ -263,6 +263,17 @@ def cpu_sample(name, seconds=8.0, procs=None):
 
 
 # ---------------------------------------------------------------------- arms
+def bench_config(w, world, **extra):
+    """The `config` object of both arms (same workload description)."""
+    cfg = {"workload": f"{w.name}: H_nu alpha=2, {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, "
+                       f"perturbed box, c={w.c}, dt={w.dt}",
+           "fields": 4, "l2": "inputs (11.7 GB/op) exceed L2; no flush",
+           "parallelism": (f"x-slabs x{world} of a ({w.nx}*{world})x{w.ny}x{w.nv} box, slab-face "
+                           "DSS over NCCL p2p" if world > 1 else "single GPU")}
+    cfg.update(extra)
+    return cfg
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -286,8 +297,7 @@ def run_reference(args, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, host-generated)",
-        "config": {"workload": f"{args.workload}: {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, alpha={w.alpha}",
-                   "sample": desc},
+        "config": bench_config(w, world, sample=desc),
         "cpu_baseline": {"value": rate, "unit": "DOF-updates/s", "cores": cores, "kind": "port", "sample": desc},
         "e2e": {"value": rate, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -477,12 +487,7 @@ def run_ours(args, rank, world, local):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded, host-generated geometry; Fourier state)",
-            "config": {"workload": f"{w.name}: H_nu alpha=2, {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, "
-                                   f"perturbed box, c={w.c}, dt={w.dt}",
-                       "nglobal_per_gpu": ng, "nelem_per_gpu": m.nelem, "fields": 4,
-                       "l2": "inputs (11.7 GB/op) exceed L2; no flush",
-                       "parallelism": (f"x-slabs x{world} of a ({w.nx}*{world})x{w.ny}x{w.nv} box, slab-face "
-                                       "DSS over NCCL p2p" if world > 1 else "single GPU")},
+            "config": bench_config(w, world, nglobal_per_gpu=ng, nelem_per_gpu=m.nelem),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": kern_name, "kernel_ms_per_launch": kern_ms,
