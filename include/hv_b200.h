@@ -157,6 +157,12 @@ typedef struct hv_lap_plan {
  * accumulate != 0 adds into out. */
 int hv_lap_local(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf, double* d_out,
                  int64_t ldo, const int32_t* h_of, double scale, uint32_t zero_mask, int accumulate, void* stream);
+/* hv_lap_local on the tiles [t0, t1) only (pack != 0: then pack the interface sums).  The
+ * tile plan puts the tiles holding slab-interface columns first, so a pass can sweep them,
+ * start the neighbour exchange and sweep the interior tiles while it is in flight. */
+int hv_lap_local_tiles(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,
+                       double* d_out, int64_t ldo, const int32_t* h_of, double scale, uint32_t zero_mask, int accumulate,
+                       int64_t t0, int64_t t1, int pack, void* stream);
 int hv_lap_finish(const hv_lap_plan* plan, double* d_out, int64_t ldo, int nf, const int32_t* h_of, double scale,
                   uint32_t zero_mask, int accumulate, void* stream);
 

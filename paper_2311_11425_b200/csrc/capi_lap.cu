@@ -29,7 +29,7 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
                        int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, int accumulate) {
   hv::TileArgs A{};
   A.TX = P->TX; A.TY = P->TY; A.nlay = P->nlay; A.n_z = P->n_z;
-  A.ntiles = P->ntiles; A.nslot = P->nslot;
+  A.ntiles = P->ntiles; A.nslot = P->nslot; A.tile0 = 0; A.tile1 = P->ntiles;
   A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
   A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
   A.Wt = P->d_Wt; A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = q; A.ldq = ldq; A.ldo = ldo; A.qf = qf; A.of = of;
@@ -46,13 +46,16 @@ bool use_tiles(const hv_lap_plan* P, int nf) {
   return use_plane(P, nf) || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf));
 }
 
-// tile sweep + packing of the interface sums (no-op on one GPU)
+// tile sweep over [t0, t1) (+ packing of the interface sums when pack != 0; no-op on one GPU)
 int lap_local(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
-              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st, int accumulate) {
-  const hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
+              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st, int accumulate,
+              int64_t t0 = 0, int64_t t1 = -1, int pack = 1) {
+  hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
+  A.tile0 = t0;
+  A.tile1 = (t1 < 0) ? P->ntiles : t1;
   const int rc = use_plane(P, nf) ? hv::laplacian_plane(A, P->N, nf, P->D, st) : hv::laplacian_tile(A, P->N, nf, P->D, st);
   if (rc) return rc;
-  return hv::slot_pack(A, nf, st);
+  return pack ? hv::slot_pack(A, nf, st) : HV_OK;
 }
 
 int lap_finish(const hv_lap_plan* P, int nf, double* out, int64_t ldo, const hv::FieldMap& of, double scale,
@@ -121,6 +124,20 @@ extern "C" int hv_lap_local(const hv_lap_plan* P, const double* d_q, int64_t ldq
   if (!h_qf || !d_q || !d_out) HV_FAIL(HV_ERR_INVALID, "hv_lap_local: null argument");
   if (!use_tiles(P, nf)) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_lap_local needs a tile plan");
   return lap_local(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, zero_mask, (cudaStream_t)stream, accumulate);
+}
+
+extern "C" int hv_lap_local_tiles(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nf, const int32_t* h_qf,
+                                  double* d_out, int64_t ldo, const int32_t* h_of, double scale, uint32_t zero_mask,
+                                  int accumulate, int64_t t0, int64_t t1, int pack, void* stream) {
+  int rc = check_plan(P);
+  if (rc) return rc;
+  hv::FieldMap qf{}, of{};
+  if ((rc = field_maps(nf, h_qf, ldq, h_of, ldo, qf, of))) return rc;
+  if (!h_qf || !d_q || !d_out) HV_FAIL(HV_ERR_INVALID, "hv_lap_local_tiles: null argument");
+  if (!use_tiles(P, nf)) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_lap_local_tiles needs a tile plan");
+  if (t0 < 0 || t1 > P->ntiles || t0 > t1) HV_FAIL(HV_ERR_INVALID, "hv_lap_local_tiles: bad tile range");
+  return lap_local(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, zero_mask, (cudaStream_t)stream, accumulate, t0, t1,
+                   pack);
 }
 
 extern "C" int hv_lap_finish(const hv_lap_plan* P, double* d_out, int64_t ldo, int nf, const int32_t* h_of,

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
   const int jp = min(tid / (F * H * NE), n - 1);
   const int I0 = ih * NR, K0 = ih * NK;
   const int px = e / TY, py = e % TY;
-  const int64_t t = blockIdx.x;
+  const int64_t t = A.tile0 + blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
   const bool pth = tid < C::NP;       // plane thread (the rest: helper lanes for the node-granular steps)
   const bool act = pth && (px < tx) && (py < ty);
@@ -584,7 +584,8 @@ int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
   using C = PlaneCfg<n, TX, TY, F, WV, H>;
   auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-  kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
+  if (A.tile1 <= A.tile0) return HV_OK;
+  kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

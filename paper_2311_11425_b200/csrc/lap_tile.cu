@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(TileCfg<n, TX, TY, F, FP>::NT, MB)
   const int ij = line % NN;
   const int i = ij / n, j = ij % n;
   const int px = e / TY, py = e % TY;
-  const int64_t t = blockIdx.x;
+  const int64_t t = A.tile0 + blockIdx.x;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
   const bool act = (px < tx) && (py < ty);
   const int nlay = A.nlay;
@@ -512,7 +512,8 @@ int run_tile(const TileArgs& A, const double* Drow, cudaStream_t st) {
   hv::fill_dtab(Dt, Drow);
   auto kern = lap_tile_kernel<n, TX, TY, F, FP, C::MINB>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-  kern<<<(unsigned)A.ntiles, C::NT, C::SMEM, st>>>(Dt, A);
+  if (A.tile1 <= A.tile0) return HV_OK;
+  kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

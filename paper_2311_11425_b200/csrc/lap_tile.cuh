@@ -9,6 +9,7 @@ namespace hv {
 struct TileArgs {
   int TX, TY, nlay, n_z;
   int64_t ntiles, nslot;
+  int64_t tile0, tile1;     // tile range of this launch: [tile0, tile1)
   const int32_t* gt;        // (ntiles, nlay, GTS) tile node gids (U*V*n used, padded to 4), -1 = absent
   const int32_t* code;      // (ntiles, U, V) -1 = tile-owned column node, else partial row
   const int32_t* tmeta;     // (ntiles, 2) active tx, ty of ragged tiles

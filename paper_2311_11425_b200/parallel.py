@@ -94,12 +94,16 @@ class SlabLayout:
 
 
 class DistTransport:
-    """Neighbour exchange with torch.distributed point-to-point ops (NCCL or gloo)."""
+    """Neighbour exchange with torch.distributed point-to-point ops (NCCL or gloo).
+
+    ``start`` enqueues the sends / receives (with NCCL they run on the communicator's stream,
+    ordered after the work already queued on the current stream) and returns the handles;
+    ``wait`` makes the current stream (NCCL) or the host (gloo) wait for them."""
 
     def __init__(self, rank, world):
         self.rank, self.world = rank, world
 
-    def exchange(self, send, recv):
+    def start(self, send, recv):
         import torch.distributed as dist
 
         ops = []
@@ -107,9 +111,15 @@ class DistTransport:
             ops += [dist.P2POp(dist.isend, send[0], self.rank - 1), dist.P2POp(dist.irecv, recv[0], self.rank - 1)]
         if self.rank < self.world - 1:
             ops += [dist.P2POp(dist.isend, send[1], self.rank + 1), dist.P2POp(dist.irecv, recv[1], self.rank + 1)]
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    @staticmethod
+    def wait(works):
+        for r in works:
+            r.wait()
+
+    def exchange(self, send, recv):
+        self.wait(self.start(send, recv))
 
 
 class LoopbackTransport:
@@ -202,7 +212,14 @@ class SlabHyperDiffusion:
         return self.ops.halo
 
     # ---- one pass: local stage (tile sweep + pack), exchange, finish stage (slots)
-    def pass_local(self, k, q, out):
+    @property
+    def next_tiles(self):
+        """Tiles holding slab-interface columns (the tile plan puts them first)."""
+        return self.ops._tile_arrays()[0].next_tiles
+
+    def pass_local(self, k, q, out, part="all"):
+        """Tile sweep of pass k: ``part`` = "all", "ext" (interface tiles + interface sums
+        packed into the send buffer) or "int" (the remaining tiles, no packing)."""
         vars_ = list(self.cfg.variables)
         nv = len(vars_)
         if k == 0:
@@ -221,8 +238,10 @@ class SlabHyperDiffusion:
         self._cur = (dst, ldo, of, scale, zmask)
         qa = (C.c_int32 * nv)(*qf)
         oa = (C.c_int32 * nv)(*of)
-        _lib.check(_lib.lib().hv_lap_local(C.byref(self.plan), src.data_ptr(), ldq, nv, qa, dst.data_ptr(), ldo, oa,
-                                           scale, zmask, 0, _lib.stream_handle()))
+        nt, ne = self.plan.ntiles, self.next_tiles
+        t0, t1, pack = {"all": (0, nt, 1), "ext": (0, ne, 1), "int": (ne, nt, 0)}[part]
+        _lib.check(_lib.lib().hv_lap_local_tiles(C.byref(self.plan), src.data_ptr(), ldq, nv, qa, dst.data_ptr(), ldo,
+                                                 oa, scale, zmask, 0, t0, t1, pack, _lib.stream_handle()))
 
     def pass_finish(self):
         dst, ldo, of, scale, zmask = self._cur
@@ -230,12 +249,14 @@ class SlabHyperDiffusion:
         _lib.check(_lib.lib().hv_lap_finish(C.byref(self.plan), dst.data_ptr(), ldo, len(of), oa, scale, zmask, 0,
                                             _lib.stream_handle()))
 
-    # ---- one process per GPU
+    # ---- one process per GPU: interface tiles, exchange overlapped with the interior tiles
     def apply(self, q, out, transport):
         for k in range(self.cfg.alpha):
-            self.pass_local(k, q, out)
+            self.pass_local(k, q, out, "ext")
             send, recv = self.halo
-            transport.exchange(send, recv)
+            works = transport.start(send, recv)
+            self.pass_local(k, q, out, "int")
+            transport.wait(works)
             self.pass_finish()
         return out
 
@@ -248,12 +269,15 @@ def setup_distributed(layout, cfg, dt, transport):
 
 
 def run_loopback(ops, qs, outs):
-    """H_nu on all slabs of one process (1-GPU test of the device pipeline)."""
+    """H_nu on all slabs of one process (1-GPU test of the device pipeline), in the same
+    interface-tiles / exchange / interior-tiles / finish order as ``apply``."""
     alpha = ops[0].cfg.alpha
     for k in range(alpha):
         for op, q, o in zip(ops, qs, outs):
-            op.pass_local(k, q, o)
+            op.pass_local(k, q, o, "ext")
         LoopbackTransport.exchange_all([op.halo for op in ops])
+        for op, q, o in zip(ops, qs, outs):
+            op.pass_local(k, q, o, "int")
         for op in ops:
             op.pass_finish()
     return outs

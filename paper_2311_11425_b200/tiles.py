@@ -41,10 +41,13 @@ class TilePlan:
         self.__dict__.update(kw)
 
 
-def build_tile_plan(mesh, TX, TY, ext_cols=None):
+def build_tile_plan(mesh, TX, TY, ext_cols=None, _order=None):
     """Tile plan of ``mesh``; ``ext_cols`` maps column id -> interface code
     (side * face + jf) for column nodes also owned by a neighbouring rank
-    (parallel.py): they become slots even when a single local tile owns them."""
+    (parallel.py): they become slots even when a single local tile owns them,
+    and the tiles holding them come first (``next_tiles`` of them) so that one
+    pass can sweep them, ship the interface sums and sweep the interior tiles
+    while the exchange is in flight."""
     N = mesh.degree
     n = N + 1
     if mesh.hgrid is None:
@@ -67,6 +70,8 @@ def build_tile_plan(mesh, TX, TY, ext_cols=None):
             for b0 in range(0, ny, TY):
                 tiles.append((p, a0, b0, min(TX, nx - a0), min(TY, ny - b0)))
     tiles = np.array(tiles, dtype=np.int64)
+    if _order is not None:
+        tiles = tiles[_order]
     nt = len(tiles)
     U, V = TX * N + 1, TY * N + 1
     NE = TX * TY
@@ -143,7 +148,14 @@ def build_tile_plan(mesh, TX, TY, ext_cols=None):
     gtp[:, :, :nodes] = gt.reshape(nt, nlay, nodes)
     slot_ext = ext_code[shared_cols].astype(np.int32)
     ext_slots = np.nonzero(slot_ext >= 0)[0].astype(np.int32)
-    return TilePlan(N=N, n=n, TX=TX, TY=TY, U=U, V=V, NE=NE, nlay=nlay, ntiles=nt, tiles=tiles, elem=elem,
+    ext_tile = np.zeros(nt, dtype=bool)
+    if ext_cols:
+        ext_tile = (np.where(col >= 0, is_ext[np.maximum(col, 0)], False)).reshape(nt, -1).any(axis=1)
+        if _order is None and not np.all(ext_tile[:ext_tile.sum()]):
+            # interface tiles first (stable), rebuild with that order
+            return build_tile_plan(mesh, TX, TY, ext_cols,
+                                   _order=np.concatenate([np.nonzero(ext_tile)[0], np.nonzero(~ext_tile)[0]]))
+    return TilePlan(next_tiles=int(ext_tile.sum()), N=N, n=n, TX=TX, TY=TY, U=U, V=V, NE=NE, nlay=nlay, ntiles=nt, tiles=tiles, elem=elem,
                     slot_ext=slot_ext, ext_slots=ext_slots,
                     gt=gtp, gts=gts, mts=mts, nodes=nodes, code=code.astype(np.int32), nslot=nslot,
                     slot_col=shared_cols.astype(np.int32), slot_row0=slot_row0.astype(np.int32),

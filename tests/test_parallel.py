@@ -94,14 +94,14 @@ def test_local_to_global_map_and_counts():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_pipeline_matches_single_mesh(world):
+@pytest.mark.parametrize("world,nxp", [(2, 2), (3, 2), (2, 6)])
+def test_slab_pipeline_matches_single_mesh(world, nxp):
     import torch
 
     from cases import rel_l2
     from paper_2311_11425_b200 import euler, hyperdiff, mesh as hm, metrics, state, synthetic
 
-    nxp, ny, nv, N = 2, 3, 2, 4
+    ny, nv, N = 3, 2, 4
     esz = (100.0, 120.0, 50.0)
     ext = (esz[0] * nxp * world, esz[1] * ny, esz[2] * nv)
     cfg = hyperdiff.HyperDiffConfig(alpha=2, c=(0.05, 0.05, 0.0))
@@ -114,6 +114,10 @@ def test_slab_pipeline_matches_single_mesh(world):
     layouts = [parallel.SlabLayout(r, world, nxp, ny, nv, N, elem_size=esz) for r in range(world)]
     ops = parallel.setup_loopback(layouts, cfg, 0.5)
     maps = [L.local_to_global(op.mesh, g) for L, op in zip(layouts, ops)]
+    for op in ops:   # interface tiles first; with nxp = 6 the interior launch is not empty
+        assert 0 < op.next_tiles <= op.plan.ntiles
+        if nxp == 6:
+            assert op.next_tiles < op.plan.ntiles
     # slab mass / projected metrics equal the single-mesh ones (rank-order sums)
     for op, l2g in zip(ops, maps):
         assert rel_l2(op.ops.mass.d_M.cpu().numpy(), gops.mass.M[l2g]) <= 1e-15
