@@ -249,13 +249,22 @@ class SlabHyperDiffusion:
         _lib.check(_lib.lib().hv_lap_finish(C.byref(self.plan), dst.data_ptr(), ldo, len(of), oa, scale, zmask, 0,
                                             _lib.stream_handle()))
 
-    # ---- one process per GPU: interface tiles, exchange overlapped with the interior tiles
+    # ---- one process per GPU: the interface tiles on a high-priority side stream, their sums
+    # shipped as soon as they are packed, while the interior tiles run on the compute stream
     def apply(self, q, out, transport):
+        torch = torch_mod()
+        main = torch.cuda.current_stream()
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(priority=-1)
+        side = self._side
         for k in range(self.cfg.alpha):
-            self.pass_local(k, q, out, "ext")
-            send, recv = self.halo
-            works = transport.start(send, recv)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self.pass_local(k, q, out, "ext")
+                send, recv = self.halo
+                works = transport.start(send, recv)
             self.pass_local(k, q, out, "int")
+            main.wait_stream(side)
             transport.wait(works)
             self.pass_finish()
         return out
