@@ -631,7 +631,7 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
 namespace hv {
 
 bool plane_supported(int N, int TX, int TY, int F) {
-  if (N == 7) return F == 4 && TX == 2 && TY == 2;     // split planes (H = 2)
+  if (N == 7) return F == 4 && ((TX == 2 && TY == 2) || (TX == 1 && TY == 1));   // split planes
   return (F == 1 || F == 4 || F == 5) && TX == 2 && TY == 2 && N >= 1 && N <= 4;
 }
 
@@ -642,7 +642,8 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
     if (F == 4) return run_plane<NN_ + 1, 2, 2, 4>(A, Drow, st);  \
     if (F == 5) return run_plane<NN_ + 1, 2, 2, 5>(A, Drow, st);  \
   }
-  if (N == 7 && F == 4) return run_plane<8, 2, 2, 4>(A, Drow, st);
+  if (N == 7 && F == 4 && A.TX == 2) return run_plane<8, 2, 2, 4>(A, Drow, st);
+  if (N == 7 && F == 4 && A.TX == 1) return run_plane<8, 1, 1, 4>(A, Drow, st);
   HV_PLANE_CASE(1)
   HV_PLANE_CASE(2)
   HV_PLANE_CASE(3)

@@ -106,10 +106,10 @@ class EulerOps:
                 torch = torch_mod()
                 tp, d = ta
                 Wt = torch.empty(tp.ntiles * tp.nlay * 6 * n * tp.NE * n * n, dtype=torch.float64, device="cuda")
-                # plane-owner kernel (lap_plane.cu) for N <= 4 (and N = 7 with HV_N7_KERNEL=plane),
-                # line-tile kernel otherwise;
+                # plane-owner kernel (lap_plane.cu) for N <= 4 and N = 7 (split planes; the line
+                # kernel with HV_N7_KERNEL=line), line-tile kernel otherwise;
                 # HV_KERNEL=line forces the line-tile kernel (cross-checks)
-                n7p = dev.N == 7 and os.environ.get("HV_N7_KERNEL", "") == "plane"
+                n7p = dev.N == 7 and os.environ.get("HV_N7_KERNEL", "") != "line"
                 layout = 1 if (os.environ.get("HV_KERNEL", "") != "line" and (dev.N <= 4 or n7p)) else 0
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
                                                           d["elem"].data_ptr(), W.data_ptr(), dev.nloc, layout,

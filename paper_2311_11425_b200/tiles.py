@@ -25,11 +25,11 @@ __all__ = ["TilePlan", "build_tile_plan", "tile_shape"]
 
 def tile_shape(N, F=4):
     """(TX, TY) of the compiled sweep kernels: 2x2 columns for the plane-owner kernel
-    (lap_plane.cu) and the line kernel (lap_tile.cu); single columns for the N = 7 line
-    kernel (the 6-component metric of an N = 7 element is 24.6 KB: 1x1 tiles keep two CTAs
-    per SM).  ``HV_N7_KERNEL=plane`` selects 2x2 tiles and the split-plane kernel at N = 7
-    (measured slower on c4)."""
-    if N == 7 and os.environ.get("HV_N7_KERNEL", "") != "plane":
+    (lap_plane.cu, N <= 4) and the line kernel (lap_tile.cu, N = 5, 6); single columns at
+    N = 7 (the 6-component metric of an N = 7 element layer is 24.6 KB), where the default is
+    the split-plane kernel (H = 4); ``HV_N7_KERNEL=plane2x2`` selects 2x2 tiles for it
+    (measured slower)."""
+    if N == 7 and os.environ.get("HV_N7_KERNEL", "") != "plane2x2":
         return (1, 1)
     return (2, 2)
 

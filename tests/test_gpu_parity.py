@@ -339,11 +339,12 @@ def test_diagnostics_device(cname):
                 (s, k, d[k], v)
 
 
-@pytest.mark.parametrize("split", ["4", "2"])
-def test_n7_split_plane_kernel(monkeypatch, split):
-    """The opt-in split-plane sweep at N = 7 (HV_N7_KERNEL=plane, 2x2 tiles, H lanes per plane
-    exchanging xi lines by shuffles) against the oracle and the reference golden."""
-    monkeypatch.setenv("HV_N7_KERNEL", "plane")
+@pytest.mark.parametrize("kernel,split,tile", [("", "4", (1, 1)), ("", "2", (1, 1)), ("plane2x2", "4", (2, 2)),
+                                               ("plane2x2", "2", (2, 2)), ("line", "4", (1, 1))])
+def test_n7_sweep_kernels(monkeypatch, kernel, split, tile):
+    """The N = 7 sweeps: split-plane kernel (H lanes per plane exchanging xi lines by shuffles)
+    on 1x1 (default) and 2x2 tiles, and the line kernel, against the oracle and the golden."""
+    monkeypatch.setenv("HV_N7_KERNEL", kernel)
     monkeypatch.setenv("HV_N7_SPLIT", split)
     from oracle_cases import OracleProblem
     from product_cases import ProductProblem
@@ -351,7 +352,7 @@ def test_n7_split_plane_kernel(monkeypatch, split):
 
     p = ProductProblem("box_n7")
     plan = p.ops.lap_plan(p.vm)
-    assert plan.kernel == 1 and (plan.TX, plan.TY) == (2, 2)
+    assert plan.kernel == (0 if kernel == "line" else 1) and (plan.TX, plan.TY) == tile
     o = OracleProblem("box_n7")
     got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
     assert rel_l2(got, o.hyper()) <= TOL
