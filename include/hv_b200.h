@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define HV_ABI_VERSION 2
+#define HV_ABI_VERSION 3
 
 #define HV_OK 0
 #define HV_ERR_INVALID 1        /* ValueError: bad argument / config                  */
@@ -204,7 +204,8 @@ int hv_euler_setup(int N, const double* h_D, int64_t nelem, const int32_t* d_gid
  * 159-224): element fluxes -> flat-order DSS -> Minv.  out (nglobal, ldo>=5)
  * receives the 5 tendencies (accumulate != 0: added). d_work >= 5*nelem*n^3. */
 int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int coriolis, double P_A, double R, double gamma,
-                 double omega, int64_t nelem, int64_t nglobal, const int32_t* d_gid, const double* d_w3,
+                 double omega, int64_t nelem, int64_t nglobal, const int32_t* d_gid, const int32_t* d_elem_layer,
+                 int nlay, const double* d_w3,
                  const double* d_M, const int64_t* d_off, const int32_t* d_idx, const double* d_Minv,
                  const double* d_q, int64_t ldq, double* d_work, double* d_out, int64_t ldo, int accumulate,
                  void* stream);
@@ -238,6 +239,14 @@ int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int M, int32_t
                       void* stream);
 int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_t nb, int kl, int ku, int M, double* d_x,
                   void* stream);
+
+/* hv_euler_rhs on a single-column tile plan (the N = 7 plan): the element accumulators of
+ * each column are assembled on chip (vertical DSS carried between layers, tile-owned nodes
+ * finished in the sweep, side-face nodes via partial rows + the fixed-order slot fix-up), no
+ * (5 x nloc) work array.  d_elem: (ntiles, nlay) element of each tile layer. */
+int hv_euler_rhs_tiles(const hv_lap_plan* plan, const int32_t* d_elem, const double* d_w3, int set_id, int dirs,
+                       int coriolis, double P_A, double R, double gamma, double omega, const double* d_M,
+                       const double* d_q, int64_t ldq, double* d_out, int64_t ldo, int accumulate, void* stream);
 
 /* EulerOps.diagnostics (euler.py:421-456): d_out[7] = mass, energy_internal, energy_kinetic,
  * energy_potential, energy_total, p_surface_min, w_vertical_max.  d_M: the global mass (nglobal),

@@ -102,14 +102,16 @@ _SIGS = {
     "hv_elem_deriv": (C.c_int, [C.c_int, _P, _P, _I64, _P, C.c_int, C.c_int, _P, _P]),
     "hv_lap_local_tiles": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, C.c_uint32,
                                      C.c_int, _I64, _I64, C.c_int, _P]),
-    "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, _P,
-                               _P, _P, _P, _P, _I64, _P, _P, _I64, C.c_int, _P]),
+    "hv_euler_rhs_tiles": (C.c_int, [C.POINTER(LapPlan), _P, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _P, _P,
+                                     _I64, _P, _I64, C.c_int, _P]),
+    "hv_euler_rhs": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.c_int, _D, _D, _D, _D, _I64, _I64, _P, _P, C.c_int,
+                               _P, _P, _P, _P, _P, _P, _I64, _P, _P, _I64, C.c_int, _P]),
     # test hook (host build of the metric arithmetic); never used by the product path
     "hv_debug_metric_terms_host": (C.c_int, [C.c_int, C.c_int, _P, _P, _I64, _P, _P, _P]),
 }
 
 _lib = None
-ABI_VERSION = 2          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
+ABI_VERSION = 3          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
 
 
 def lib():

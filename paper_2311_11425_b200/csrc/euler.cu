@@ -21,8 +21,10 @@
 
 #include "hv_common.h"
 #include "lap_common.cuh"
+#include "lap_tile.cuh"
 
 namespace hv {
+int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
 int dss_minv_accumulate(const double* work, int64_t nloc, const int64_t* off, const int32_t* idx, const double* Minv,
                         int64_t ng, double* out, int64_t ldo, int nf, bool accumulate, cudaStream_t st);
 }
@@ -93,17 +95,18 @@ __global__ void __launch_bounds__(512) euler_setup_kernel(hv::DTab<n> Dt, int64_
   }
 }
 
+// One element's RHS accumulator at node t (all threads of the CTA call it: it holds a CTA
+// barrier).  Phase 1: gather, EOS, contravariant velocities, fluxes into shared memory;
+// phase 2: weak / strong line sums, geopotential, Coriolis -> acc[5] (valid for t < n^3).
 template <int n>
-__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
-                                                         const int32_t* __restrict__ gid, const double* __restrict__ w3,
-                                                         const double* __restrict__ Mt, const double* __restrict__ q,
-                                                         int64_t ldq, double* __restrict__ work) {
+__device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const EulerConsts& K, int64_t nelem,
+                                               int64_t e, int t, const int32_t* __restrict__ gid,
+                                               const double* __restrict__ w3, const double* __restrict__ Mt,
+                                               const double* __restrict__ q, int64_t ldq, double* sm,
+                                               double (&acc)[5], int& g_out, int layer, int nlay) {
   constexpr int nn = n * n * n;
-  extern __shared__ double sm[];
   // 2C / 3C: per direction m: [0] w3*F_rho, [1] w3*F_thermo (weak), [2..4] momentum fluxes (strong)
   // 2NC: [0..2] w3*F_rho per m (weak), [3..7] u, v, w, theta, P (strong derivatives)
-  const int64_t e = blockIdx.x;
-  const int t = threadIdx.x;
   const bool act = t < nn;
   const int64_t nloc = nelem * nn;
   const int64_t p = e * nn + (act ? t : 0);
@@ -111,6 +114,7 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
   double qv[5] = {0, 0, 0, 0, 0}, gm[3][3] = {}, Jg = 0, mask = 0, dphi[3] = {}, phi = 0, P = 0, un[3] = {};
   if (act) {
     const int g = gid[p];
+    g_out = g;
 #pragma unroll
     for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
 #pragma unroll
@@ -118,10 +122,12 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
 #pragma unroll
       for (int c = 0; c < 3; ++c) gm[m][c] = Mt[(m * 3 + c) * nloc + p];
     Jg = Mt[M_JG * nloc + p];
-    mask = Mt[M_MASK * nloc + p];
+    // flux mask (mesh.py:141-143): zero on the bottom and top levels of every column, i.e. at
+    // k = 0 of the first layer and k = N of the last one (derived, not read from the record)
+    mask = ((layer == 0 && k == 0) || (layer == nlay - 1 && k == n - 1)) ? 0.0 : 1.0;
 #pragma unroll
     for (int m = 0; m < 3; ++m) dphi[m] = Mt[(M_DPHI + m) * nloc + p];
-    phi = Mt[M_PHI * nloc + p];
+    if (K.set == 2) phi = Mt[M_PHI * nloc + p];   // the geopotential enters the 3C pressure only
     const double rho = qv[0];
     // EOS (state.py:84-101), reference expression order
     if (K.set == 0) P = K.P_A * pow(qv[0] * K.R * qv[4] / K.P_A, K.gamma);
@@ -140,7 +146,8 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
   }
   const double w = act ? w3[t] : 0.0;
   const double wj = w * Jg;
-  double acc[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int f = 0; f < 5; ++f) acc[f] = 0.0;
   if (K.set != 0) {
     const double tflux = (K.set == 1) ? qv[4] / qv[0] : (qv[4] + P) / qv[0];
     double* s = sm;  // [m][5][nn]
@@ -239,8 +246,99 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
     acc[2] -= wj * 2.0 * K.omega * cy;
     acc[3] -= wj * 2.0 * K.omega * cz;
   }
+}
+
+template <int n>
+__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
+                                                         const int32_t* __restrict__ gid, const double* __restrict__ w3,
+                                                         const double* __restrict__ Mt, const double* __restrict__ q,
+                                                         int64_t ldq, double* __restrict__ work,
+                                                         const int32_t* __restrict__ elem_layer, int nlay) {
+  constexpr int nn = n * n * n;
+  extern __shared__ double sm[];
+  const int64_t e = blockIdx.x;
+  const int t = threadIdx.x;
+  double acc[5];
+  int g = 0;
+  euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, elem_layer[e], nlay);
+  if (t >= nn) return;
+  const int64_t nloc = nelem * nn;
+  const int64_t p = e * nn + t;
 #pragma unroll
   for (int f = 0; f < 5; ++f) work[f * nloc + p] = acc[f];
+}
+
+// Column sweep of the Euler RHS on single-column tiles (the N = 7 tile plan, tiles.py): one
+// CTA per element column walks the layers; each layer's element accumulator comes from
+// euler_node_acc, then the DSS happens on chip: the top level is carried (shared memory,
+// double-buffered by layer parity) into the next layer's bottom level, nodes of the column's
+// interior (tile-owned) columns get Minv * acc written (or added) to the output row, nodes on
+// the element's side faces (shared with neighbouring columns) write 5-wide partial rows that
+// slot_fixup sums in fixed order.  Replaces the element kernel + CSR DSS round trip of the
+// (5 x nloc) work array.
+template <int n>
+__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::DTab<n> Dt, EulerConsts K, int64_t nelem,
+                                                         const int32_t* __restrict__ gid, const double* __restrict__ w3,
+                                                         const double* __restrict__ Mt, const double* __restrict__ q,
+                                                         int64_t ldq, hv::TileArgs A,
+                                                         const int32_t* __restrict__ elem) {
+  constexpr int nn = n * n * n, N = n - 1;
+  extern __shared__ double sm[];
+  double* s_carry = sm + 15 * nn;                 // [2][n*n][5]
+  int* s_code = reinterpret_cast<int*>(s_carry + 2 * n * n * 5);   // [n*n]
+  const int64_t tl = blockIdx.x;
+  const int t = threadIdx.x;
+  const int i = t / (n * n), j = (t / n) % n, k = t % n;
+  const int nlay = A.nlay;
+  if (t < n * n) s_code[t] = A.code[tl * n * n + t];
+  const double* Mt_t = A.Mt + tl * (int64_t)nlay * (((nn + 1) & ~1));
+  for (int l = 0; l < nlay; ++l) {
+    const int64_t e = elem[tl * nlay + l];
+    double acc[5];
+    int g = 0;
+    euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, l, nlay);
+    if (t < nn) {
+      double* cw = s_carry + (l & 1) * n * n * 5 + (i * n + j) * 5;
+      const double* cr = s_carry + ((l + 1) & 1) * n * n * 5 + (i * n + j) * 5;
+      if (k == 0 && l > 0) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) acc[f] = cr[f] + acc[f];   // previous layer's top first
+      }
+      if (k == N && l < nlay - 1) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) cw[f] = acc[f];
+      } else {
+        const int cd = s_code[i * n + j];
+        const int z = l * N + k;
+        if (cd < 0) {
+          const double m = A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t];
+          double* o = A.out + (int64_t)g * A.ldo;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) o[f] = A.accumulate ? o[f] + m * acc[f] : m * acc[f];
+        } else {
+          double* o = A.part + ((int64_t)cd * A.n_z + z) * 5;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) o[f] = acc[f];
+        }
+      }
+    }
+    // the next layer's phase-1 barrier orders the carry / scratch reuse
+  }
+}
+
+template <int n>
+int run_tile(const double* Drow, const EulerConsts& K, int64_t nelem, const int32_t* gid, const double* w3,
+             const double* Mt, const double* q, int64_t ldq, const hv::TileArgs& A, const int32_t* elem,
+             cudaStream_t st) {
+  hv::DTab<n> Dt;
+  hv::fill_dtab(Dt, Drow);
+  constexpr int nn = n * n * n;
+  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n * 5) + sizeof(int) * n * n;
+  auto kern = euler_tile_kernel<n>;
+  HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)A.ntiles, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
 }
 
 template <int n>
@@ -258,14 +356,15 @@ int run_setup(const double* Drow, int64_t nelem, const int32_t* gid, const doubl
 
 template <int n>
 int run_elem(const double* Drow, const EulerConsts& K, int64_t nelem, const int32_t* gid, const double* w3,
-             const double* Mt, const double* q, int64_t ldq, double* work, cudaStream_t st) {
+             const double* Mt, const double* q, int64_t ldq, double* work, const int32_t* elem_layer, int nlay,
+             cudaStream_t st) {
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;
   const size_t smem = sizeof(double) * 15 * nn;
   auto kern = euler_elem_kernel<n>;
   if (smem > 48 * 1024) HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)nelem, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, work);
+  kern<<<(unsigned)nelem, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, work, elem_layer, nlay);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
@@ -292,23 +391,24 @@ extern "C" int hv_euler_setup(int N, const double* h_D, int64_t nelem, const int
 
 extern "C" int hv_euler_rhs(int N, const double* h_D, int set_id, int dirs, int coriolis, double P_A, double R,
                             double gamma, double omega, int64_t nelem, int64_t nglobal, const int32_t* d_gid,
+                            const int32_t* d_elem_layer, int nlay,
                             const double* d_w3, const double* d_M, const int64_t* d_off, const int32_t* d_idx,
                             const double* d_Minv, const double* d_q, int64_t ldq, double* d_work, double* d_out,
                             int64_t ldo, int accumulate, void* stream) {
   if (N < 1 || N > 7 || set_id < 0 || set_id > 2 || dirs <= 0 || dirs > 7 || !d_q || !d_out || !d_work || ldq < 5 ||
-      ldo < 5)
+      ldo < 5 || !d_elem_layer || nlay < 1)
     HV_FAIL(HV_ERR_INVALID, "hv_euler_rhs: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   EulerConsts K{P_A, R, gamma, omega, set_id, dirs, coriolis};
   int rc;
   switch (N + 1) {
-    case 2: rc = run_elem<2>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    case 3: rc = run_elem<3>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    case 4: rc = run_elem<4>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    case 5: rc = run_elem<5>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    case 6: rc = run_elem<6>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    case 7: rc = run_elem<7>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
-    default: rc = run_elem<8>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, st); break;
+    case 2: rc = run_elem<2>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    case 3: rc = run_elem<3>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    case 4: rc = run_elem<4>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    case 5: rc = run_elem<5>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    case 6: rc = run_elem<6>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    case 7: rc = run_elem<7>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
+    default: rc = run_elem<8>(h_D, K, nelem, d_gid, d_w3, d_M, d_q, ldq, d_work, d_elem_layer, nlay, st); break;
   }
   if (rc) return rc;
   const int n = N + 1;
@@ -592,4 +692,33 @@ extern "C" int hv_euler_diagnostics(int set_id, double P_A, double R, double gam
   diag_final_kernel<<<1, DIAG_T, 0, st>>>(d_work, set_id, d_out);
   HV_LAUNCH_CHECK();
   return HV_OK;
+}
+
+extern "C" int hv_euler_rhs_tiles(const hv_lap_plan* P, const int32_t* d_elem, const double* d_w3, int set_id,
+                                  int dirs, int coriolis, double P_A, double R, double gamma, double omega,
+                                  const double* d_M, const double* d_q, int64_t ldq, double* d_out, int64_t ldo,
+                                  int accumulate, void* stream) {
+  if (!P || !P->d_gt || !P->d_Mt || !P->d_part || !d_elem || !d_w3 || P->TX != 1 || P->TY != 1 || set_id < 0 ||
+      set_id > 2 || dirs <= 0 || dirs > 7 || !d_q || !d_out || ldq < 5 || ldo < 5 || !d_M || P->N < 1 || P->N > 7)
+    HV_FAIL(HV_ERR_INVALID, "hv_euler_rhs_tiles: needs a single-column tile plan and valid arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  EulerConsts K{P_A, R, gamma, omega, set_id, dirs, coriolis};
+  hv::TileArgs A{};
+  A.TX = 1; A.TY = 1; A.nlay = P->nlay; A.n_z = P->n_z;
+  A.ntiles = P->ntiles; A.nslot = P->nslot; A.tile0 = 0; A.tile1 = P->ntiles;
+  A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
+  A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
+  A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = d_q; A.ldq = ldq; A.ldo = ldo;
+  for (int f = 0; f < 5; ++f) A.of.f[f] = f;
+  A.zero_mask = 0; A.accumulate = accumulate; A.scale = 1.0; A.out = d_out; A.part = P->d_part;
+  int rc;
+#define HV_ET(NN_) \
+  case NN_: rc = run_tile<NN_>(P->D, K, P->nelem, P->d_gid, d_w3, d_M, d_q, ldq, A, d_elem, st); break;
+  switch (P->N + 1) {
+    HV_ET(2) HV_ET(3) HV_ET(4) HV_ET(5) HV_ET(6) HV_ET(7) HV_ET(8)
+    default: HV_FAIL(HV_ERR_UNSUPPORTED, "hv_euler_rhs_tiles: N=%d", P->N);
+  }
+#undef HV_ET
+  if (rc) return rc;
+  return hv::slot_fixup(A, 5, st);   // shared side-face nodes: fixed-order sums of the partial rows
 }

@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import os
 
+import ctypes as C
+
 import numpy as np
 
 from . import _lib
@@ -167,6 +169,38 @@ class EulerOps:
             self._h["euler_M"] = M
         return self._h["euler_M"]
 
+    def _euler_tile_plan(self):
+        """hv_lap_plan carrying the single-column tile plan for hv_euler_rhs_tiles (N = 7), or None."""
+        if "euler_tiles" not in self._h:
+            self._h["euler_tiles"] = None
+            ta = self._tile_arrays()
+            if ta is not None and os.environ.get("HV_EULER_TILES", "1") != "0" and not self.ext_cols:
+                tp, d = ta
+                if tp.TX == 1 and tp.TY == 1:
+                    torch = torch_mod()
+                    dev = self.mesh.device()
+                    p = _lib.LapPlan()
+                    p.N = dev.N
+                    n = dev.n
+                    for i in range(n):
+                        for a in range(n):
+                            p.D[i * n + a] = float(dev.D[i, a])
+                    p.nelem, p.nglobal = dev.nelem, dev.nglobal
+                    p.d_gid, p.d_Minv = dev.gid32.data_ptr(), self.mass.d_Minv.data_ptr()
+                    p.TX, p.TY, p.nlay, p.n_z = 1, 1, tp.nlay, tp.n_z
+                    p.ntiles, p.nslot = tp.ntiles, tp.nslot
+                    p.d_gt, p.d_code, p.d_tmeta = d["gt"].data_ptr(), d["code"].data_ptr(), d["tmeta"].data_ptr()
+                    p.d_slot_col, p.d_slot_row0 = d["slot_col"].data_ptr(), d["slot_row0"].data_ptr()
+                    p.d_slot_nc, p.d_col_gid = d["slot_nc"].data_ptr(), d["col_gid"].data_ptr()
+                    Mt = torch.empty(tp.ntiles * tp.nlay * tp.mts, dtype=torch.float64, device="cuda")
+                    _lib.check(_lib.lib().hv_tile_pack_minv(tp.ntiles * tp.nlay, tp.gts, tp.mts, d["gt"].data_ptr(),
+                                                            self.mass.d_Minv.data_ptr(), Mt.data_ptr(),
+                                                            _lib.stream_handle()))
+                    p.d_Mt, p.d_part = Mt.data_ptr(), d["part"].data_ptr()
+                    elem = d["elem"].reshape(tp.ntiles, tp.nlay).contiguous()
+                    self._h["euler_tiles"] = (p, [Mt, elem], elem)
+        return self._h["euler_tiles"]
+
     def _rhs(self, state, dirs, coriolis, out=None, accumulate=False):
         from .hyperdiff import _as_device
 
@@ -177,13 +211,24 @@ class EulerOps:
             raise ValueError("state data must be (nglobal, 5)")
         dev = self.mesh.device()
         M = self._euler_record()
-        work, _ = self._workspace()
         if out is None:
             out = torch.empty_like(q)
         k = self.c
+        et = self._euler_tile_plan()
+        if et is not None:
+            p, _, elem = et
+            _lib.check(_lib.lib().hv_euler_rhs_tiles(
+                C.byref(p), elem.data_ptr(), dev.w3.data_ptr(), self._SETS[self.set_name], dirs, coriolis, k.P_A, k.R,
+                k.gamma, k.omega, M.data_ptr(), q.data_ptr(), 5, out.data_ptr(), 5, int(bool(accumulate)),
+                _lib.stream_handle()))
+            return out, host
+        work, _ = self._workspace()
+        if "elem_layer" not in self._h:
+            self._h["elem_layer"] = to_dev(np.ascontiguousarray(self.mesh.elem_layer, dtype=np.int32))
         _lib.check(_lib.lib().hv_euler_rhs(
             dev.N, dev.D.ctypes.data, self._SETS[self.set_name], dirs, coriolis, k.P_A, k.R, k.gamma, k.omega,
-            dev.nelem, dev.nglobal, dev.gid32.data_ptr(), dev.w3.data_ptr(), M.data_ptr(), dev.off.data_ptr(),
+            dev.nelem, dev.nglobal, dev.gid32.data_ptr(), self._h["elem_layer"].data_ptr(),
+            self.mesh.cfg.n_elem_vertical, dev.w3.data_ptr(), M.data_ptr(), dev.off.data_ptr(),
             dev.idx.data_ptr(), self.mass.d_Minv.data_ptr(), q.data_ptr(), 5, work.data_ptr(), out.data_ptr(), 5,
             int(bool(accumulate)), _lib.stream_handle()))
         return out, host

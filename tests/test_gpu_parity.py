@@ -384,3 +384,37 @@ def test_column_apply(pair):
         got = ops.column_apply(rs[p.m.col_gid])
         ref = o.euler(s).rhs_vertical(rs)[p.m.col_gid]
         assert rel_l2(got, ref) <= TOL, s
+
+
+def test_euler_column_sweep_vs_element_path(monkeypatch):
+    """N = 7 (single-column tile plan): the column-sweep Euler RHS (hv_euler_rhs_tiles, on-chip
+    vertical DSS + fixed-order slot fix-up) against the element kernel + CSR DSS path and the
+    oracle, all sets, S and H (with and without accumulation)."""
+    import torch
+
+    from cases import random_state
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import euler, state
+
+    p = ProductProblem("box_n7")
+    o = OracleProblem("box_n7")
+    for s in ("2C", "2NC", "3C"):
+        ops = euler.EulerOps(p.m, p.mets, p.consts, s)
+        assert ops._euler_tile_plan() is not None
+        q = torch.from_numpy(random_state(p.m.nglobal, s)).cuda()
+        full = ops.rhs_full(state.StateField(s, q)).cpu().numpy()
+        hor = ops.rhs_horizontal(state.StateField(s, q), with_hyperdiff=False).cpu().numpy()
+        acc = torch.ones_like(q)
+        ops._rhs(q, 7, 0, out=acc, accumulate=True)
+        monkeypatch.setenv("HV_EULER_TILES", "0")
+        ops2 = euler.EulerOps(p.m, p.mets, p.consts, s)
+        assert ops2._euler_tile_plan() is None
+        full2 = ops2.rhs_full(state.StateField(s, q)).cpu().numpy()
+        hor2 = ops2.rhs_horizontal(state.StateField(s, q), with_hyperdiff=False).cpu().numpy()
+        monkeypatch.delenv("HV_EULER_TILES")
+        oe = o.euler(s)
+        rs = q.cpu().numpy()
+        assert rel_l2(full, oe.rhs_full(rs)) <= TOL and rel_l2(full, full2) <= 1e-13, s
+        assert rel_l2(hor, oe.rhs_horizontal_nohd(rs)) <= TOL and rel_l2(hor, hor2) <= 1e-13, s
+        assert rel_l2(acc.cpu().numpy() - 1.0, full) <= 1e-12, s
