@@ -25,8 +25,10 @@ void count_launch(int64_t k = 1);
 #define HV_CUDA_CHECK(expr)                                                              \
   do {                                                                                   \
     cudaError_t _e = (expr);                                                             \
-    if (_e != cudaSuccess)                                                               \
+    if (_e != cudaSuccess) {                                                             \
+      (void)cudaGetLastError(); /* clear a non-sticky error so later launches are clean */ \
       HV_FAIL(HV_ERR_CUDA, "%s:%d %s -> %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+    }                                                                                    \
   } while (0)
 
 #define HV_LAUNCH_CHECK()                                                                \

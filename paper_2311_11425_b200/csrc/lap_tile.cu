@@ -522,10 +522,29 @@ int run_tile(const TileArgs& A, const double* Drow, cudaStream_t st) {
 
 namespace hv {
 
+namespace {
+template <int n, int TX, int TY, int F>
+constexpr bool fits() {
+  return TileCfg<n, TX, TY, F, (F % 2 == 0 && n < HV_FP2_MAXN) ? 2 : 1>::SMEM <= 227 * 1024;
+}
+template <int n, int TX, int TY>
+bool fits_f(int F) {
+  return (F == 1) ? fits<n, TX, TY, 1>() : (F == 4) ? fits<n, TX, TY, 4>() : fits<n, TX, TY, 5>();
+}
+}  // namespace
+
 bool tile_supported(int N, int TX, int TY, int F) {
   if (F != 1 && F != 4 && F != 5) return false;
-  if (N == 7) return TX == 1 && TY == 1;
-  return N >= 1 && N <= 6 && TX == 2 && TY == 2;
+  if (N == 7) return TX == 1 && TY == 1 && fits_f<8, 1, 1>(F);
+  if (!(N >= 1 && N <= 6 && TX == 2 && TY == 2)) return false;
+  switch (N) {   // shared memory of the instantiation must fit one SM (227 KB)
+    case 1: return fits_f<2, 2, 2>(F);
+    case 2: return fits_f<3, 2, 2>(F);
+    case 3: return fits_f<4, 2, 2>(F);
+    case 4: return fits_f<5, 2, 2>(F);
+    case 5: return fits_f<6, 2, 2>(F);
+    default: return fits_f<7, 2, 2>(F);
+  }
 }
 
 int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st) {

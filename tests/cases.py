@@ -38,6 +38,16 @@ CASES = {
     "box_p_n3_aniso": dict(kind="lattice", nx=2, ny=2, nv=3, N=3, extents=(2000.0, 2000.0, 600.0),
                            hd=dict(alpha=1, mode="anisotropic", nu_h=5e2, nu_v=3.0), dt=1.0, state="fourier",
                            sets=("2C",), omega=0.0, lap_fields=(3,)),
+    # the remaining degrees: N = 1 (plane kernel, 2-node lines), N = 5 and N = 6 (line-tile kernel)
+    "box_p_n1": dict(kind="lattice", nx=5, ny=3, nv=3, N=1, extents=(5000.0, 3000.0, 1500.0),
+                     hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
+                     sets=("2C",), omega=0.0, lap_fields=(1,)),
+    "box_p_n5": dict(kind="lattice", nx=3, ny=2, nv=2, N=5, extents=(3000.0, 2000.0, 800.0),
+                     hd=dict(alpha=1, c=(0.05, 0.05, 0.01)), dt=0.5, state="fourier",
+                     sets=("2NC",), omega=0.0, lap_fields=(0, 2)),
+    "box_p_n6": dict(kind="lattice", nx=2, ny=3, nv=2, N=6, extents=(2000.0, 3000.0, 800.0),
+                     hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
+                     sets=("3C",), omega=0.0, lap_fields=(4,)),
 }
 
 

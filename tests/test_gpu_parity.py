@@ -273,12 +273,14 @@ def test_column_system(pair):
         assert np.array_equal(ipiv, g[f"ipiv_{s}"]), s
         rhs = np.random.default_rng(11).standard_normal((24, ops.Mdim))
         x, _ = linalg.banded_solve_batch(ref_band, ipiv, kl, ku, rhs)
-        assert rel_l2(x, g[f"solve_{s}"]) <= 1e-12, (s, rel_l2(x, g[f"solve_{s}"]))
+        # a backward-stable solve: the bar scales with the system's conditioning (~1e4 for the
+        # N = 6 3C columns), so 1e-11 here
+        assert rel_l2(x, g[f"solve_{s}"]) <= 1e-11, (s, rel_l2(x, g[f"solve_{s}"]))
         # our own band end to end: same pivots, solution within tolerance
         ip2, _ = linalg.banded_lu_factor_batch(band, kl, ku)
         assert np.array_equal(ip2, g[f"ipiv_{s}"]), s
         x2, _ = linalg.banded_solve_batch(band, ip2, kl, ku, rhs)
-        assert rel_l2(x2, g[f"solve_{s}"]) <= 1e-12, (s, rel_l2(x2, g[f"solve_{s}"]))
+        assert rel_l2(x2, g[f"solve_{s}"]) <= 1e-11, (s, rel_l2(x2, g[f"solve_{s}"]))
 
 
 def test_band_lu_singular_and_wide():
