@@ -42,8 +42,12 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
 bool use_plane(const hv_lap_plan* P, int nf) {
   return P->d_gt && P->d_Mt && P->kernel == 1 && hv::plane_supported(P->N, P->TX, P->TY, nf);
 }
+// The packed metric of a plan has ONE layout (P->kernel): the line-tile kernel may only run on a
+// line-layout plan; field counts the plane kernel lacks on a plane-layout plan fall back to the
+// element-parallel path.
 bool use_tiles(const hv_lap_plan* P, int nf) {
-  return use_plane(P, nf) || (P->d_gt && P->d_Mt && hv::tile_supported(P->N, P->TX, P->TY, nf));
+  return use_plane(P, nf) ||
+         (P->d_gt && P->d_Mt && P->kernel == 0 && hv::tile_supported(P->N, P->TX, P->TY, nf));
 }
 
 // tile sweep over [t0, t1) (+ packing of the interface sums when pack != 0; no-op on one GPU)

@@ -48,6 +48,14 @@ CASES = {
     "box_p_n6": dict(kind="lattice", nx=2, ny=3, nv=2, N=6, extents=(2000.0, 3000.0, 800.0),
                      hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
                      sets=("3C",), omega=0.0, lap_fields=(4,)),
+    # a single layer (bottom and top level in one element: carries, masks, column DSS)
+    "box_p_1lay": dict(kind="lattice", nx=3, ny=2, nv=1, N=4, extents=(3000.0, 2000.0, 500.0),
+                       hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
+                       sets=("2C", "3C"), omega=0.0, lap_fields=(1,)),
+    # N = 7 on the cubed sphere with rotation (split-plane sweep and Euler column sweep on curved panels)
+    "sphere_n7": dict(kind="sphere", ne=1, nv=2, N=7, radius=6.371e6, z_top=1.0e4,
+                      hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere",
+                      sets=("2C", "3C"), omega=7.292e-5, lap_fields=None),
 }
 
 
