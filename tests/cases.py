@@ -52,6 +52,14 @@ CASES = {
     "box_p_1lay": dict(kind="lattice", nx=3, ny=2, nv=1, N=4, extents=(3000.0, 2000.0, 500.0),
                        hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier",
                        sets=("2C", "3C"), omega=0.0, lap_fields=(1,)),
+    # N = 7 with a single layer (Euler column sweep: no carries, both masked levels in one element)
+    "box_n7_1lay": dict(kind="box", ne=2, nv=1, N=7, extents=(1.0e4, 1.0e4, 2.0e3),
+                        hd=dict(alpha=2, c=(0.02, 0.02, 0.02)), dt=0.1, state="bubble",
+                        sets=("2C", "2NC"), omega=0.0, lap_fields=None),
+    # ragged 2x2 tiles on the sphere (3 elements per panel edge), N = 3
+    "sphere_n3_ragged": dict(kind="sphere", ne=3, nv=2, N=3, radius=6.371e6, z_top=1.0e4,
+                             hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere",
+                             sets=("2C",), omega=7.292e-5, lap_fields=(2,)),
     # N = 7 on the cubed sphere with rotation (split-plane sweep and Euler column sweep on curved panels)
     "sphere_n7": dict(kind="sphere", ne=1, nv=2, N=7, radius=6.371e6, z_top=1.0e4,
                       hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere",
