@@ -1,5 +1,9 @@
 """Small end-to-end run of every device kernel for compute-sanitizer (dev helper)."""
 import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import sys
 
 import numpy as np
 import torch

@@ -1,7 +1,11 @@
 """Time the LHEVI column-system path (Jacobian band + band LU + one solve) on a BASELINE mesh (dev helper).
 
-python tools_time_column.py c2 [ncol]
+python tools/time_column.py c2 [ncol]
 """
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import sys
 import time
 

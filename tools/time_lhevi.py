@@ -1,7 +1,11 @@
 """Time one LHEVI step (eager vs CUDA-graph replay) on a BASELINE mesh (dev helper).
 
-python tools_time_lhevi.py c2 [ARK2]
+python tools/time_lhevi.py c2 [ARK2]
 """
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import sys
 from pathlib import Path
 
@@ -14,7 +18,7 @@ from paper_2311_11425_b200.hevi import LheviGraph, LheviState, step_lhevi
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 tname = sys.argv[2] if len(sys.argv) > 2 else "ARK2"
-z = np.load(Path(__file__).parent / "tests" / "golden" / "lhevi.npz")
+z = np.load(Path(__file__).resolve().parents[1] / "tests" / "golden" / "lhevi.npz")
 
 
 class Tab:

@@ -1,7 +1,11 @@
 """Time the c5 sweep kernel (one Laplacian pass, hv_lap_local) per HV_PLANE_VARIANT (dev helper).
 
-python tools_time_plane.py 0 1 2 3 4   -> ms per launch for each variant and max |diff| vs the first
+python tools/time_plane.py 0 1 2 3 4   -> ms per launch for each variant and max |diff| vs the first
 """
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import ctypes as C
 import os
 import sys
