@@ -224,7 +224,8 @@ int run_jacobian(const double* hD, const double* hw, const ColConsts& K, int64_t
 }
 
 // ---------------------------------------------------------------- band LU / solve
-constexpr int CH = 16;   // columns per retire / load chunk
+constexpr int CH = 4;    // LU: columns per retire / load chunk (small window: more systems per SM)
+constexpr int CHS = 8;   // solve: columns per streamed chunk
 
 struct BandDims {
   int kl, ku, R, M, WC, RS;   // window columns WC = kl + ku + 1 + CH, padded row stride RS (even)
@@ -371,7 +372,7 @@ __device__ __forceinline__ void load_chunk(double* ch, int RS, const double* g, 
   }
 }
 
-// Solve with the factors streamed through shared memory in CH-column chunks (row segments of
+// Solve with the factors streamed through shared memory in CHS-column chunks (row segments of
 // a chunk are contiguous in the band layout: coalesced).  Forward: pivot swap + L column
 // (reference order, a - (l * x) without contraction).  Backward in column order: x_i /= U_ii,
 // then the column's U entries update the rows above (same operations as the reference's row
@@ -386,7 +387,7 @@ __global__ void band_solve_kernel(BandDims B, int64_t nb, const double* __restri
   const int RW = d + 1;                          // chunk rows: U part 0..d (forward uses d+1..d+kl)
   const int RL = B.kl;
   const int CRS = RW | 1;                        // odd column stride of the chunk buffer
-  double* xs = xs_all + (size_t)warp * (B.M + CRS * CH);
+  double* xs = xs_all + (size_t)warp * (B.M + CRS * CHS);
   double* ch = xs + B.M;                         // [col][CRS]
   if (s >= nb) return;
   const double* g = data + s * (int64_t)B.R * B.M;
@@ -395,8 +396,8 @@ __global__ void band_solve_kernel(BandDims B, int64_t nb, const double* __restri
   const int32_t* ip = ipiv + s * (int64_t)B.M;
   __syncwarp();
   // forward: L rows d+1 .. d+kl of each chunk
-  for (int c0 = 0; c0 < B.M - 1; c0 += CH) {
-    const int w = min(CH, B.M - 1 - c0);
+  for (int c0 = 0; c0 < B.M - 1; c0 += CHS) {
+    const int w = min(CHS, B.M - 1 - c0);
     load_chunk(ch, CRS, g, d + 1, RL, c0, w, B.M, lane);
     const int pl = (lane < w) ? ip[c0 + lane] : 0;   // the chunk's pivots, one per lane
     __syncwarp();
@@ -416,8 +417,8 @@ __global__ void band_solve_kernel(BandDims B, int64_t nb, const double* __restri
     }
   }
   // backward, column by column from the last: rows 0 .. d of each chunk (d = diagonal)
-  for (int c1 = B.M; c1 > 0; c1 -= CH) {
-    const int c0 = max(0, c1 - CH), w = c1 - c0;
+  for (int c1 = B.M; c1 > 0; c1 -= CHS) {
+    const int c0 = max(0, c1 - CHS), w = c1 - c0;
     load_chunk(ch, CRS, g, 0, RW, c0, w, B.M, lane);
     __syncwarp();
     for (int jj = w - 1; jj >= 0; --jj) {
@@ -473,13 +474,10 @@ extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int
   if (!d_data || !d_ipiv || !d_info || nb <= 0 || kl < 0 || ku < 0 || M <= 0)
     HV_FAIL(HV_ERR_INVALID, "hv_band_lu_factor: bad arguments");
   const BandDims B = band_dims(kl, ku, M);
-  int wpb = 4;
-  size_t smem = 0;
-  for (; wpb >= 1; --wpb) {
-    smem = sizeof(double) * (size_t)wpb * B.R * B.RS;
-    if (smem <= 200 * 1024) break;
-  }
-  if (wpb < 1) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
+  // one warp (system) per block: the SM packs as many ~35 KB windows as fit (6 at N = 4)
+  const int wpb = 1;
+  const size_t smem = sizeof(double) * (size_t)wpb * B.R * B.RS;
+  if (smem > 227 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
   HV_CUDA_CHECK(cudaFuncSetAttribute(band_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   band_lu_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
                                                                                               d_info);
@@ -493,7 +491,7 @@ extern "C" int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_
     HV_FAIL(HV_ERR_INVALID, "hv_band_solve: bad arguments");
   const BandDims B = band_dims(kl, ku, M);
   const int wpb = 4;
-  const size_t smem = sizeof(double) * (size_t)wpb * (M + ((kl + ku + 1) | 1) * CH);
+  const size_t smem = sizeof(double) * (size_t)wpb * (M + ((kl + ku + 1) | 1) * CHS);
   if (smem > 200 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_solve: system too large (M=%d)", M);
   HV_CUDA_CHECK(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   band_solve_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
