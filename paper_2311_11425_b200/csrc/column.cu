@@ -263,21 +263,49 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
   };
   auto store_cols = [&](int c0, int c1) {
     const int w = c1 - c0, tot = B.R * w;
-    for (int e = lane; e < tot; e += 32) g[(int64_t)(e / w) * B.M + c0 + e % w] = win[(e / w) * B.RS + slot(c0 + e % w)];
+    for (int e = lane; e < tot; e += 32) {
+      const int r = e / w, c = e - r * w;
+      g[(int64_t)r * B.M + c0 + c] = win[r * B.RS + slot(c0 + c)];
+    }
+  };
+  // the next chunk is prefetched into registers one chunk ahead (R * CH <= 32 * PFN)
+  constexpr int PFN = 16;
+  double pf[PFN];
+  int pf_c0 = 0, pf_w = 0;
+  auto prefetch = [&](int c0, int c1) {
+    pf_c0 = c0;
+    pf_w = c1 - c0;
+    const int tot = B.R * pf_w;
+#pragma unroll
+    for (int u = 0; u < PFN; ++u) {
+      const int e = u * 32 + lane;
+      const int r = (pf_w == CH) ? e / CH : e / pf_w, c = (pf_w == CH) ? e % CH : e % pf_w;
+      pf[u] = (e < tot) ? g[(int64_t)r * B.M + c0 + c] : 0.0;
+    }
+  };
+  auto commit = [&]() {
+    const int tot = B.R * pf_w;
+#pragma unroll
+    for (int u = 0; u < PFN; ++u) {
+      const int e = u * 32 + lane;
+      const int r = (pf_w == CH) ? e / CH : e / pf_w, c = (pf_w == CH) ? e % CH : e % pf_w;
+      if (e < tot) win[r * B.RS + slot(pf_c0 + c)] = pf[u];
+    }
   };
   int loaded = min(B.M, B.WC);
   load_cols(0, loaded);
+  if (loaded < B.M) prefetch(loaded, min(B.M, loaded + CH));
   int stored = 0;
   __syncwarp();
   for (int j = 0; j < B.M; ++j) {
     const int jmax = min(B.M - 1, j + B.ku + B.kl);
-    if (jmax >= loaded) {   // retire finished columns [stored, j) and bring in the next chunk
+    if (jmax >= loaded) {   // retire finished columns [stored, j), bring in the prefetched chunk
       store_cols(stored, j);
       stored = j;
-      const int nl = min(B.M, loaded + CH);
       __syncwarp();
-      load_cols(loaded, nl);
-      loaded = nl;
+      commit();
+      loaded = pf_c0 + pf_w;
+      if (loaded < B.M) prefetch(loaded, min(B.M, loaded + CH));
       __syncwarp();
     }
     const int lm = min(B.kl, B.M - 1 - j);
@@ -477,7 +505,8 @@ extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int
   // one warp (system) per block: the SM packs as many ~35 KB windows as fit (6 at N = 4)
   const int wpb = 1;
   const size_t smem = sizeof(double) * (size_t)wpb * B.R * B.RS;
-  if (smem > 227 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
+  if (smem > 227 * 1024 || B.R * CH > 32 * 16)
+    HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
   HV_CUDA_CHECK(cudaFuncSetAttribute(band_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   band_lu_kernel<<<(unsigned)((nb + wpb - 1) / wpb), 32 * wpb, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv,
                                                                                               d_info);
