@@ -19,16 +19,34 @@ namespace {
 
 using hv::TileArgs;
 
+// partial row of F doubles (rows are F-strided, so F = 4 rows are 32-byte aligned: two 16-byte loads)
 template <int F>
-__device__ __forceinline__ void local_sum(const TileArgs& A, int64_t s, int z, double acc[F]) {
+__device__ __forceinline__ void load_row(const double* p, double (&v)[F]) {
+  if constexpr (F == 4) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  } else {
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) v[ff] = __ldg(p + ff);
+  }
+}
+
+template <int F>
+__device__ __forceinline__ void local_sum(const TileArgs& A, int64_t s, int z, double (&acc)[F]) {
   const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
   for (int r = 0; r < nc; ++r) {
-    const double* p = A.part + ((int64_t)(r0 + r) * A.n_z + z) * F;   // partial rows: F doubles
+    double v[F];
+    load_row<F>(A.part + ((int64_t)(r0 + r) * A.n_z + z) * F, v);   // partial rows: F doubles
 #pragma unroll
-    for (int ff = 0; ff < F; ++ff) acc[ff] += p[ff];
+    for (int ff = 0; ff < F; ++ff) acc[ff] += v[ff];
   }
+}
+
+__device__ __forceinline__ void st2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
 template <int F>
@@ -45,11 +63,12 @@ __global__ void slot_pack_kernel(TileArgs A) {
 }
 
 template <int F>
-__global__ void slot_fixup_kernel(TileArgs A) {
+__global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (id >= A.nslot * A.n_z) return;
-  const int64_t s = id / A.n_z;
-  const int z = (int)(id % A.n_z);
+  const unsigned nz = (unsigned)A.n_z;
+  const int64_t s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
+  const int z = (int)((unsigned)id - (unsigned)s * nz);
   const int c = A.slot_col[s];
   const int g = A.col_gid[(int64_t)c * A.n_z + z];
   double acc[F];
@@ -63,11 +82,30 @@ __global__ void slot_fixup_kernel(TileArgs A) {
   }
   double* o = A.out + (int64_t)g * A.ldo;
   const double mi = A.Minv[g];
+  double r[F];
 #pragma unroll
-  for (int ff = 0; ff < F; ++ff) {
-    const double r = A.scale * (mi * acc[ff]);
-    o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r : r;
+  for (int ff = 0; ff < F; ++ff) r[ff] = A.scale * (mi * acc[ff]);
+  if constexpr (F == 4) {
+    if (row_mode == 1) {             // (ng, 4) rows, fields 0..3
+      st2(o, r[0], r[1]);
+      st2(o + 2, r[2], r[3]);
+      return;
+    }
+    if (row_mode == 2) {             // (ng, 5) rows, fields 1..4, column 0 zeroed
+      if ((g & 1) == 0) {
+        st2(o, 0.0, r[0]);
+        st2(o + 2, r[1], r[2]);
+        o[4] = r[3];
+      } else {
+        o[0] = 0.0;
+        st2(o + 1, r[0], r[1]);
+        st2(o + 3, r[2], r[3]);
+      }
+      return;
+    }
   }
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r[ff] : r[ff];
   if (A.zero_mask && !A.accumulate)
     for (int zc = 0; zc < A.ldo; ++zc)
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
@@ -86,7 +124,16 @@ template <int F>
 int fixup_f(const TileArgs& A, cudaStream_t st) {
   if (A.nslot <= 0) return HV_OK;
   const int64_t tot = A.nslot * A.n_z;
-  slot_fixup_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+  if (tot >= (int64_t)1 << 31) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: %lld slot rows", (long long)tot);
+  int row_mode = 0;
+  if (F == 4 && !A.accumulate && A.out && ((uintptr_t)A.out & 15) == 0) {
+    if (A.ldo == 4 && !A.zero_mask && A.of.f[0] == 0 && A.of.f[1] == 1 && A.of.f[2] == 2 && A.of.f[3] == 3)
+      row_mode = 1;
+    else if (A.ldo == 5 && A.zero_mask == 1u && A.of.f[0] == 1 && A.of.f[1] == 2 && A.of.f[2] == 3 &&
+             A.of.f[3] == 4)
+      row_mode = 2;
+  }
+  slot_fixup_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, row_mode);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
