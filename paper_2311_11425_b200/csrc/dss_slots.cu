@@ -32,16 +32,29 @@ __device__ __forceinline__ void load_row(const double* p, double (&v)[F]) {
   }
 }
 
+// fixed-order (r ascending) sum of a slot's partial rows; the first four rows (all of them
+// except at cube corners of fine meshes) are loaded before any is added, so their loads overlap
 template <int F>
 __device__ __forceinline__ void local_sum(const TileArgs& A, int64_t s, int z, double (&acc)[F]) {
+  constexpr int U = 4;
   const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
+  double v[U][F];
+#pragma unroll
+  for (int r = 0; r < U; ++r)
+    if (r < nc) load_row<F>(A.part + ((int64_t)(r0 + r) * A.n_z + z) * F, v[r]);   // partial rows: F doubles
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
-  for (int r = 0; r < nc; ++r) {
-    double v[F];
-    load_row<F>(A.part + ((int64_t)(r0 + r) * A.n_z + z) * F, v);   // partial rows: F doubles
 #pragma unroll
-    for (int ff = 0; ff < F; ++ff) acc[ff] += v[ff];
+  for (int r = 0; r < U; ++r)
+    if (r < nc) {
+#pragma unroll
+      for (int ff = 0; ff < F; ++ff) acc[ff] += v[r][ff];
+    }
+  for (int r = U; r < nc; ++r) {
+    double w[F];
+    load_row<F>(A.part + ((int64_t)(r0 + r) * A.n_z + z) * F, w);
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) acc[ff] += w[ff];
   }
 }
 
@@ -71,6 +84,13 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   const int z = (int)((unsigned)id - (unsigned)s * nz);
   const int c = A.slot_col[s];
   const int g = A.col_gid[(int64_t)c * A.n_z + z];
+  double* o = A.out + (int64_t)g * A.ldo;
+  const double mi = __ldg(A.Minv + g);
+  double prev[F];
+  if (A.accumulate) {
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) prev[ff] = o[A.of.f[ff]];
+  }
   double acc[F];
   local_sum<F>(A, s, z, acc);
   if (A.slot_ext && A.slot_ext[s] >= 0) {
@@ -80,8 +100,6 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
 #pragma unroll
     for (int ff = 0; ff < F; ++ff) acc[ff] = lower_side ? rm[ff] + acc[ff] : acc[ff] + rm[ff];
   }
-  double* o = A.out + (int64_t)g * A.ldo;
-  const double mi = A.Minv[g];
   double r[F];
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) r[ff] = A.scale * (mi * acc[ff]);
@@ -105,7 +123,7 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
     }
   }
 #pragma unroll
-  for (int ff = 0; ff < F; ++ff) o[A.of.f[ff]] = A.accumulate ? o[A.of.f[ff]] + r[ff] : r[ff];
+  for (int ff = 0; ff < F; ++ff) o[A.of.f[ff]] = A.accumulate ? prev[ff] + r[ff] : r[ff];
   if (A.zero_mask && !A.accumulate)
     for (int zc = 0; zc < A.ldo; ++zc)
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
