@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define HV_ABI_VERSION 3
+#define HV_ABI_VERSION 4
 
 #define HV_OK 0
 #define HV_ERR_INVALID 1        /* ValueError: bad argument / config                  */
@@ -108,6 +108,14 @@ int hv_mass_proj_finalize(int64_t nglobal, const double* d_S, double* d_M, doubl
 int hv_viscous_metric(int N, int mode, const double* h_a, double b, const double* h_nu, const double* d_grad,
                       int64_t nelem, const double* d_w3, const double* d_Jg, const int32_t* d_gid32,
                       double* d_Gnu, double* d_lam, double* d_evecs, double* d_W, void* stream);
+/* Axis form of the Laplacian metric for scaled mode with c_1 == c_2 (every BASELINE config):
+ * then G_nu = sum_m k_m e_m e_m^T (hyperdiff.py:80, k_m = nu_m vals_m = a_m / b) collapses to
+ * k_h I + (k_v - k_h) e_3 e_3^T, e_3 the eigenvector of the largest eigenvalue of G (the same
+ * Jacobi eigensolve as hv_viscous_metric), so W = w3 Jg G_nu = kh |u|^2 I + kd u u^T with
+ * u = sqrt(w3 Jg[gid]) e_3: d_U (3, nelem*n^3) component-major, half the bytes of d_W.
+ * Returns HV_ERR_DEGENERATE like hv_viscous_metric. */
+int hv_viscous_axis(int N, const double* d_grad, int64_t nelem, const double* d_w3, const double* d_Jg,
+                    const int32_t* d_gid32, double* d_U, void* stream);
 
 /* ------------------------------------------------------------- hot path
  * Laplacian plan: everything laplacian_apply (hyperdiff.py:84-94) reads. */
@@ -145,6 +153,11 @@ typedef struct hv_lap_plan {
   int face;                    /* column nodes per slab face                                   */
   double* d_send;              /* (2*face, n_z, 5) local interface sums (NCCL send payload)    */
   double* d_recv;              /* (2*face, n_z, 5) neighbour sums (NCCL receive buffer)        */
+  /* form of d_Wt for the plane kernel (kernel == 1): 0 = the 6 components of W;
+   * 1 = axis form (scaled mode with c_1 == c_2, hyperdiff.py:71-80: G_nu = k_h I + (k_v - k_h) e_3 e_3^T):
+   * u = sqrt(w3 Jg[gid]) e_3 (3 components, hv_viscous_axis) and W = kh |u|^2 I + kd u u^T */
+  int wform;
+  double kh, kd;
 } hv_lap_plan;
 
 /* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the
@@ -168,7 +181,8 @@ int hv_lap_finish(const hv_lap_plan* plan, double* d_out, int64_t ldo, int nf, c
 
 /* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
  * (layout 0: line-tile kernel, [t][l][pair][k][e][i*n+j][2]; layout 1: plane kernel,
- * [t][l][pair][i][k][e][j][2]) using d_elem (ntiles, nlay, TX*TY),
+ * [t][l][pair][i][k][e][j][2]; layout 2: plane kernel, axis form, d_W = U (3, nelem*n^3) of
+ * hv_viscous_axis -> [t][l][c][i][k][e][j]) using d_elem (ntiles, nlay, TX*TY),
  * -1 for the absent elements of ragged tiles. */
 /* Minv in tile order: d_Mt[r*mts + c] = d_Minv[d_gt[r*gts + c]] for the rows r = (tile, layer)
  * (0 for absent nodes and padding). */

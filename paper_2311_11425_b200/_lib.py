@@ -65,6 +65,9 @@ class LapPlan(C.Structure):
         ("face", C.c_int),
         ("d_send", _P),
         ("d_recv", _P),
+        ("wform", C.c_int),
+        ("kh", C.c_double),
+        ("kd", C.c_double),
     ]
 
 
@@ -85,6 +88,7 @@ _SIGS = {
     "hv_viscous_metric": (C.c_int, [C.c_int, C.c_int, _P, _D, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "hv_laplacian": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, _P]),
     "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
+    "hv_viscous_axis": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, C.c_int, _P, _P]),
     "hv_lap_local": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, C.c_uint32, C.c_int,
                                _P]),
@@ -111,7 +115,7 @@ _SIGS = {
 }
 
 _lib = None
-ABI_VERSION = 3          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
+ABI_VERSION = 4          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
 
 
 def lib():

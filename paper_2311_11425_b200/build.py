@@ -33,8 +33,9 @@ def _sources():
     return sorted(CSRC.glob("*.cu")), sorted(CSRC.glob("*.cpp"))
 
 
-def _digest():
+def _digest(defines=()):
     h = hashlib.sha256()
+    h.update(" ".join(defines).encode())
     for p in sorted(CSRC.glob("*")) + sorted(INCLUDE.glob("*.h")):
         if p.is_file():
             h.update(p.name.encode())
@@ -53,24 +54,30 @@ def _run(cmd, verbose):
         print(r.stderr, file=sys.stderr)
 
 
-def build(force=False, verbose=False, jobs=None):
-    """Compile every CUDA/C++ source for sm_100a and link libhv_b200.so."""
-    stamp = HERE / "libhv_b200.sha256"
-    dig = _digest()
-    if not force and LIB.exists() and stamp.exists() and stamp.read_text().strip() == dig:
-        return LIB
+def build(force=False, verbose=False, jobs=None, defines=(), lib=None):
+    """Compile every CUDA/C++ source for sm_100a and link libhv_b200.so.
+
+    ``defines``/``lib``: development builds (e.g. ``-DHV_PLANE_ABLATE`` into ablate/libhv_b200.so,
+    loaded with HV_LIB=...) use their own object directory and never replace the product library.
+    """
+    lib_path = Path(lib) if lib else LIB
+    obj_dir = OBJ if not defines else lib_path.parent / "_obj"
+    stamp = lib_path.with_suffix(".sha256")
+    dig = _digest(defines)
+    if not force and lib_path.exists() and stamp.exists() and stamp.read_text().strip() == dig:
+        return lib_path
     nvcc = _nvcc()
-    OBJ.mkdir(exist_ok=True)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     cus, cpps = _sources()
     objs = []
     cmds = []
     for src in cus:
-        obj = OBJ / (src.stem + ".cu.o")
-        cmds.append([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
+        obj = obj_dir / (src.stem + ".cu.o")
+        cmds.append([nvcc, *ARCH, *defines, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fopenmp",
                      "-Xptxas", "-warn-spills", "-I", INCLUDE, "-c", src, "-o", obj])
         objs.append(obj)
     for src in cpps:
-        obj = OBJ / (src.stem + ".cpp.o")
+        obj = obj_dir / (src.stem + ".cpp.o")
         cmds.append(["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-ffp-contract=off", "-I", INCLUDE,
                      "-I", "/usr/local/cuda/include", "-c", src, "-o", obj])
         objs.append(obj)
@@ -78,12 +85,16 @@ def build(force=False, verbose=False, jobs=None):
 
     with ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 2)) as ex:
         list(ex.map(lambda c: _run(c, verbose), cmds))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib_path.with_suffix(".so.tmp")
     _run([nvcc, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", tmp, *objs, "-lgomp"], verbose)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_path)
     stamp.write_text(dig)
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--ablate" in sys.argv:   # development variants (HV_PLANE_VARIANT), tools/time_plane.py with HV_LIB
+        print(build(force="--force" in sys.argv, verbose=True, defines=("-DHV_PLANE_ABLATE",),
+                    lib=HERE.parent / "ablate" / "libhv_b200.so"))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

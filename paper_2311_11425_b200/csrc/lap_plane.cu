@@ -78,7 +78,9 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {
 // index, field).  H = 2 (N = 7: a 64-node plane does not fit in registers): the plane's xi
 // rows are split over two lanes (ih = 0, 1) that exchange the other half of every xi line
 // with warp shuffles; the eta lines of the line-owner role are split by zeta halves.
-template <int n, int TX, int TY, int F, int WV, int H = 1>
+// WF: form of the packed metric.  0: the 6 components of W as 3 pairs; 1: axis form (scaled
+// mode with c_1 == c_2): u = sqrt(w3 Jg) e_3 (3 doubles per node), W d = kh |u|^2 d + kd u (u . d).
+template <int n, int TX, int TY, int F, int WV, int H = 1, int WF = 0>
 struct PlaneCfg {
   static constexpr int N = n - 1;
   static constexpr int U = TX * N + 1, V = TY * N + 1, UV = U * V;
@@ -104,7 +106,7 @@ struct PlaneCfg {
   static constexpr int SP = TUNED ? 588 : pad16(NE * n * n * n);
   static constexpr int SQ = QP * F;
   static constexpr int SE = SP * F;
-  static constexpr int WL = 6 * n * NE * n * n;          // packed metric doubles per tile-layer
+  static constexpr int WL = (WF ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
   static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
   static constexpr int FI = UV * N;                      // output items per layer (k < N)
   static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
@@ -126,9 +128,9 @@ struct PlaneCfg {
 // layer ahead, coalesced from the tile-ordered map), Minv is read coalesced at step e.
 // AB: ablation bit mask for development timing only (0 in production): 1 = no node-owner
 // step (f), 2 = no q gather, 4 = no metric TMA, 8 = no plane arithmetic (steps b-e)
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1>
-__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
-  using C = PlaneCfg<n, TX, TY, F, WV, H>;
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
+__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
+  using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
   constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                                    // [F][QP] gathered q of the current layer
@@ -377,10 +379,43 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
     }
     // ---- c: flux at the plane nodes, weak xi / zeta in registers
     if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)(l & 1));
+    if (run && WF == 1) {
+      // axis form: [c][i][k][e][j]; the F field lanes of a plane read the same u (broadcast)
+      const double* Uw = s_w + e * n + jp;
+      const double kh = A.kh, kd = A.kd;
+      constexpr int CS = n * n * NE * n;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int i = I0 + r;
+        constexpr int KB = (n > 5) ? 1 : n;
+#pragma unroll
+        for (int k0 = 0; k0 < n; k0 += KB) {
+          double d1[KB], u0[KB], u1[KB], u2[KB];
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const int wo = (i * n + k0 + kk) * NE * n;
+            u0[kk] = Uw[wo];
+            u1[kk] = Uw[CS + wo];
+            u2[kk] = Uw[2 * CS + wo];
+            d1[kk] = s_s[sidx(e, i, jp, k0 + kk)];
+          }
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) {
+            const int k = k0 + kk;
+            const double d0 = p0[r][k], d2 = p2[r][k];
+            const double hs = kh * (u0[kk] * u0[kk] + u1[kk] * u1[kk] + u2[kk] * u2[kk]);
+            const double tv = kd * (u0[kk] * d0 + u1[kk] * d1[kk] + u2[kk] * d2);
+            p0[r][k] = hs * d0 + tv * u0[kk];
+            s_s[sidx(e, i, jp, k)] = hs * d1[kk] + tv * u1[kk];
+            p2[r][k] = hs * d2 + tv * u2[kk];
+          }
+        }
+      }
+    }
     if (run) {
       const double* W = (WV == 0) ? s_w + (e * n + jp) * 2 : Wt_t + (int64_t)l * C::WL + (e * n + jp) * 2;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
+      for (int r = 0; r < NR && WF == 0; ++r) {
         const int i = I0 + r;
         // all loads of a row chunk first: one shared-memory round trip per chunk, not per node
         constexpr int KB = (n > 5) ? n / 2 : n;
@@ -560,29 +595,31 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H>::NT, MB) lap_pla
 
 
 // Plane-layout packed metric, component pairs:
-// Wp[t][l][cp][i][k][e][j][h] = W[2cp+h][elem(t,l,e)*n^3 + (i*n + j)*n + k].
+// Wp[t][l][cp][i][k][e][j][h] = W[2cp+h][elem(t,l,e)*n^3 + (i*n + j)*n + k];
+// axis form (axis != 0, W = U (3, nloc)): Wp[t][l][c][i][k][e][j] = U[c][...].
 __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const int32_t* __restrict__ elem,
-                                  const double* __restrict__ W, int64_t nloc, double* __restrict__ Wp) {
-  const int64_t per = (int64_t)6 * n * n * NE * n;
+                                  const double* __restrict__ W, int64_t nloc, int axis, double* __restrict__ Wp) {
+  const int64_t per = (int64_t)(axis ? 3 : 6) * n * n * NE * n;
   const int64_t total = ntiles * nlay * per;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tl = id / per;
     int64_t r = id % per;
-    const int h = (int)(r % 2); r /= 2;
+    int h = 0;
+    if (!axis) { h = (int)(r % 2); r /= 2; }
     const int j = (int)(r % n); r /= n;
     const int e = (int)(r % NE); r /= NE;
     const int k = (int)(r % n); r /= n;
     const int i = (int)(r % n); r /= n;
-    const int c = (int)r * 2 + h;
+    const int c = axis ? (int)r : (int)r * 2 + h;
     const int eg = elem[tl * NE + e];
     Wp[id] = (eg >= 0) ? W[c * nloc + (int64_t)eg * n * n * n + (i * n + j) * n + k] : 0.0;
   }
 }
 
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1>
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
 int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
-  using C = PlaneCfg<n, TX, TY, F, WV, H>;
-  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H>;
+  using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
+  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   if (A.tile1 <= A.tile0) return HV_OK;
   kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
@@ -600,6 +637,10 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   hv::fill_dtab(Dt, Drow);
   if constexpr (n == 8) {
     const char* hs = getenv("HV_N7_SPLIT");
+    if (A.wform == 1) {
+      if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2, 1>(A, Dt, st);
+      return run_plane_v<n, TX, TY, F, 0, 1, 0, 4, 1>(A, Dt, st);
+    }
     if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2>(A, Dt, st);
     return run_plane_v<n, TX, TY, F, 0, 1, 0, 4>(A, Dt, st);
   } else {
@@ -622,6 +663,13 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
       }
     }
 #endif
+    if (A.wform == 1) {
+#ifdef HV_PLANE_ABLATE
+      const char* v = getenv("HV_PLANE_VARIANT");
+      if (v && atoi(v) == 40) return run_plane_v<n, TX, TY, F, 0, 4, 0, 1, 1>(A, Dt, st);
+#endif
+      return run_plane_v<n, TX, TY, F, 0, 3, 0, 1, 1>(A, Dt, st);
+    }
     return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
   }
 }
@@ -653,8 +701,8 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
 }
 
 int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
-               double* Wp, cudaStream_t st) {
-  plane_pack_metric<<<148 * 8, 256, 0, st>>>(N + 1, NE, ntiles, nlay, elem, W, nloc, Wp);
+               int axis, double* Wp, cudaStream_t st) {
+  plane_pack_metric<<<148 * 8, 256, 0, st>>>(N + 1, NE, ntiles, nlay, elem, W, nloc, axis, Wp);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

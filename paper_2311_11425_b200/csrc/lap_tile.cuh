@@ -35,6 +35,8 @@ struct TileArgs {
   int face;                 // column nodes per slab face
   double* send;             // (2 * face, n_z, 5) local sums for the neighbours
   const double* recv;       // (2 * face, n_z, 5) neighbours' sums
+  int wform;                // Wt form (plane kernel): 0 = 6 components, 1 = axis form u (W = kh|u|^2 I + kd u u^T)
+  double kh, kd;
 };
 
 bool tile_supported(int N, int TX, int TY, int F);
@@ -43,7 +45,7 @@ int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
-               double* Wp, cudaStream_t st);
+               int axis, double* Wp, cudaStream_t st);
 int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* gt, const double* Minv, double* Mt, cudaStream_t st);
 int tile_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,

@@ -214,7 +214,7 @@ __global__ void viscous_kernel(int nn, ViscParams P, const double* __restrict__ 
                                const double* __restrict__ w3, const double* __restrict__ Jg,
                                const int32_t* __restrict__ gid, double* __restrict__ Gnu_out,
                                double* __restrict__ lam_out, double* __restrict__ evec_out,
-                               double* __restrict__ W_out) {
+                               double* __restrict__ W_out, double* __restrict__ U_out) {
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= nloc) return;
   const int64_t e = p / nn, r = p % nn;
@@ -260,6 +260,11 @@ __global__ void viscous_kernel(int nn, ViscParams P, const double* __restrict__ 
     for (int c = 0; c < 3; ++c)
 #pragma unroll
       for (int m = 0; m < 3; ++m) evec_out[p * 9 + c * 3 + m] = V[c][m];
+  }
+  if (U_out) {   // axis form (hv_viscous_axis): u = sqrt(w3 Jg) e_3, e_3 = eigenvector of the largest eigenvalue
+    const double su = sqrt(w3[r] * Jg[gid[p]]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) U_out[c * nloc + p] = su * V[c][2];
   }
   if (W_out) {
     const double s = w3[r] * Jg[gid[p]];
@@ -385,7 +390,29 @@ extern "C" int hv_viscous_metric(int N, int mode, const double* h_a, double b, c
   const int64_t nloc = nelem * nn;
   const int T = 128;
   viscous_kernel<<<(unsigned)((nloc + T - 1) / T), T, 0, st>>>(nn, P, d_grad, nloc, d_w3, d_Jg, d_gid32, d_Gnu, d_lam,
-                                                              d_evecs, d_W);
+                                                              d_evecs, d_W, nullptr);
+  HV_LAUNCH_CHECK();
+  unsigned int f[4];
+  rc = read_flags(st, f);
+  if (rc) return rc;
+  if (f[1]) HV_FAIL(HV_ERR_DEGENERATE, "degenerate element: non-positive metric eigenvalue");
+  return HV_OK;
+}
+
+extern "C" int hv_viscous_axis(int N, const double* d_grad, int64_t nelem, const double* d_w3, const double* d_Jg,
+                               const int32_t* d_gid32, double* d_U, void* stream) {
+  if (N < 1 || !d_grad || nelem <= 0 || !d_w3 || !d_Jg || !d_gid32 || !d_U)
+    HV_FAIL(HV_ERR_INVALID, "hv_viscous_axis: bad args");
+  ViscParams P{};
+  P.mode = 1;   // the eigenvectors only; nu unused
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = reset_flags(st);
+  if (rc) return rc;
+  const int n = N + 1, nn = n * n * n;
+  const int64_t nloc = nelem * nn;
+  const int T = 128;
+  viscous_kernel<<<(unsigned)((nloc + T - 1) / T), T, 0, st>>>(nn, P, d_grad, nloc, d_w3, d_Jg, d_gid32, nullptr,
+                                                              nullptr, nullptr, nullptr, d_U);
   HV_LAUNCH_CHECK();
   unsigned int f[4];
   rc = read_flags(st, f);

@@ -107,16 +107,28 @@ class EulerOps:
             if ta is not None:
                 torch = torch_mod()
                 tp, d = ta
-                Wt = torch.empty(tp.ntiles * tp.nlay * 6 * n * tp.NE * n * n, dtype=torch.float64, device="cuda")
                 # plane-owner kernel (lap_plane.cu) for N <= 4 and N = 7 (split planes; the line
                 # kernel with HV_N7_KERNEL=line), line-tile kernel otherwise;
                 # HV_KERNEL=line forces the line-tile kernel (cross-checks)
                 n7p = dev.N == 7 and os.environ.get("HV_N7_KERNEL", "") != "line"
                 layout = 1 if (os.environ.get("HV_KERNEL", "") != "line" and (dev.N <= 4 or n7p)) else 0
+                # axis form of W (3 doubles per node instead of 6) where G_nu = kh I + kd e3 e3^T, for
+                # N <= 4 (the N = 7 split-plane kernel spills with it: c4 6.91 -> 7.04 ms);
+                # HV_WFORM=0 forces the 6-component form (cross-checks), HV_WFORM=1 also at N = 7
+                wf = os.environ.get("HV_WFORM", "")
+                ax = viscous.axis_form() if layout == 1 and wf != "0" and (dev.N <= 4 or wf == "1") else None
+                ncomp = 3 if ax is not None else 6
+                Wt = torch.empty(tp.ntiles * tp.nlay * ncomp * n * tp.NE * n * n, dtype=torch.float64,
+                                 device="cuda")
+                src = viscous.packed_axis(self.metrics.d_Jg) if ax is not None else W
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
-                                                          d["elem"].data_ptr(), W.data_ptr(), dev.nloc, layout,
-                                                          Wt.data_ptr(), _lib.stream_handle()))
+                                                          d["elem"].data_ptr(), src.data_ptr(), dev.nloc,
+                                                          2 if ax is not None else layout, Wt.data_ptr(),
+                                                          _lib.stream_handle()))
                 p.kernel = layout
+                if ax is not None:
+                    p.wform, p.kh, p.kd = 1, ax[0], ax[1]
+                del src
                 p.TX, p.TY, p.nlay, p.n_z = tp.TX, tp.TY, tp.nlay, tp.n_z
                 p.ntiles, p.nslot = tp.ntiles, tp.nslot
                 p.d_gt, p.d_code, p.d_tmeta = d["gt"].data_ptr(), d["code"].data_ptr(), d["tmeta"].data_ptr()

@@ -107,6 +107,29 @@ class ViscousMetric:
     def evecs(self):
         return self._materialise()[2]
 
+    def axis_form(self):
+        """(kh, kd) when G_nu = kh I + kd e_3 e_3^T exactly (scaled mode, c_1 == c_2), else None.
+
+        hyperdiff.py:71-80: k_m = nu_m vals_m = ((a_m lam_m) / b) vals_m = a_m / b to an ulp, so with
+        a_1 == a_2 the two horizontal modes share one coefficient and only e_3 carries geometry.
+        """
+        mode, a, b, _ = self._params
+        if mode != 0 or float(a[0]) != float(a[1]):
+            return None
+        kh = float(a[0]) / float(b)
+        return kh, float(a[2]) / float(b) - kh
+
+    def packed_axis(self, d_Jg):
+        """u = sqrt(w3 Jg[gid]) e_3 (3, nloc) for the axis form of W (hv_viscous_axis); not cached
+        (the plan keeps only its tile-ordered copy)."""
+        torch = torch_mod()
+        dev = self.mesh.device()
+        U = torch.empty((3, dev.nloc), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().hv_viscous_axis(dev.N, self.mets.d_grad.data_ptr(), dev.nelem, dev.w3.data_ptr(),
+                                              d_Jg.data_ptr(), dev.gid32.data_ptr(), U.data_ptr(),
+                                              _lib.stream_handle()))
+        return U
+
     def packed(self, d_Jg):
         """W = w3 Jg[gid] G_nu, 6 components (component-major) for this Jg."""
         key = d_Jg.data_ptr()

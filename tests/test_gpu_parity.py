@@ -173,6 +173,34 @@ def test_tile_path_used_and_matches_element_path(pair):
         assert rel_l2(la, lb) <= 1e-14 and rel_l2(lc, lb) <= 1e-14
 
 
+def test_axis_form_matches_six_components(pair, monkeypatch):
+    """Plane kernel with the axis form of W (u = sqrt(w3 Jg) e_3, scaled mode with c_1 == c_2) equals
+    the 6-component form (HV_WFORM=0) to rounding, and the plan picks the axis form exactly when
+    G_nu = kh I + kd e_3 e_3^T."""
+    name, p, o = pair
+    from paper_2311_11425_b200 import euler, hyperdiff, state
+
+    plan = p.ops.lap_plan(p.vm)
+    ax = p.vm.axis_form()
+    hd = p.cfg
+    assert (ax is not None) == (hd.mode == "scaled" and hd.c[0] == hd.c[1])
+    assert plan.wform == (1 if (ax is not None and plan.kernel == 1) else 0)
+    if plan.wform != 1:
+        pytest.skip("6-component form for this case")
+    monkeypatch.setenv("HV_WFORM", "0")
+    ops6 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+    assert ops6.lap_plan(p.vm).wform == 0
+    st = state.StateField("2C", o.state)
+    a = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops)
+    b = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops6)
+    assert rel_l2(a, b) <= 1e-14
+    assert rel_l2(a, o.hyper()) <= TOL
+    for f in (1, 4):
+        la = hyperdiff.laplacian_apply(o.state[:, f], p.vm, p.ops)
+        lb = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops6)
+        assert rel_l2(la, lb) <= 1e-14
+
+
 def test_all_five_fields_one_pass(pair):
     """F=5 tile kernel (config 1 applies L to all five fields)."""
     name, p, o = pair
