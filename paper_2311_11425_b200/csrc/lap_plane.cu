@@ -666,7 +666,16 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
     if (A.wform == 1) {
 #ifdef HV_PLANE_ABLATE
       const char* v = getenv("HV_PLANE_VARIANT");
-      if (v && atoi(v) == 40) return run_plane_v<n, TX, TY, F, 0, 4, 0, 1, 1>(A, Dt, st);
+      switch (v ? atoi(v) : 0) {
+        case 41: return run_plane_v<n, TX, TY, F, 0, 3, 1, 1, 1>(A, Dt, st);
+        case 42: return run_plane_v<n, TX, TY, F, 0, 3, 2, 1, 1>(A, Dt, st);
+        case 44: return run_plane_v<n, TX, TY, F, 0, 3, 4, 1, 1>(A, Dt, st);
+        case 48: return run_plane_v<n, TX, TY, F, 0, 3, 8, 1, 1>(A, Dt, st);
+        case 43: return run_plane_v<n, TX, TY, F, 0, 3, 3, 1, 1>(A, Dt, st);
+        case 47: return run_plane_v<n, TX, TY, F, 0, 3, 7, 1, 1>(A, Dt, st);
+        case 55: return run_plane_v<n, TX, TY, F, 0, 3, 15, 1, 1>(A, Dt, st);
+        default: break;
+      }
 #endif
       return run_plane_v<n, TX, TY, F, 0, 3, 0, 1, 1>(A, Dt, st);
     }

@@ -31,12 +31,21 @@ oa = (C.c_int32 * nv)(*range(nv))
 L = _lib.lib()
 st = _lib.stream_handle()
 ref = None
+# HV_PASS=2: the second pass of H_nu (y (ng, 4) in, (ng, 5) rows out with column 0 zeroed, scale -1)
+pass2 = os.environ.get("HV_PASS", "1") == "2"
+if pass2:
+    q = q[:, 1:5].contiguous()
+    qa = (C.c_int32 * nv)(*range(nv))
+    oa = (C.c_int32 * nv)(*cfg.variables)
 for v in sys.argv[1:]:
     os.environ["HV_PLANE_VARIANT"] = v
-    y = torch.zeros((ng, nv), dtype=torch.float64, device="cuda")
+    y = torch.zeros((ng, 5 if pass2 else nv), dtype=torch.float64, device="cuda")
 
     def one():
-        _lib.check(L.hv_lap_local(C.byref(plan), q.data_ptr(), 5, nv, qa, y.data_ptr(), nv, oa, 1.0, 0, 0, st))
+        if pass2:
+            _lib.check(L.hv_lap_local(C.byref(plan), q.data_ptr(), nv, nv, qa, y.data_ptr(), 5, oa, -1.0, 1, 0, st))
+        else:
+            _lib.check(L.hv_lap_local(C.byref(plan), q.data_ptr(), 5, nv, qa, y.data_ptr(), nv, oa, 1.0, 0, 0, st))
 
     for _ in range(3):
         one()
