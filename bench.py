@@ -108,9 +108,12 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- workloads
-def algorithmic_bytes_hnu(ng, nloc, F=4, alpha=2):
-    """per pass 2*F*ng*8 (read q / write) + 6*nloc*8 (G_nu J w) + ng*8 (Minv) + nloc*4 (map)."""
-    return alpha * (2 * F * ng * 8 + 6 * nloc * 8 + ng * 8 + nloc * 4)
+def algorithmic_bytes_hnu(ng, nloc, F=4, alpha=2, ncomp=6):
+    """per pass 2*F*ng*8 (read q / write) + 6*nloc*8 (G_nu J w) + ng*8 (Minv) + nloc*4 (map).
+
+    ncomp=3: the same count with the axis form of the metric the plane kernel reads instead of the
+    6 components (u = sqrt(w3 Jg) e_3) -- the bytes this kernel actually needs."""
+    return alpha * (2 * F * ng * 8 + ncomp * nloc * 8 + ng * 8 + nloc * 4)
 
 
 def algorithmic_bytes_c4(ng, nloc):
@@ -435,7 +438,7 @@ def run_ours(args, rank, world, local):
     alg = algorithmic_bytes_hnu(ng, nloc)
     achieved_op = alg / (ms * 1e-3) / 1e9
     # dominant kernel alone: the tile sweep of one pass (pass 1, q -> L q), CUDA events on its stream
-    kern_ms, kern_name, traffic = None, None, None
+    kern_ms, kern_name, traffic, wform = None, None, None, 0
     if world == 1 and getattr(ops, "_plans", None):
         import ctypes as C
 
@@ -463,12 +466,16 @@ def run_ours(args, rank, world, local):
             torch.cuda.synchronize()
             kern_ms = k0.elapsed_time(k1) / nk
             kern_name = "lap_plane_kernel" if plan.kernel == 1 else "lap_tile_kernel"
+            wform = int(plan.wform)
             prof = ROOT / "profiles" / "r01_dominant_kernel.json"
             if prof.exists():
                 traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
             del y
     alg_launch = alg / 2                       # one pass = one sweep launch
     achieved = alg_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else achieved_op
+    # what the kernel must move with its metric form (axis form: 3 of the 6 metric doubles)
+    own_launch = algorithmic_bytes_hnu(ng, nloc, ncomp=3 if wform == 1 else 6) / 2
+    own_achieved = own_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -494,7 +501,13 @@ def run_ours(args, rank, world, local):
                          "algorithmic_bytes_per_launch": alg_launch, "algorithmic_bytes_per_op": alg,
                          "op_achieved": achieved_op, "op_frac": achieved_op / peak,
                          "kernel_share_of_step": (2 * kern_ms / ms) if kern_ms else None,
+                         "metric_form": "axis (3 doubles per element node)" if wform == 1 else "6 components",
+                         "kernel_form_bytes_per_launch": own_launch,
+                         "kernel_form_achieved": own_achieved,
+                         "kernel_form_frac": (own_achieved / peak) if own_achieved else None,
                          "scope": "dominant kernel = tile sweep of one Laplacian pass (2 per H_nu op); "
+                                  "achieved/frac use SURVEY 8(d)'s bytes (6 metric doubles per element node); "
+                                  "kernel_form_* the bytes of the metric form the kernel reads; "
                                   "op_* = whole op incl. perimeter fix-ups; traffic = ncu dram bytes per "
                                   "launch (profiles/r01_dominant_kernel.json)"},
             "cpu_baseline": cpu,

@@ -112,10 +112,12 @@ int hv_viscous_metric(int N, int mode, const double* h_a, double b, const double
  * then G_nu = sum_m k_m e_m e_m^T (hyperdiff.py:80, k_m = nu_m vals_m = a_m / b) collapses to
  * k_h I + (k_v - k_h) e_3 e_3^T, e_3 the eigenvector of the largest eigenvalue of G (the same
  * Jacobi eigensolve as hv_viscous_metric), so W = w3 Jg G_nu = kh |u|^2 I + kd u u^T with
- * u = sqrt(w3 Jg[gid]) e_3: d_U (3, nelem*n^3) component-major, half the bytes of d_W.
- * Returns HV_ERR_DEGENERATE like hv_viscous_metric. */
+ * u = sqrt(w3 Jg[gid]) e_3: d_U (3, nelem*n^3) component-major, half the bytes of d_W (ncomp = 3).
+ * Isotropic form (c_1 == c_2 == c_3, so k_v == k_h and G_nu = k_h I): ncomp = 1 writes
+ * d_U[p] = scale * w3 Jg[gid] with scale = k_h, one double per node (no eigensolve).
+ * Returns HV_ERR_DEGENERATE like hv_viscous_metric (ncomp = 3). */
 int hv_viscous_axis(int N, const double* d_grad, int64_t nelem, const double* d_w3, const double* d_Jg,
-                    const int32_t* d_gid32, double* d_U, void* stream);
+                    const int32_t* d_gid32, int ncomp, double scale, double* d_U, void* stream);
 
 /* ------------------------------------------------------------- hot path
  * Laplacian plan: everything laplacian_apply (hyperdiff.py:84-94) reads. */
@@ -155,7 +157,8 @@ typedef struct hv_lap_plan {
   double* d_recv;              /* (2*face, n_z, 5) neighbour sums (NCCL receive buffer)        */
   /* form of d_Wt for the plane kernel (kernel == 1): 0 = the 6 components of W;
    * 1 = axis form (scaled mode with c_1 == c_2, hyperdiff.py:71-80: G_nu = k_h I + (k_v - k_h) e_3 e_3^T):
-   * u = sqrt(w3 Jg[gid]) e_3 (3 components, hv_viscous_axis) and W = kh |u|^2 I + kd u u^T */
+   * u = sqrt(w3 Jg[gid]) e_3 (3 components, hv_viscous_axis) and W = kh |u|^2 I + kd u u^T;
+   * 2 = isotropic form (c_1 == c_2 == c_3): s = kh w3 Jg[gid] (1 component), W = s I */
   int wform;
   double kh, kd;
 } hv_lap_plan;
@@ -182,7 +185,8 @@ int hv_lap_finish(const hv_lap_plan* plan, double* d_out, int64_t ldo, int nf, c
 /* Reorder the packed metric W (6, nelem*n^3) into the tile-sweep layout
  * (layout 0: line-tile kernel, [t][l][pair][k][e][i*n+j][2]; layout 1: plane kernel,
  * [t][l][pair][i][k][e][j][2]; layout 2: plane kernel, axis form, d_W = U (3, nelem*n^3) of
- * hv_viscous_axis -> [t][l][c][i][k][e][j]) using d_elem (ntiles, nlay, TX*TY),
+ * hv_viscous_axis -> [t][l][c][i][k][e][j]; layout 3: plane kernel, isotropic form, d_W = s (nelem*n^3)
+ * -> [t][l][i][k][e][j]) using d_elem (ntiles, nlay, TX*TY),
  * -1 for the absent elements of ragged tiles. */
 /* Minv in tile order: d_Mt[r*mts + c] = d_Minv[d_gt[r*gts + c]] for the rows r = (tile, layer)
  * (0 for absent nodes and padding). */

@@ -79,7 +79,8 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {
 // rows are split over two lanes (ih = 0, 1) that exchange the other half of every xi line
 // with warp shuffles; the eta lines of the line-owner role are split by zeta halves.
 // WF: form of the packed metric.  0: the 6 components of W as 3 pairs; 1: axis form (scaled
-// mode with c_1 == c_2): u = sqrt(w3 Jg) e_3 (3 doubles per node), W d = kh |u|^2 d + kd u (u . d).
+// mode with c_1 == c_2): u = sqrt(w3 Jg) e_3 (3 doubles per node), W d = kh |u|^2 d + kd u (u . d);
+// 2: isotropic form (c_1 == c_2 == c_3): s = kh w3 Jg (1 double per node), W d = s d.
 template <int n, int TX, int TY, int F, int WV, int H = 1, int WF = 0>
 struct PlaneCfg {
   static constexpr int N = n - 1;
@@ -106,7 +107,7 @@ struct PlaneCfg {
   static constexpr int SP = TUNED ? 588 : pad16(NE * n * n * n);
   static constexpr int SQ = QP * F;
   static constexpr int SE = SP * F;
-  static constexpr int WL = (WF ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
+  static constexpr int WL = (WF == 2 ? 1 : WF == 1 ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
   static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
   static constexpr int FI = UV * N;                      // output items per layer (k < N)
   static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
@@ -379,6 +380,26 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     }
     // ---- c: flux at the plane nodes, weak xi / zeta in registers
     if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)(l & 1));
+    if (run && WF == 2) {
+      // isotropic form: [i][k][e][j]; the F field lanes of a plane read the same s (broadcast)
+      const double* Sw = s_w + e * n + jp;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int i = I0 + r;
+        double d1[n], sv[n];
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          sv[k] = Sw[(i * n + k) * NE * n];
+          d1[k] = s_s[sidx(e, i, jp, k)];
+        }
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          p0[r][k] *= sv[k];
+          s_s[sidx(e, i, jp, k)] = sv[k] * d1[k];
+          p2[r][k] *= sv[k];
+        }
+      }
+    }
     if (run && WF == 1) {
       // axis form: [c][i][k][e][j]; the F field lanes of a plane read the same u (broadcast)
       const double* Uw = s_w + e * n + jp;
@@ -596,10 +617,11 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
 
 // Plane-layout packed metric, component pairs:
 // Wp[t][l][cp][i][k][e][j][h] = W[2cp+h][elem(t,l,e)*n^3 + (i*n + j)*n + k];
-// axis form (axis != 0, W = U (3, nloc)): Wp[t][l][c][i][k][e][j] = U[c][...].
+// axis form (axis == 1, W = U (3, nloc)): Wp[t][l][c][i][k][e][j] = U[c][...];
+// isotropic form (axis == 2, W = s (1, nloc)): Wp[t][l][i][k][e][j] = s[...].
 __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const int32_t* __restrict__ elem,
                                   const double* __restrict__ W, int64_t nloc, int axis, double* __restrict__ Wp) {
-  const int64_t per = (int64_t)(axis ? 3 : 6) * n * n * NE * n;
+  const int64_t per = (int64_t)(axis == 2 ? 1 : axis ? 3 : 6) * n * n * NE * n;
   const int64_t total = ntiles * nlay * per;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tl = id / per;
@@ -641,6 +663,10 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
       if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2, 1>(A, Dt, st);
       return run_plane_v<n, TX, TY, F, 0, 1, 0, 4, 1>(A, Dt, st);
     }
+    if (A.wform == 2) {
+      if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2, 2>(A, Dt, st);
+      return run_plane_v<n, TX, TY, F, 0, 1, 0, 4, 2>(A, Dt, st);
+    }
     if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2>(A, Dt, st);
     return run_plane_v<n, TX, TY, F, 0, 1, 0, 4>(A, Dt, st);
   } else {
@@ -679,6 +705,7 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
 #endif
       return run_plane_v<n, TX, TY, F, 0, 3, 0, 1, 1>(A, Dt, st);
     }
+    if (A.wform == 2) return run_plane_v<n, TX, TY, F, 0, 3, 0, 1, 2>(A, Dt, st);
     return run_plane_v<n, TX, TY, F, 0, 3>(A, Dt, st);
   }
 }

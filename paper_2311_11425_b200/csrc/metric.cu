@@ -399,10 +399,25 @@ extern "C" int hv_viscous_metric(int N, int mode, const double* h_a, double b, c
   return HV_OK;
 }
 
+// isotropic form: s[p] = scale * w3 * Jg[gid[p]]
+__global__ void iso_kernel(int nn, const double* __restrict__ w3, const double* __restrict__ Jg,
+                           const int32_t* __restrict__ gid, int64_t nloc, double scale, double* __restrict__ S) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p < nloc) S[p] = scale * (w3[p % nn] * Jg[gid[p]]);
+}
+
 extern "C" int hv_viscous_axis(int N, const double* d_grad, int64_t nelem, const double* d_w3, const double* d_Jg,
-                               const int32_t* d_gid32, double* d_U, void* stream) {
-  if (N < 1 || !d_grad || nelem <= 0 || !d_w3 || !d_Jg || !d_gid32 || !d_U)
+                               const int32_t* d_gid32, int ncomp, double scale, double* d_U, void* stream) {
+  if (N < 1 || !d_grad || nelem <= 0 || !d_w3 || !d_Jg || !d_gid32 || !d_U || (ncomp != 1 && ncomp != 3))
     HV_FAIL(HV_ERR_INVALID, "hv_viscous_axis: bad args");
+  if (ncomp == 1) {
+    const int n = N + 1, nn = n * n * n;
+    const int64_t nloc = nelem * nn;
+    iso_kernel<<<(unsigned)((nloc + 255) / 256), 256, 0, (cudaStream_t)stream>>>(nn, d_w3, d_Jg, d_gid32, nloc, scale,
+                                                                               d_U);
+    HV_LAUNCH_CHECK();
+    return HV_OK;
+  }
   ViscParams P{};
   P.mode = 1;   // the eigenvectors only; nu unused
   cudaStream_t st = (cudaStream_t)stream;

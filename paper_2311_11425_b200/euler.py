@@ -112,22 +112,28 @@ class EulerOps:
                 # HV_KERNEL=line forces the line-tile kernel (cross-checks)
                 n7p = dev.N == 7 and os.environ.get("HV_N7_KERNEL", "") != "line"
                 layout = 1 if (os.environ.get("HV_KERNEL", "") != "line" and (dev.N <= 4 or n7p)) else 0
-                # axis form of W (3 doubles per node instead of 6) where G_nu = kh I + kd e3 e3^T, for
-                # N <= 4 (the N = 7 split-plane kernel spills with it: c4 6.91 -> 7.04 ms);
-                # HV_WFORM=0 forces the 6-component form (cross-checks), HV_WFORM=1 also at N = 7
+                # compact forms of W for the plane kernel: isotropic (G_nu = kh I: 1 double per node)
+                # or axis (G_nu = kh I + kd e3 e3^T: 3 doubles; N <= 4 -- the N = 7 split-plane kernel
+                # spills with it, c4 6.91 -> 7.04 ms); HV_WFORM=0 forces the 6 components (cross-checks),
+                # HV_WFORM=1 the axis form also at N = 7 / for isotropic viscosity
                 wf = os.environ.get("HV_WFORM", "")
-                ax = viscous.axis_form() if layout == 1 and wf != "0" and (dev.N <= 4 or wf == "1") else None
-                ncomp = 3 if ax is not None else 6
+                ax = viscous.axis_form() if layout == 1 and wf != "0" else None
+                wform = 0
+                if ax is not None and ax[1] == 0.0 and wf != "1":
+                    wform = 2
+                elif ax is not None and (dev.N <= 4 or wf == "1"):
+                    wform = 1
+                ncomp = {0: 6, 1: 3, 2: 1}[wform]
                 Wt = torch.empty(tp.ntiles * tp.nlay * ncomp * n * tp.NE * n * n, dtype=torch.float64,
                                  device="cuda")
-                src = viscous.packed_axis(self.metrics.d_Jg) if ax is not None else W
+                src = viscous.packed_axis(self.metrics.d_Jg, ncomp, ax[0]) if wform else W
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
                                                           d["elem"].data_ptr(), src.data_ptr(), dev.nloc,
-                                                          2 if ax is not None else layout, Wt.data_ptr(),
+                                                          wform + 1 if wform else layout, Wt.data_ptr(),
                                                           _lib.stream_handle()))
                 p.kernel = layout
-                if ax is not None:
-                    p.wform, p.kh, p.kd = 1, ax[0], ax[1]
+                if wform:
+                    p.wform, p.kh, p.kd = wform, ax[0], ax[1]
                 del src
                 p.TX, p.TY, p.nlay, p.n_z = tp.TX, tp.TY, tp.nlay, tp.n_z
                 p.ntiles, p.nslot = tp.ntiles, tp.nslot

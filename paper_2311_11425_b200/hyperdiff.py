@@ -119,15 +119,16 @@ class ViscousMetric:
         kh = float(a[0]) / float(b)
         return kh, float(a[2]) / float(b) - kh
 
-    def packed_axis(self, d_Jg):
-        """u = sqrt(w3 Jg[gid]) e_3 (3, nloc) for the axis form of W (hv_viscous_axis); not cached
-        (the plan keeps only its tile-ordered copy)."""
+    def packed_axis(self, d_Jg, ncomp=3, scale=1.0):
+        """Axis form u = sqrt(w3 Jg[gid]) e_3 (3, nloc), or (ncomp=1, isotropic case) s = scale w3 Jg[gid]
+        (1, nloc), for the plane kernel (hv_viscous_axis); not cached (the plan keeps only its
+        tile-ordered copy)."""
         torch = torch_mod()
         dev = self.mesh.device()
-        U = torch.empty((3, dev.nloc), dtype=torch.float64, device="cuda")
+        U = torch.empty((ncomp, dev.nloc), dtype=torch.float64, device="cuda")
         _lib.check(_lib.lib().hv_viscous_axis(dev.N, self.mets.d_grad.data_ptr(), dev.nelem, dev.w3.data_ptr(),
-                                              d_Jg.data_ptr(), dev.gid32.data_ptr(), U.data_ptr(),
-                                              _lib.stream_handle()))
+                                              d_Jg.data_ptr(), dev.gid32.data_ptr(), ncomp, float(scale),
+                                              U.data_ptr(), _lib.stream_handle()))
         return U
 
     def packed(self, d_Jg):

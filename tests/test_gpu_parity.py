@@ -174,9 +174,9 @@ def test_tile_path_used_and_matches_element_path(pair):
 
 
 def test_axis_form_matches_six_components(pair, monkeypatch):
-    """Plane kernel with the axis form of W (u = sqrt(w3 Jg) e_3, scaled mode with c_1 == c_2) equals
-    the 6-component form (HV_WFORM=0) to rounding, and the plan picks the axis form exactly when
-    G_nu = kh I + kd e_3 e_3^T."""
+    """Plane kernel with the compact forms of W -- axis (u = sqrt(w3 Jg) e_3, scaled mode with
+    c_1 == c_2) and isotropic (s = kh w3 Jg, c_1 == c_2 == c_3) -- equals the 6-component form
+    (HV_WFORM=0) to rounding, and the plan picks them exactly when G_nu has that structure."""
     name, p, o = pair
     from paper_2311_11425_b200 import euler, hyperdiff, state
 
@@ -184,8 +184,11 @@ def test_axis_form_matches_six_components(pair, monkeypatch):
     ax = p.vm.axis_form()
     hd = p.cfg
     assert (ax is not None) == (hd.mode == "scaled" and hd.c[0] == hd.c[1])
-    assert plan.wform == (1 if (ax is not None and plan.kernel == 1 and plan.N <= 4) else 0)
-    if plan.wform != 1:
+    if ax is not None and plan.kernel == 1 and ax[1] == 0.0:
+        assert plan.wform == 2                       # isotropic: c_1 == c_2 == c_3
+    else:
+        assert plan.wform == (1 if (ax is not None and plan.kernel == 1 and plan.N <= 4) else 0)
+    if plan.wform == 0:
         pytest.skip("6-component form for this case")
     monkeypatch.setenv("HV_WFORM", "0")
     ops6 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
