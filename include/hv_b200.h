@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define HV_ABI_VERSION 4
+#define HV_ABI_VERSION 5
 
 #define HV_OK 0
 #define HV_ERR_INVALID 1        /* ValueError: bad argument / config                  */
@@ -161,6 +161,7 @@ typedef struct hv_lap_plan {
    * 2 = isotropic form (c_1 == c_2 == c_3): s = kh w3 Jg[gid] (1 component), W = s I */
   int wform;
   double kh, kd;
+  const double* d_Ms;          /* (nslot, n_z) Minv of the shared column nodes in slot order, or NULL */
 } hv_lap_plan;
 
 /* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the

@@ -68,6 +68,7 @@ class LapPlan(C.Structure):
         ("wform", C.c_int),
         ("kh", C.c_double),
         ("kd", C.c_double),
+        ("d_Ms", _P),
     ]
 
 
@@ -115,7 +116,7 @@ _SIGS = {
 }
 
 _lib = None
-ABI_VERSION = 4          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
+ABI_VERSION = 5          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
 
 
 def lib():

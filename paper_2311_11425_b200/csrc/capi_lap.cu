@@ -36,7 +36,7 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.zero_mask = zero_mask; A.accumulate = accumulate; A.scale = scale; A.out = out; A.part = P->d_part;
   A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
-  A.wform = P->wform; A.kh = P->kh; A.kd = P->kd;
+  A.wform = P->wform; A.kh = P->kh; A.kd = P->kd; A.Ms = P->d_Ms;
   return A;
 }
 

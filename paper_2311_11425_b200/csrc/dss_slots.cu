@@ -85,7 +85,7 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   const int c = A.slot_col[s];
   const int g = A.col_gid[(int64_t)c * A.n_z + z];
   double* o = A.out + (int64_t)g * A.ldo;
-  const double mi = __ldg(A.Minv + g);
+  const double mi = A.Ms ? __ldg(A.Ms + id) : __ldg(A.Minv + g);
   double prev[F];
   if (A.accumulate) {
 #pragma unroll

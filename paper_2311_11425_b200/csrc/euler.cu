@@ -708,7 +708,7 @@ extern "C" int hv_euler_rhs_tiles(const hv_lap_plan* P, const int32_t* d_elem, c
   A.ntiles = P->ntiles; A.nslot = P->nslot; A.tile0 = 0; A.tile1 = P->ntiles;
   A.gt = P->d_gt; A.code = P->d_code; A.tmeta = P->d_tmeta;
   A.slot_col = P->d_slot_col; A.slot_row0 = P->d_slot_row0; A.slot_nc = P->d_slot_nc; A.col_gid = P->d_col_gid;
-  A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.q = d_q; A.ldq = ldq; A.ldo = ldo;
+  A.Mt = P->d_Mt; A.Minv = P->d_Minv; A.Ms = P->d_Ms; A.q = d_q; A.ldq = ldq; A.ldo = ldo;
   for (int f = 0; f < 5; ++f) A.of.f[f] = f;
   A.zero_mask = 0; A.accumulate = accumulate; A.scale = 1.0; A.out = d_out; A.part = P->d_part;
   int rc;

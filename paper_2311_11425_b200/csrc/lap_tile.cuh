@@ -37,6 +37,7 @@ struct TileArgs {
   const double* recv;       // (2 * face, n_z, 5) neighbours' sums
   int wform;                // Wt form (plane kernel): 0 = 6 components, 1 = axis form u (W = kh|u|^2 I + kd u u^T)
   double kh, kd;
+  const double* Ms;         // (nslot, n_z) Minv in slot order (coalesced in slot_fixup), or nullptr
 };
 
 bool tile_supported(int N, int TX, int TY, int F);

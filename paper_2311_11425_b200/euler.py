@@ -80,6 +80,13 @@ class EulerOps:
                 self._h["tiles"] = (tp, d)
         return self._h["tiles"]
 
+    def _slot_minv(self, d):
+        """Minv of the shared column nodes in slot order, (nslot, n_z): the fix-up reads it coalesced."""
+        if d["slot_col"].numel() == 0:
+            return None
+        cols = d["col_gid"][d["slot_col"].long()].long()
+        return self.mass.d_Minv[cols].contiguous()
+
     def lap_plan(self, viscous):
         """hv_lap_plan for this (viscous metric, operator set) pair."""
         key = id(viscous)
@@ -145,7 +152,9 @@ class EulerOps:
                                                         self.mass.d_Minv.data_ptr(), Mt.data_ptr(),
                                                         _lib.stream_handle()))
                 p.d_Wt, p.d_Mt, p.d_part = Wt.data_ptr(), Mt.data_ptr(), d["part"].data_ptr()
-                keep += [Wt, Mt]
+                Ms = self._slot_minv(d)
+                p.d_Ms = _lib.ptr(Ms)
+                keep += [Wt, Mt, Ms]
                 if self.ext_cols:
                     face = self.ext_face
                     p.d_slot_ext, p.d_ext_slots = d["slot_ext"].data_ptr(), d["ext_slots"].data_ptr()
@@ -215,8 +224,10 @@ class EulerOps:
                                                             self.mass.d_Minv.data_ptr(), Mt.data_ptr(),
                                                             _lib.stream_handle()))
                     p.d_Mt, p.d_part = Mt.data_ptr(), d["part"].data_ptr()
+                    Ms = self._slot_minv(d)
+                    p.d_Ms = _lib.ptr(Ms)
                     elem = d["elem"].reshape(tp.ntiles, tp.nlay).contiguous()
-                    self._h["euler_tiles"] = (p, [Mt, elem], elem)
+                    self._h["euler_tiles"] = (p, [Mt, elem, Ms], elem)
         return self._h["euler_tiles"]
 
     def _rhs(self, state, dirs, coriolis, out=None, accumulate=False):
