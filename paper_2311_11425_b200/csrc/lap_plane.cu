@@ -129,7 +129,10 @@ struct PlaneCfg {
 // layer ahead, coalesced from the tile-ordered map), Minv is read coalesced at step e.
 // AB: ablation bit mask for development timing only (0 in production): 1 = no node-owner
 // step (f), 2 = no q gather, 4 = no metric TMA, 8 = no plane arithmetic (steps b-e)
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
+// OM: output rows, fixed at compile time for the hot passes (smaller code): 0 = any (runtime
+// checks below), 1 = (ng, 4) rows of fields 0..3 written, 2 = (ng, 5) rows of fields 1..4 written
+// with column 0 zeroed (H_nu's second pass)
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0>
 __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
   constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
@@ -211,6 +214,22 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     if (cd < 0) {
       double* o = A.out + (int64_t)g * A.ldo;
       const double m = A.scale * mi;
+      if constexpr (F == 4 && OM == 1) {
+        st_v2(o, m * val.v[0], m * val.v[1]);
+        st_v2(o + 2, m * val.v[2], m * val.v[3]);
+        return;
+      } else if constexpr (F == 4 && OM == 2) {
+        if ((g & 1) == 0) {
+          st_v2(o, 0.0, m * val.v[0]);
+          st_v2(o + 2, m * val.v[1], m * val.v[2]);
+          o[4] = m * val.v[3];
+        } else {
+          o[0] = 0.0;
+          st_v2(o + 1, m * val.v[0], m * val.v[1]);
+          st_v2(o + 3, m * val.v[2], m * val.v[3]);
+        }
+        return;
+      }
       if constexpr (F == 4) {
         if (vec4) {
           st_v2(o, m * val.v[0], m * val.v[1]);
@@ -638,15 +657,37 @@ __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const
   }
 }
 
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
-int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
+// compile-time output mode of this pass (OM of lap_plane_kernel)
+inline int output_mode(const TileArgs& A, int F) {
+  if (F != 4 || A.accumulate) return 0;
+  const bool f0 = A.of.f[0] == 0 && A.of.f[1] == 1 && A.of.f[2] == 2 && A.of.f[3] == 3;
+  const bool f1 = A.of.f[0] == 1 && A.of.f[1] == 2 && A.of.f[2] == 3 && A.of.f[3] == 4;
+  if (A.ldo == 4 && !A.zero_mask && f0) return 1;
+  if (A.ldo == 5 && f1) return 2;
+  return 0;
+}
+
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0>
+int run_plane_om(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
-  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF>;
+  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF, OM>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   if (A.tile1 <= A.tile0) return HV_OK;
   kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   return HV_OK;
+}
+
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
+int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
+  // N = 7 hot passes (c4: 6.17 -> 6.02 ms); at N = 4 the specialised code measured slower
+  // (c5 sweep 1.76 -> 1.90 ms, scheduling), so N <= 4 keeps the runtime checks
+  if constexpr (F == 4 && n == 8 && AB == 0) {
+    const int om = output_mode(A, F);
+    if (om == 1) return run_plane_om<n, TX, TY, F, WV, MB, AB, H, WF, 1>(A, Dt, st);
+    if (om == 2) return run_plane_om<n, TX, TY, F, WV, MB, AB, H, WF, 2>(A, Dt, st);
+  }
+  return run_plane_om<n, TX, TY, F, WV, MB, AB, H, WF, 0>(A, Dt, st);
 }
 
 // Production: W by TMA into shared memory, 3 CTAs/SM (N <= 4); split planes H = 4 at N = 7
