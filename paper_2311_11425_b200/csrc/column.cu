@@ -19,6 +19,8 @@
 //                     (linalg.py:166-194), one warp per system.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <cmath>
 
 #include "hv_common.h"
@@ -380,6 +382,167 @@ __global__ void band_lu_kernel(BandDims B, int64_t nb, double* __restrict__ data
   if (lane == 0) info[s] = 0;
 }
 
+// Block-per-system band LU (default): the same sliding window and elementary operations as
+// band_lu_kernel (bitwise the same factors), with NT threads per system instead of one warp, so
+// the per-column critical path (pivot, swap, multipliers, rank-1 update) is spread out:
+// thread t updates window column j + 1 + (t % CW) for the rows i = t / CW, t / CW + G, ...
+// (CW = kl + ku update columns, G = NT / CW row groups); every warp finds the pivot redundantly
+// (read-only).  Two CTA barriers per column: (1) the row swap of columns j+1..jmax and the
+// multipliers of column j (computed from the pre-swap column into a side buffer, so the slower
+// warps' pivot search is never disturbed) run together; (2) the rank-1 update, while the
+// multiplier threads write column j's final values (pivot, multipliers) into the window.  RS is
+// even here: the column-walking update and swap (stride RS - 1, odd) hit distinct banks.
+template <int PFN>
+__global__ void __launch_bounds__(128) band_lu_block_kernel(BandDims B, int64_t nb, double* __restrict__ data,
+                                                           int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
+  extern __shared__ double win[];
+  double* mb = win + (size_t)B.R * B.RS;   // [kl] multipliers of the current column
+  const int t = threadIdx.x, NT = blockDim.x, lane = t % 32;
+  const int64_t s = blockIdx.x;
+  if (s >= nb) return;
+  double* g = data + s * (int64_t)B.R * B.M;
+  const int d = B.kl + B.ku;
+  const int CW = max(1, d), G = max(1, NT / CW);
+  const int tc = t % CW, tr = t / CW;
+  // window slot of column c0 + c for c < WC, given s0 = slot(c0) (no integer division in the loops)
+  auto wrap = [&](int q) { return q >= B.WC ? q - B.WC : q; };
+  auto load_cols = [&](int c0, int c1) {   // once, c0 = 0: slots = columns
+    const int w = c1 - c0, tot = B.R * w;
+    for (int e = t; e < tot; e += NT) {
+      const int r = e / w, c = e - r * w;
+      win[r * B.RS + c0 + c] = g[(int64_t)r * B.M + c0 + c];
+    }
+  };
+  auto store_cols = [&](int c0, int c1) {   // w = c1 - c0 <= WC columns
+    const int w = c1 - c0, tot = B.R * w;
+    const int s0 = c0 % B.WC;
+    if (w == CH) {
+      for (int e = t; e < tot; e += NT) {
+        const int r = e / CH, c = e % CH;
+        g[(int64_t)r * B.M + c0 + c] = win[r * B.RS + wrap(s0 + c)];
+      }
+    } else {
+      for (int e = t; e < tot; e += NT) {
+        const int r = e / w, c = e - r * w;
+        g[(int64_t)r * B.M + c0 + c] = win[r * B.RS + wrap(s0 + c)];
+      }
+    }
+  };
+  // the next chunk is prefetched into registers (R * CH <= NT * PFN, checked by the launcher)
+  double pf[PFN];
+  int pf_c0 = 0, pf_w = 0;
+  auto prefetch = [&](int c0, int c1) {
+    pf_c0 = c0;
+    pf_w = c1 - c0;
+    const int tot = B.R * pf_w;
+#pragma unroll
+    for (int u = 0; u < PFN; ++u) {
+      const int e = u * NT + t;
+      const int r = (pf_w == CH) ? e / CH : e / pf_w, c = (pf_w == CH) ? e % CH : e % pf_w;
+      pf[u] = (e < tot) ? g[(int64_t)r * B.M + c0 + c] : 0.0;
+    }
+  };
+  auto commit = [&]() {
+    const int tot = B.R * pf_w;
+    const int s0 = pf_c0 % B.WC;
+#pragma unroll
+    for (int u = 0; u < PFN; ++u) {
+      const int e = u * NT + t;
+      const int r = (pf_w == CH) ? e / CH : e / pf_w, c = (pf_w == CH) ? e % CH : e % pf_w;
+      if (e < tot) win[r * B.RS + wrap(s0 + c)] = pf[u];
+    }
+  };
+  int loaded = min(B.M, B.WC);
+  load_cols(0, loaded);
+  if (loaded < B.M) prefetch(loaded, min(B.M, loaded + CH));
+  int stored = 0;
+  int sj = 0;                    // window slot of column j (j % WC, kept incrementally)
+  __syncthreads();
+  for (int j = 0; j < B.M; ++j, sj = wrap(sj + 1)) {
+    const int jmax = min(B.M - 1, j + B.ku + B.kl);
+    if (jmax >= loaded) {   // retire finished columns [stored, j), bring in the prefetched chunk
+      store_cols(stored, j);
+      stored = j;
+      __syncthreads();
+      commit();
+      loaded = pf_c0 + pf_w;
+      if (loaded < B.M) prefetch(loaded, min(B.M, loaded + CH));
+      __syncthreads();
+    }
+    const int lm = min(B.kl, B.M - 1 - j);
+    auto sl = [&](int col) { return wrap(sj + (col - j)); };
+    // pivot: first index of the largest |candidate| (np.argmax), found by every warp
+    double best = -1.0;
+    int bi = 0;
+    for (int r = lane; r <= lm; r += 32) {
+      const double v = fabs(win[(d + r) * B.RS + sj]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int prel = bi;
+    const double piv = win[(d + prel) * B.RS + sj];
+    if (piv == 0.0) {
+      if (t == 0) info[s] = j + 1;
+      __syncthreads();
+      store_cols(stored, loaded);
+      return;
+    }
+    if (t == 0) ipiv[s * B.M + j] = j + prel;
+    const int ncol = jmax - j;   // update columns j + 1 .. jmax
+    // phase 1: row swap in columns j+1..jmax (threads from the top), multipliers of column j
+    // from its pre-swap values (threads from the bottom) -- disjoint data
+    double mcol = 0.0;           // this thread's final column-j value (written in phase 2)
+    if (prel != 0)
+      for (int c = 1 + t; c <= ncol; c += NT) {
+        const int col = j + c, off = d + j - col;
+        double* x = win + off * B.RS + sl(col);
+        double* y = x + prel * B.RS;
+        const double tmp = *x;
+        *x = *y;
+        *y = tmp;
+      }
+    const int tm = NT - 1 - t;   // multiplier / column-j thread: tm < lm (row j+1+tm), tm == lm (pivot row)
+    if (tm < lm) {
+      // after the swap, row j + 1 + tm holds the old row j value if j + 1 + tm == j + prel
+      const double v = (tm + 1 == prel) ? win[d * B.RS + sj] : win[(d + 1 + tm) * B.RS + sj];
+      mcol = v / piv;
+      mb[tm] = mcol;
+    }
+    __syncthreads();
+    // phase 2: rank-1 update of columns j+1..jmax; column j gets its pivot and multipliers
+    if (tm < lm) win[(d + 1 + tm) * B.RS + sj] = mcol;
+    else if (tm == lm) win[d * B.RS + sj] = piv;
+    if (tr < G && tc < ncol) {
+      const int col = j + 1 + tc;
+      const int so = (d + j - col) * B.RS + sl(col);
+      const double u = win[so];
+      // rows in batches of four: loads of a batch before its stores
+      for (int i0 = tr; i0 < lm; i0 += 4 * G) {
+        double a[4], m[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = i0 + k * G;
+          a[k] = (i < lm) ? win[so + (1 + i) * B.RS] : 0.0;
+          m[k] = (i < lm) ? mb[i] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = i0 + k * G;
+          if (i < lm) win[so + (1 + i) * B.RS] = dsub_mul(a[k], m[k], u);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  store_cols(stored, B.M);
+  if (t == 0) info[s] = 0;
+}
+
 // rows [r0, r0 + nr) x columns [c0, c0 + w) of a band into ch[col][RS] (column-major in shared
 // memory: the lanes of the substitution steps walk rows); eight global loads in flight
 __device__ __forceinline__ void load_chunk(double* ch, int RS, const double* g, int r0, int nr, int c0, int w, int M,
@@ -501,6 +664,22 @@ extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int
                                  void* stream) {
   if (!d_data || !d_ipiv || !d_info || nb <= 0 || kl < 0 || ku < 0 || M <= 0)
     HV_FAIL(HV_ERR_INVALID, "hv_band_lu_factor: bad arguments");
+  const char* lv = getenv("HV_BAND_LU");
+  if (!(lv && atoi(lv) == 1)) {   // block per system (default); HV_BAND_LU=1: the warp-per-system kernel
+    BandDims B = band_dims(kl, ku, M);
+    B.RS = B.WC + (B.WC & 1);      // even: stride RS - 1 of the column walks is odd
+    const int d = kl + ku, CW = d > 0 ? d : 1;
+    const int G = CW >= 128 ? 1 : 128 / CW;
+    const int NT = ((CW * G + 31) / 32) * 32;
+    const size_t smem = sizeof(double) * ((size_t)B.R * B.RS + kl + 1);
+    if (smem > 227 * 1024 || B.R * CH > NT * 8 || NT > 128 || NT < kl + 1)
+      HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
+    auto kern = (B.R * CH <= NT * 4) ? band_lu_block_kernel<4> : band_lu_block_kernel<8>;
+    HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)nb, NT, smem, (cudaStream_t)stream>>>(B, nb, d_data, d_ipiv, d_info);
+    HV_LAUNCH_CHECK();
+    return HV_OK;
+  }
   const BandDims B = band_dims(kl, ku, M);
   // one warp (system) per block: the SM packs as many ~35 KB windows as fit (6 at N = 4)
   const int wpb = 1;
