@@ -402,8 +402,27 @@ __global__ void __launch_bounds__(128) band_lu_block_kernel(BandDims B, int64_t 
   if (s >= nb) return;
   double* g = data + s * (int64_t)B.R * B.M;
   const int d = B.kl + B.ku;
-  const int CW = max(1, d), G = max(1, NT / CW);
-  const int tc = t % CW, tr = t / CW;
+  // phase-2 mapping: column j+1 by warp 0 (one row per lane; look-ahead pivot search right after),
+  // columns j+2..jmax by (column, row group) threads
+  const int CB = max(1, d - 1), G = max(1, NT / CB);
+  const int tc = t % CB, tr = t / CB;
+  int* s_prel = reinterpret_cast<int*>(mb + B.kl + 1);   // pivot row (relative) of the next column
+  // first index of the largest |candidate| of column `col` (window slot sc), rows 0..lm; warp 0
+  auto find_pivot = [&](int sc, int lm_) {
+    double best = -1.0;
+    int bi = 0;
+    for (int r = lane; r <= lm_; r += 32) {
+      const double v = fabs(win[(d + r) * B.RS + sc]);
+      if (v > best) { best = v; bi = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) *s_prel = bi;
+  };
   // window slot of column c0 + c for c < WC, given s0 = slot(c0) (no integer division in the loops)
   auto wrap = [&](int q) { return q >= B.WC ? q - B.WC : q; };
   auto load_cols = [&](int c0, int c1) {   // once, c0 = 0: slots = columns
@@ -458,6 +477,8 @@ __global__ void __launch_bounds__(128) band_lu_block_kernel(BandDims B, int64_t 
   int stored = 0;
   int sj = 0;                    // window slot of column j (j % WC, kept incrementally)
   __syncthreads();
+  if (t < 32) find_pivot(0, min(B.kl, B.M - 1));
+  __syncthreads();
   for (int j = 0; j < B.M; ++j, sj = wrap(sj + 1)) {
     const int jmax = min(B.M - 1, j + B.ku + B.kl);
     if (jmax >= loaded) {   // retire finished columns [stored, j), bring in the prefetched chunk
@@ -471,20 +492,7 @@ __global__ void __launch_bounds__(128) band_lu_block_kernel(BandDims B, int64_t 
     }
     const int lm = min(B.kl, B.M - 1 - j);
     auto sl = [&](int col) { return wrap(sj + (col - j)); };
-    // pivot: first index of the largest |candidate| (np.argmax), found by every warp
-    double best = -1.0;
-    int bi = 0;
-    for (int r = lane; r <= lm; r += 32) {
-      const double v = fabs(win[(d + r) * B.RS + sj]);
-      if (v > best) { best = v; bi = r; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const int prel = bi;
+    const int prel = *s_prel;    // found during the previous column's update (look-ahead)
     const double piv = win[(d + prel) * B.RS + sj];
     if (piv == 0.0) {
       if (t == 0) info[s] = j + 1;
@@ -517,8 +525,18 @@ __global__ void __launch_bounds__(128) band_lu_block_kernel(BandDims B, int64_t 
     // phase 2: rank-1 update of columns j+1..jmax; column j gets its pivot and multipliers
     if (tm < lm) win[(d + 1 + tm) * B.RS + sj] = mcol;
     else if (tm == lm) win[d * B.RS + sj] = piv;
-    if (tr < G && tc < ncol) {
-      const int col = j + 1 + tc;
+    if (t < 32 && ncol >= 1) {   // column j+1 first, then its pivot (the next step's critical path)
+      const int so = (d - 1) * B.RS + sl(j + 1);
+      const double u = win[so];
+      for (int i = lane; i < lm; i += 32) {
+        double* ap = win + so + (1 + i) * B.RS;
+        *ap = dsub_mul(*ap, mb[i], u);
+      }
+      __syncwarp();
+      find_pivot(sl(j + 1), min(B.kl, B.M - 2 - j));
+    }
+    if (tr < G && 1 + tc < ncol) {
+      const int col = j + 2 + tc;
       const int so = (d + j - col) * B.RS + sl(col);
       const double u = win[so];
       // rows in batches of four: loads of a batch before its stores
@@ -668,10 +686,10 @@ extern "C" int hv_band_lu_factor(double* d_data, int64_t nb, int kl, int ku, int
   if (!(lv && atoi(lv) == 1)) {   // block per system (default); HV_BAND_LU=1: the warp-per-system kernel
     BandDims B = band_dims(kl, ku, M);
     B.RS = B.WC + (B.WC & 1);      // even: stride RS - 1 of the column walks is odd
-    const int d = kl + ku, CW = d > 0 ? d : 1;
-    const int G = CW >= 128 ? 1 : 128 / CW;
-    const int NT = ((CW * G + 31) / 32) * 32;
-    const size_t smem = sizeof(double) * ((size_t)B.R * B.RS + kl + 1);
+    const int d = kl + ku, CB = d > 1 ? d - 1 : 1;
+    const int G = CB >= 128 ? 1 : 128 / CB;
+    const int NT = ((CB * G + 31) / 32) * 32;
+    const size_t smem = sizeof(double) * ((size_t)B.R * B.RS + kl + 2);
     if (smem > 227 * 1024 || B.R * CH > NT * 8 || NT > 128 || NT < kl + 1)
       HV_FAIL(HV_ERR_UNSUPPORTED, "hv_band_lu_factor: band too wide (kl=%d ku=%d)", kl, ku);
     auto kern = (B.R * CH <= NT * 4) ? band_lu_block_kernel<4> : band_lu_block_kernel<8>;
