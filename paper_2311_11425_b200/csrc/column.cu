@@ -53,21 +53,17 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
   constexpr int NV = 5;
   constexpr int KL = NV * n - 1, KU = KL, D0 = KL + KU, R = 2 * KL + KU + 1;
   __shared__ LayerNodes<n> L;
+  // band columns of the current layer, [R][TW]: the layer's block entries accumulate here (no global
+  // read-modify-write); after the layer its first TW - NV columns are final and leave with coalesced
+  // row segments, the last NV (the node shared with the next layer) move to the front
+  constexpr int TW = NV * n;
+  __shared__ double T[R][TW];
   const int64_t c = blockIdx.x;
   const int t = threadIdx.x;
   const int64_t M = (int64_t)NV * n_z;
   double* bc = band + c * R * M;
   const double* w = Wz.D[0];
-  // band = I (zeros elsewhere)
-  for (int r = 0; r < R; ++r) {
-    const double v = (r == D0) ? 1.0 : 0.0;
-    double* br = bc + (int64_t)r * M;
-    if ((M & 1) == 0 && ((reinterpret_cast<uintptr_t>(br) & 15) == 0)) {
-      for (int64_t e = t; e < M / 2; e += blockDim.x) reinterpret_cast<double2*>(br)[e] = make_double2(v, v);
-    } else {
-      for (int64_t e = t; e < M; e += blockDim.x) br[e] = v;
-    }
-  }
+  for (int e = t; e < R * TW; e += blockDim.x) T[e / TW][e % TW] = (e / TW == D0) ? 1.0 : 0.0;   // band = I
   __syncthreads();
   const int32_t* cg = col_gid + c * (int64_t)n_z;
   const double* qc = qcol + c * (int64_t)n_z * NV;
@@ -204,9 +200,28 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
         }
       }
       const double contrib = (-K.lam * B) / L.mass[i];
-      const int64_t row = (int64_t)NV * (l * N + i) + vi, col = (int64_t)NV * (l * N + a) + va;
-      double* p = bc + (D0 + row - col) * M + col;
-      *p = *p + contrib;
+      const int row = NV * i + vi, col = NV * a + va;   // layer-local: band row D0 + row - col
+      T[D0 + row - col][col] = T[D0 + row - col][col] + contrib;
+    }
+    __syncthreads();
+    // columns NV*l*N .. + wout are final: all R band rows, row segments of wout doubles
+    const int wout = (l == nlay - 1) ? TW : TW - NV;
+    const int64_t c0 = (int64_t)NV * l * N;
+    for (int e = t; e < R * wout; e += blockDim.x) {
+      const int r = e / wout, k = e - r * wout;
+      bc[(int64_t)r * M + c0 + k] = T[r][k];
+    }
+    __syncthreads();
+    if (l < nlay - 1) {
+      for (int e = t; e < R * NV; e += blockDim.x) {   // shared node's columns to the front (TW >= 2 NV)
+        const int r = e / NV, k = e % NV;
+        T[r][k] = T[r][TW - NV + k];
+      }
+      __syncthreads();
+      for (int e = t; e < R * (TW - NV); e += blockDim.x) {   // the next layer's new columns: identity
+        const int r = e / (TW - NV), k = NV + e % (TW - NV);
+        T[r][k] = (r == D0) ? 1.0 : 0.0;
+      }
     }
     __syncthreads();
   }
