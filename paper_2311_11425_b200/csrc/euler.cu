@@ -103,7 +103,8 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
                                                int64_t e, int t, const int32_t* __restrict__ gid,
                                                const double* __restrict__ w3, const double* __restrict__ Mt,
                                                const double* __restrict__ q, int64_t ldq, double* sm,
-                                               double (&acc)[5], int& g_out, int layer, int nlay) {
+                                               double (&acc)[5], int& g_out, int layer, int nlay,
+                                               const double* __restrict__ sD) {
   constexpr int nn = n * n * n;
   // 2C / 3C: per direction m: [0] w3*F_rho, [1] w3*F_thermo (weak), [2..4] momentum fluxes (strong)
   // 2NC: [0..2] w3*F_rho per m (weak), [3..7] u, v, w, theta, P (strong derivatives)
@@ -171,7 +172,8 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
         for (int a = 0; a < n; ++a) {
           const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
           const int ii = (m == 0) ? i : (m == 1) ? j : k;
-          const double dw = Dt.D[a][ii], ds = Dt.D[ii][a];
+          // D from shared memory: the lanes of a warp index it with different ii (LDC would serialise)
+          const double dw = sD[a * n + ii], ds = sD[ii * n + a];
           wk0 += dw * s[(m * 5 + 0) * nn + o];
           wk4 += dw * s[(m * 5 + 1) * nn + o];
 #pragma unroll
@@ -211,9 +213,10 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
         for (int a = 0; a < n; ++a) {
           const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
           const int ii = (m == 0) ? i : (m == 1) ? j : k;
-          wk0 += Dt.D[a][ii] * s[m * nn + o];
+          const double dw = sD[a * n + ii], ds = sD[ii * n + a];
+          wk0 += dw * s[m * nn + o];
 #pragma unroll
-          for (int f = 0; f < 5; ++f) dd[f] += Dt.D[ii][a] * s[(3 + f) * nn + o];
+          for (int f = 0; f < 5; ++f) dd[f] += ds * s[(3 + f) * nn + o];
         }
         acc[0] += wk0;
 #pragma unroll
@@ -258,9 +261,11 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
   extern __shared__ double sm[];
   const int64_t e = blockIdx.x;
   const int t = threadIdx.x;
+  double* sD = sm + 15 * nn;                      // D (n x n), row-major
+  for (int x = t; x < n * n; x += blockDim.x) sD[x] = Dt.D[x / n][x % n];
   double acc[5];
   int g = 0;
-  euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, elem_layer[e], nlay);
+  euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, elem_layer[e], nlay, sD);
   if (t >= nn) return;
   const int64_t nloc = nelem * nn;
   const int64_t p = e * nn + t;
@@ -286,8 +291,10 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::D
   extern __shared__ double sm[];
   double* s_carry = sm + 15 * nn;                 // [2][n*n][5]
   int* s_code = reinterpret_cast<int*>(s_carry + 2 * n * n * 5);   // [n*n]
+  double* sD = s_carry + 2 * n * n * 5 + (n * n + 1) / 2;           // D (n x n), row-major
   const int64_t tl = blockIdx.x;
   const int t = threadIdx.x;
+  for (int x = t; x < n * n; x += blockDim.x) sD[x] = Dt.D[x / n][x % n];
   const int i = t / (n * n), j = (t / n) % n, k = t % n;
   const int nlay = A.nlay;
   if (t < n * n) s_code[t] = A.code[tl * n * n + t];
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::D
     const int64_t e = elem[tl * nlay + l];
     double acc[5];
     int g = 0;
-    euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, l, nlay);
+    euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, l, nlay, sD);
     if (t < nn) {
       double* cw = s_carry + (l & 1) * n * n * 5 + (i * n + j) * 5;
       const double* cr = s_carry + ((l + 1) & 1) * n * n * 5 + (i * n + j) * 5;
@@ -333,7 +340,7 @@ int run_tile(const double* Drow, const EulerConsts& K, int64_t nelem, const int3
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;
-  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n * 5) + sizeof(int) * n * n;
+  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n * 5 + (n * n + 1) / 2 + n * n);
   auto kern = euler_tile_kernel<n>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)A.ntiles, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
@@ -361,7 +368,7 @@ int run_elem(const double* Drow, const EulerConsts& K, int64_t nelem, const int3
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;
-  const size_t smem = sizeof(double) * 15 * nn;
+  const size_t smem = sizeof(double) * (15 * nn + n * n);
   auto kern = euler_elem_kernel<n>;
   if (smem > 48 * 1024) HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)nelem, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, work, elem_layer, nlay);
