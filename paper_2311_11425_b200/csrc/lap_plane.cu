@@ -118,7 +118,10 @@ struct PlaneCfg {
   static constexpr int OFF_C = OFF_T + 2 * UV;
   static constexpr int OFF_P = OFF_C + (UV + 1) / 2;
   static constexpr int OFF_BAR = (OFF_P + (UV + 1) / 2 + 1) & ~1;
-  static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + 2);
+  // split planes (H > 1): D in shared memory for the xi exchange, whose row / column offsets vary
+  // across the lanes of a warp (constant-bank loads would serialise)
+  static constexpr int OFF_D = OFF_BAR + 2;
+  static constexpr size_t SMEM = sizeof(double) * (OFF_D + (H > 1 ? n * n : 0));
 };
 
 // Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
   int* s_code = reinterpret_cast<int*>(sm + C::OFF_C); // [UV] partial row or -1
   int* s_perm = reinterpret_cast<int*>(sm + C::OFF_P); // [UV] output column order: tile-owned first
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // metric stage (WV 0)
+  double* sD = sm + C::OFF_D;                          // [n][n] (H > 1)
   const int tid = threadIdx.x;
   const int f = tid % F;
   const int ih = (tid / F) % H;       // thread order (jp, e, ih, f): f fastest (metric pairs broadcast),
@@ -292,6 +296,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
   }
   issue_gather(gcur);
   if (nlay > 1) load_gids(1, gnext);
+  if constexpr (H > 1)
+    for (int x = tid; x < n * n; x += C::NT) sD[x] = Dt.D[x / n][x % n];
   __syncthreads();
   if (tid == 0) {   // output items walk the tile-owned columns first (uniform warps in step f)
     int c = 0;
@@ -361,12 +367,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
           for (int r = 0; r < NR; ++r) {
             double s = 0.0;
 #pragma unroll
-            for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + r][I0 + a], co[a], s);
+            for (int a = 0; a < NR; ++a) s = fma(sD[(I0 + r) * n + I0 + a], co[a], s);
 #pragma unroll
             for (int m = 1; m < H; ++m) {
               const int pb = (ih ^ m) * NR;
 #pragma unroll
-              for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + r][pb + a], cp[m - 1][a], s);
+              for (int a = 0; a < NR; ++a) s = fma(sD[(I0 + r) * n + pb + a], cp[m - 1][a], s);
             }
             p0[r][k] = s;
           }
@@ -513,12 +519,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
           for (int r = 0; r < NR; ++r) {
             double s = 0.0;
 #pragma unroll
-            for (int a = 0; a < NR; ++a) s = fma(Dt.D[I0 + a][I0 + r], co[a], s);
+            for (int a = 0; a < NR; ++a) s = fma(sD[(I0 + a) * n + I0 + r], co[a], s);
 #pragma unroll
             for (int m = 1; m < H; ++m) {
               const int pb = (ih ^ m) * NR;
 #pragma unroll
-              for (int a = 0; a < NR; ++a) s = fma(Dt.D[pb + a][I0 + r], cp[m - 1][a], s);
+              for (int a = 0; a < NR; ++a) s = fma(sD[(pb + a) * n + I0 + r], cp[m - 1][a], s);
             }
             p0[r][k] = -s;
           }
