@@ -62,7 +62,12 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
   const int t = threadIdx.x;
   const int64_t M = (int64_t)NV * n_z;
   double* bc = band + c * R * M;
-  const double* w = Wz.D[0];
+  // D and the zeta weights in shared memory: the entry loop indexes them with thread-varying
+  // (i, a) (constant-bank loads would serialise across the warp)
+  __shared__ double sDm[n][n], sw[n];
+  for (int x = t; x < n * n; x += blockDim.x) sDm[x / n][x % n] = Dt.D[x / n][x % n];
+  if (t < n) sw[t] = Wz.D[0][t];
+  const double* w = sw;
   for (int e = t; e < R * TW; e += blockDim.x) T[e / TW][e % TW] = (e / TW == D0) ? 1.0 : 0.0;   // band = I
   __syncthreads();
   const int32_t* cg = col_gid + c * (int64_t)n_z;
@@ -145,22 +150,22 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
         const double uz_i = L.mask[i] * (L.q[1][i] * L.z[0][i] + L.q[2][i] * L.z[1][i] + L.q[3][i] * L.z[2][i]);
         const double uz_a = L.mask[a] * (L.q[1][a] * L.z[0][a] + L.q[2][a] * L.z[1][a] + L.q[3][a] * L.z[2][a]);
         if (vi == 0) {
-          if (va == 0) B = (w[a] * Dt.D[a][i]) * (L.J[a] * uz_a);
-          else if (va <= 3) B = (w[a] * Dt.D[a][i]) * (L.J[a] * (L.mask[a] * rho_a * L.z[va - 1][a]));
+          if (va == 0) B = (w[a] * sDm[a][i]) * (L.J[a] * uz_a);
+          else if (va <= 3) B = (w[a] * sDm[a][i]) * (L.J[a] * (L.mask[a] * rho_a * L.z[va - 1][a]));
         } else if (vi <= 3) {
           const double zc = L.z[vi - 1][i];
           if (va == 0) {
             const double dg = (i == a) ? (wj_i * (-zc / (rho_i * rho_i)) * L.dPz[i]) : 0.0;
-            B = -(dg + ((wj_i * zc / rho_i) * Dt.D[i][a]) * L.dP[0][a]);
+            B = -(dg + ((wj_i * zc / rho_i) * sDm[i][a]) * L.dP[0][a]);
           } else if (va <= 3) {
             const double dg = (i == a) ? (wj_i * L.mask[i] * L.z[va - 1][i] * L.dfld[vi - 1][i]) : 0.0;
-            B = (va == vi) ? -(dg + (wj_i * uz_i) * Dt.D[i][a]) : -dg;
+            B = (va == vi) ? -(dg + (wj_i * uz_i) * sDm[i][a]) : -dg;
           } else {
-            B = -(((wj_i * zc / rho_i) * Dt.D[i][a]) * L.dP[4][a]);
+            B = -(((wj_i * zc / rho_i) * sDm[i][a]) * L.dP[4][a]);
           }
         } else {
           if (va >= 1 && va <= 3) B = (i == a) ? -(wj_i * L.mask[i] * L.z[va - 1][i] * L.dth[i]) : 0.0;
-          else if (va == 4) B = -((wj_i * uz_i) * Dt.D[i][a]);
+          else if (va == 4) B = -((wj_i * uz_i) * sDm[i][a]);
         }
       } else {
         const bool three = (K.set == 2);
@@ -168,7 +173,7 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
         const double uz_a = Uz_a / rho_a;
         const double dUz_a = (va >= 1 && va <= 3) ? L.mask[a] * L.z[va - 1][a] : 0.0;
         if (vi == 0) {
-          B = (w[a] * Dt.D[a][i]) * (L.J[a] * dUz_a);
+          B = (w[a] * sDm[a][i]) * (L.J[a] * dUz_a);
         } else if (vi == 4) {
           const double T5 = L.q[4][a];
           double dF;
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
             else if (va <= 3) dF = L.mask[a] * L.z[va - 1][a] * EP / rho_a + uz_a * L.dP[va][a];
             else dF = uz_a * (1.0 + L.dP[4][a]);
           }
-          B = (w[a] * Dt.D[a][i]) * (L.J[a] * dF);
+          B = (w[a] * sDm[a][i]) * (L.J[a] * dF);
         } else {
           const int comp = vi;
           const double zc_a = L.z[comp - 1][a];
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
             if (va == comp) d = d + uz_a;
             df = L.J[a] * d;
           }
-          B = -((w[i] * Dt.D[i][a]) * df);
+          B = -((w[i] * sDm[i][a]) * df);
           if (va == 0 && i == a) B = B + -(wj_i * L.dphi[i] * L.z[comp - 1][i]);
         }
       }
