@@ -72,72 +72,104 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
   __syncthreads();
   const int32_t* cg = col_gid + c * (int64_t)n_z;
   const double* qc = qcol + c * (int64_t)n_z * NV;
-  for (int l = 0; l < nlay; ++l) {
-    if (t < n) {
-      const int i = t;
-      const int z = l * N + i;
-      const int g = cg[z];
+  // node data of the whole column, once, by n_z threads (not n threads per layer): state, J, grad
+  // zeta, mask, Phi, P, dP/dq (state.py:104-125) and the column mass DSS(w_z J) (euler.py:76-78:
+  // at a node shared by two layers the lower layer's top weight first)
+  extern __shared__ double colsm[];
+  double* cq = colsm;                    // [5][n_z]
+  double* cJ = cq + NV * n_z;
+  double* cz = cJ + n_z;                 // [3][n_z]
+  double* cmask = cz + 3 * n_z;
+  double* cphi = cmask + n_z;
+  double* cP = cphi + n_z;
+  double* cdP = cP + n_z;                // [5][n_z]
+  double* cmass = cdP + NV * n_z;
+  double* cder = cmass + n_z;            // [6][nlay * n]: Dz of Phi, P, U, V, W, Theta per layer node
+  for (int z = t; z < n_z; z += blockDim.x) {
+    const int g = cg[z];
+    double qv[NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) L.q[v][i] = qc[(int64_t)z * NV + v];
-      const double J = Jg[g];
-      L.J[i] = J;
+    for (int v = 0; v < NV; ++v) cq[v * n_z + z] = qv[v] = qc[(int64_t)z * NV + v];
+    const double J = Jg[g];
+    cJ[z] = J;
 #pragma unroll
-      for (int d = 0; d < 3; ++d) L.z[d][i] = gz[(int64_t)g * 3 + d];
-      L.mask[i] = mask_g[g];
-      L.phi[i] = Phi_g[g];
-      // column mass DSS(w_z J) at this node (euler.py:76-78): previous layer's top first
-      double m = 0.0;
-      if (i == 0 && l > 0) m = m + w[N] * J;
-      m = m + w[i] * J;
-      if (i == N && l < nlay - 1) m = m + w[0] * J;
-      L.mass[i] = m;
-      const double rho = L.q[0][i];
-      double P;
-      if (K.set == 0) P = K.P_A * pow(rho * K.R * L.q[4][i] / K.P_A, K.gamma);
-      else if (K.set == 1) P = K.P_A * pow(K.R * L.q[4][i] / K.P_A, K.gamma);
-      else {
-        const double ke = 0.5 * (L.q[1][i] * L.q[1][i] + L.q[2][i] * L.q[2][i] + L.q[3][i] * L.q[3][i]) / rho;
-        P = (K.gamma - 1.0) * (L.q[4][i] - ke - rho * L.phi[i]);
-      }
-      L.P[i] = P;
-      // dP/dq (state.py:104-125)
-      if (K.set == 0) {
-        L.dP[0][i] = K.gamma * P / rho;
-        L.dP[1][i] = L.dP[2][i] = L.dP[3][i] = 0.0;
-        L.dP[4][i] = K.gamma * P / L.q[4][i];
-      } else if (K.set == 1) {
-        L.dP[0][i] = L.dP[1][i] = L.dP[2][i] = L.dP[3][i] = 0.0;
-        L.dP[4][i] = K.gamma * P / L.q[4][i];
-      } else {
-        const double g1 = K.gamma - 1.0;
-        const double ke2 = L.q[1][i] * L.q[1][i] + L.q[2][i] * L.q[2][i] + L.q[3][i] * L.q[3][i];
-        L.dP[0][i] = g1 * (0.5 * ke2 / (rho * rho) - L.phi[i]);
-        L.dP[1][i] = -g1 * L.q[1][i] / rho;
-        L.dP[2][i] = -g1 * L.q[2][i] / rho;
-        L.dP[3][i] = -g1 * L.q[3][i] / rho;
-        L.dP[4][i] = g1;
-      }
+    for (int d = 0; d < 3; ++d) cz[d * n_z + z] = gz[(int64_t)g * 3 + d];
+    cmask[z] = mask_g[g];
+    const double phi = Phi_g[g];
+    cphi[z] = phi;
+    double m = 0.0;
+    const int i = (z == n_z - 1) ? N : z % N;
+    if (i == 0 && z > 0) m = m + w[N] * J;
+    m = m + w[i] * J;
+    cmass[z] = m;
+    const double rho = qv[0];
+    double P;
+    if (K.set == 0) P = K.P_A * pow(rho * K.R * qv[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+    else {
+      const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
+      P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);
     }
-    __syncthreads();
-    if (t < n) {   // strong zeta derivatives along the layer
-      const int i = t;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
+    cP[z] = P;
+    double dp[NV];
+    if (K.set == 0) {
+      dp[0] = K.gamma * P / rho;
+      dp[1] = dp[2] = dp[3] = 0.0;
+      dp[4] = K.gamma * P / qv[4];
+    } else if (K.set == 1) {
+      dp[0] = dp[1] = dp[2] = dp[3] = 0.0;
+      dp[4] = K.gamma * P / qv[4];
+    } else {
+      const double g1 = K.gamma - 1.0;
+      const double ke2 = qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3];
+      dp[0] = g1 * (0.5 * ke2 / (rho * rho) - phi);
+      dp[1] = -g1 * qv[1] / rho;
+      dp[2] = -g1 * qv[2] / rho;
+      dp[3] = -g1 * qv[3] / rho;
+      dp[4] = g1;
+    }
 #pragma unroll
-      for (int a = 0; a < n; ++a) {
-        const double d = Dt.D[i][a];
-        a0 += d * L.phi[a];
-        a1 += d * L.P[a];
-        a2 += d * L.q[1][a];
-        a3 += d * L.q[2][a];
-        a4 += d * L.q[3][a];
-        a5 += d * L.q[4][a];
-      }
-      L.dphi[i] = a0;
-      L.dPz[i] = a1;
-      L.dfld[0][i] = a2;
-      L.dfld[1][i] = a3;
-      L.dfld[2][i] = a4;
-      L.dth[i] = a5;
+    for (int v = 0; v < NV; ++v) cdP[v * n_z + z] = dp[v];
+  }
+  __syncthreads();
+  for (int x = t; x < nlay * n; x += blockDim.x) {   // strong zeta derivatives along each layer
+    const int l = x / n, i = x % n, z0 = l * N;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0;
+#pragma unroll
+    for (int a = 0; a < n; ++a) {
+      const double d = sDm[i][a];
+      a0 += d * cphi[z0 + a];
+      a1 += d * cP[z0 + a];
+      a2 += d * cq[1 * n_z + z0 + a];
+      a3 += d * cq[2 * n_z + z0 + a];
+      a4 += d * cq[3 * n_z + z0 + a];
+      a5 += d * cq[4 * n_z + z0 + a];
+    }
+    const int nl = nlay * n;
+    cder[0 * nl + x] = a0;
+    cder[1 * nl + x] = a1;
+    cder[2 * nl + x] = a2;
+    cder[3 * nl + x] = a3;
+    cder[4 * nl + x] = a4;
+    cder[5 * nl + x] = a5;
+  }
+  __syncthreads();
+  for (int l = 0; l < nlay; ++l) {
+    // this layer's node view (parallel copy of the column arrays)
+    const int z0 = l * N, nl = nlay * n;
+    for (int x = t; x < 24 * n; x += blockDim.x) {
+      const int f = x / n, i = x % n, z = z0 + i, li = l * n + i;
+      double v;
+      if (f < 5) v = cq[f * n_z + z];
+      else if (f == 5) v = cJ[z];
+      else if (f < 9) v = cz[(f - 6) * n_z + z];
+      else if (f == 9) v = cmask[z];
+      else if (f == 10) v = cphi[z];
+      else if (f == 11) v = cP[z];
+      else if (f < 17) v = cdP[(f - 12) * n_z + z];
+      else if (f == 17) v = cmass[z];
+      else v = cder[(f - 18) * nl + li];
+      (&L.q[0][0])[f * n + i] = v;   // LayerNodes is 24 consecutive [n] arrays in this order
     }
     __syncthreads();
     // block entries (i, vi, a, va)
@@ -239,8 +271,11 @@ int run_jacobian(const double* hD, const double* hw, const ColConsts& K, int64_t
   hv::DTab<n> Dt, Wz{};
   hv::fill_dtab(Dt, hD);
   for (int i = 0; i < n; ++i) Wz.D[0][i] = hw[i];
-  column_jacobian_kernel<n><<<(unsigned)ncol, 256, 0, st>>>(Dt, Wz, K, nlay, n_z, col_gid, qcol, Jg, gz, mask, Phi,
-                                                             band);
+  const size_t smem = sizeof(double) * ((size_t)18 * n_z + (size_t)6 * nlay * n);   // column node arrays
+  auto kern = column_jacobian_kernel<n>;
+  if (smem > 160 * 1024) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_column_jacobian: column too tall (n_z=%d)", n_z);
+  HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)ncol, 256, smem, st>>>(Dt, Wz, K, nlay, n_z, col_gid, qcol, Jg, gz, mask, Phi, band);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
