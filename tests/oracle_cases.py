@@ -9,8 +9,8 @@ from oracle import hevi_oracle as O
 from paper_2311_11425_b200 import synthetic
 
 
-def oracle_mesh(name):
-    c = CASES[name]
+def oracle_mesh(name, case=None):
+    c = CASES[name] if case is None else case
     if c["kind"] == "lattice":
         coords, layer, hcol = synthetic.perturbed_box_coords(c["nx"], c["ny"], c["nv"], c["N"], c["extents"])
         tol = O.dedupe_tol("box", max(c["nx"], c["ny"]), extents=c["extents"])
@@ -27,10 +27,10 @@ def oracle_mesh(name):
 class OracleProblem:
     """Mesh + projected curl-invariant metrics + G_nu + mass for one case."""
 
-    def __init__(self, name):
-        c = CASES[name]
+    def __init__(self, name, case=None):
+        c = CASES[name] if case is None else case
         self.name, self.c = name, c
-        self.m = m = oracle_mesh(name)
+        self.m = m = oracle_mesh(name, c)
         self.dxdxi, self.J, self.grad = O.curl_metrics(m)
         self.Jg0, self.gz0 = O.naive_gridpoint(m, self.J, self.grad)
         self.Jg, self.gz = O.project_columns(m, self.J, self.grad)

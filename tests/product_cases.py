@@ -6,8 +6,8 @@ from cases import CASES
 from paper_2311_11425_b200 import euler, hyperdiff, mesh as hm, metrics, state
 
 
-def product_mesh(name):
-    c = CASES[name]
+def product_mesh(name, case=None):
+    c = CASES[name] if case is None else case
     if c["kind"] == "lattice":
         return hm.build_box_lattice(c["nx"], c["ny"], c["nv"], c["N"], c["extents"])
     if c["kind"] == "sphere":
@@ -18,10 +18,10 @@ def product_mesh(name):
 
 
 class ProductProblem:
-    def __init__(self, name, set_name="2C"):
-        c = CASES[name]
+    def __init__(self, name, set_name="2C", case=None):
+        c = CASES[name] if case is None else case
         self.c = c
-        self.m = product_mesh(name)
+        self.m = product_mesh(name, c)
         self.mets0 = metrics.curl_invariant_metrics(self.m)
         self.mets = metrics.project_metrics_to_columns(self.mets0, self.m)
         self.cfg = hyperdiff.HyperDiffConfig(**c["hd"])

@@ -1,0 +1,108 @@
+"""GPU checks at BASELINE.json's full sizes.
+
+* Config 2 at full size (32x32x8 elements, N = 4) against the CPU oracle: H_nu within 1e-12 relative L2.
+* Config 5's per-GPU block (128x128x32 elements, 65.5 M element nodes, the bench workload) through
+  size-independent properties of the operator: the assembled Laplacian M L is symmetric and negative
+  semi-definite (the weak form is -sum D^T W D with W symmetric positive), annihilates constants,
+  is linear, and the result is bitwise reproducible run to run.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from cases import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+C2_FULL = dict(kind="lattice", nx=32, ny=32, nv=8, N=4, extents=(1.0e5, 1.0e5, 1.0e4),
+               hd=dict(alpha=2, c=(0.05, 0.05, 0.0)), dt=0.5, state="fourier", sets=("2C",), omega=0.0,
+               lap_fields=(1,))
+
+
+def test_c2_full_size_parity():
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    p = ProductProblem("c2_full", case=C2_FULL)
+    o = OracleProblem("c2_full", case=C2_FULL)
+    assert p.m.nelem == 8192 and p.m.nglobal == o.m.ng == 549153
+    assert np.array_equal(p.m.gid, o.m.gid)
+    assert p.ops.lap_plan(p.vm).wform == 1          # the axis form is what runs at this size
+    got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
+    assert rel_l2(got, o.hyper()) <= 1e-12
+    lap = hyperdiff.laplacian_apply(o.state[:, 1], p.vm, p.ops)
+    assert rel_l2(lap, o.lap(1)) <= 1e-12
+
+
+C3_FULL = dict(kind="sphere", ne=30, nv=10, N=4, radius=6.371e6, z_top=1.0e4,
+               hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere", sets=("2C",), omega=0.0,
+               lap_fields=(1,))
+
+
+def test_c3_full_size_parity():
+    """Config 3 at full size (cubed sphere 6 x 30 x 30 x 10, N = 4; ~1 min of oracle time on the host)."""
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    p = ProductProblem("c3_full", case=C3_FULL)
+    o = OracleProblem("c3_full", case=C3_FULL)
+    assert p.m.nelem == 54000 and p.m.nglobal == o.m.ng == 3542482
+    assert np.array_equal(p.m.gid, o.m.gid)
+    got = hyperdiff.hyperdiffusion_apply(state.StateField("2C", o.state), p.cfg, p.vm, p.ops)
+    assert rel_l2(got, o.hyper()) <= 1e-12
+
+
+@pytest.fixture(scope="module")
+def c5():
+    import bench
+
+    return bench.build_workload("c5", 0, 1)
+
+
+def _dot(a, b, w):
+    return float((a * b * w[:, None]).sum())
+
+
+def test_c5_full_size_properties(c5):
+    import torch
+
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    ops, vm, cfg, m = c5["ops"], c5["vm"], c5["cfg"], c5["m"]
+    ng = m.nglobal
+    assert m.nelem == 524288
+    fields = [0, 1, 2, 3]
+    M = ops.mass.d_M
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q1 = torch.randn((ng, 4), dtype=torch.float64, device="cuda", generator=g)
+    q2 = torch.randn((ng, 4), dtype=torch.float64, device="cuda", generator=g)
+    L1 = hyperdiff.laplacian_apply_fields(q1, vm, ops, fields)
+    L2 = hyperdiff.laplacian_apply_fields(q2, vm, ops, fields)
+    # symmetry of M L: <q2, M L q1> == <q1, M L q2>
+    a, b = _dot(q2, L1, M), _dot(q1, L2, M)
+    scale = float(torch.sqrt((q1 * q1 * M[:, None]).sum() * (L2 * L2 * M[:, None]).sum()))
+    assert abs(a - b) <= 1e-12 * scale, (a, b, scale)
+    # negative semi-definite: <q, M L q> <= 0 for every field
+    for f in fields:
+        assert float((q1[:, f] * L1[:, f] * M).sum()) < 0.0
+    # constants are annihilated
+    ones = torch.ones((ng, 4), dtype=torch.float64, device="cuda")
+    Lc = hyperdiff.laplacian_apply_fields(ones, vm, ops, fields)
+    assert float(Lc.abs().max()) <= 1e-12 * float(L1.abs().max())
+    # linearity and bitwise reproducibility of H_nu on the benchmark state
+    q = c5["q"]
+    qd = q if torch.is_tensor(q) else q.data
+    H = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg, vm, ops)
+    H2 = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg, vm, ops)
+    assert torch.equal(H, H2)
+    assert float(H[:, 0].abs().max()) == 0.0
+    qb = qd.clone()
+    qb[:, 1:] = 2.0 * qd[:, 1:] - 0.5 * torch.roll(qd[:, 1:], 1, 0)
+    Hb = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qb), cfg, vm, ops)
+    Hr = hyperdiff.hyperdiffusion_apply(state.StateField("2C", torch.roll(qd, 1, 0).contiguous()), cfg, vm, ops)
+    lin = 2.0 * H - 0.5 * Hr
+    assert float((Hb - lin).norm() / lin.norm()) <= 1e-13
