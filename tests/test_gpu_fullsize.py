@@ -95,7 +95,8 @@ def test_c5_full_size_properties(c5):
     assert float(Lc.abs().max()) <= 1e-12 * float(L1.abs().max())
     # linearity and bitwise reproducibility of H_nu on the benchmark state
     q = c5["q"]
-    qd = q if torch.is_tensor(q) else q.data
+    q = q.data if hasattr(q, "data") and not torch.is_tensor(q) else q
+    qd = (q if torch.is_tensor(q) else torch.from_numpy(np.ascontiguousarray(q))).cuda()
     H = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg, vm, ops)
     H2 = hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg, vm, ops)
     assert torch.equal(H, H2)
