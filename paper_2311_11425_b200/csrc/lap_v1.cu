@@ -24,8 +24,10 @@ __global__ void __launch_bounds__(512) lap_elem_v1(hv::DTab<n> Dt, const int32_t
   extern __shared__ double smem_v1[];
   double(*sq)[nn] = reinterpret_cast<double(*)[nn]>(smem_v1);
   double(*sf)[NF][nn] = reinterpret_cast<double(*)[NF][nn]>(smem_v1 + NF * nn);
+  double(*sD)[n] = reinterpret_cast<double(*)[n]>(smem_v1 + 4 * NF * nn);   // D: thread-varying rows
   const int64_t e = blockIdx.x;
   const int t = threadIdx.x;
+  for (int x = t; x < n * n; x += blockDim.x) sD[x / n][x % n] = Dt.D[x / n][x % n];
   const bool act = t < nn;
   const int i = t / (n * n), j = (t / n) % n, k = t % n;
   const int64_t p = e * nn + t;
@@ -43,9 +45,9 @@ __global__ void __launch_bounds__(512) lap_elem_v1(hv::DTab<n> Dt, const int32_t
       double d0 = 0.0, d1 = 0.0, d2 = 0.0;
 #pragma unroll
       for (int a = 0; a < n; ++a) {
-        d0 += Dt.D[i][a] * sq[f][(a * n + j) * n + k];
-        d1 += Dt.D[j][a] * sq[f][(i * n + a) * n + k];
-        d2 += Dt.D[k][a] * sq[f][(i * n + j) * n + a];
+        d0 += sD[i][a] * sq[f][(a * n + j) * n + k];
+        d1 += sD[j][a] * sq[f][(i * n + a) * n + k];
+        d2 += sD[k][a] * sq[f][(i * n + j) * n + a];
       }
       sf[0][f][t] = w00 * d0 + w01 * d1 + w02 * d2;
       sf[1][f][t] = w01 * d0 + w11 * d1 + w12 * d2;
@@ -59,9 +61,9 @@ __global__ void __launch_bounds__(512) lap_elem_v1(hv::DTab<n> Dt, const int32_t
       double s = 0.0;
 #pragma unroll
       for (int a = 0; a < n; ++a) {
-        s += Dt.D[a][i] * sf[0][f][(a * n + j) * n + k];
-        s += Dt.D[a][j] * sf[1][f][(i * n + a) * n + k];
-        s += Dt.D[a][k] * sf[2][f][(i * n + j) * n + a];
+        s += sD[a][i] * sf[0][f][(a * n + j) * n + k];
+        s += sD[a][j] * sf[1][f][(i * n + a) * n + k];
+        s += sD[a][k] * sf[2][f][(i * n + j) * n + a];
       }
       work[f * nloc + p] = -s;
     }
@@ -99,7 +101,7 @@ int run_v1(const hv_lap_plan* P, const double* q, int64_t ldq, const hv::FieldMa
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, P->D);
   const int threads = ((nn + 31) / 32) * 32;
-  const size_t smem = sizeof(double) * 4 * NF * nn;
+  const size_t smem = sizeof(double) * (4 * NF * nn + n * n);
   auto kern = lap_elem_v1<n, NF>;
   if (smem > 48 * 1024) HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)P->nelem, threads, smem, st>>>(Dt, P->d_gid, P->d_W, nloc, q, ldq, qf, P->d_work);
