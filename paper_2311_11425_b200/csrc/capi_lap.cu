@@ -55,6 +55,8 @@ bool use_tiles(const hv_lap_plan* P, int nf) {
 int lap_local(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
               int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st, int accumulate,
               int64_t t0 = 0, int64_t t1 = -1, int pack = 1) {
+  if ((reinterpret_cast<uintptr_t>(out) & 15) != 0)
+    HV_FAIL(HV_ERR_INVALID, "hv_lap_local: the output must be 16-byte aligned");
   hv::TileArgs A = tile_args(P, q, ldq, qf, out, ldo, of, scale, zero_mask, accumulate);
   A.tile0 = t0;
   A.tile1 = (t1 < 0) ? P->ntiles : t1;
@@ -73,7 +75,10 @@ int lap_finish(const hv_lap_plan* P, int nf, double* out, int64_t ldo, const hv:
 int lap_pass(const hv_lap_plan* P, const double* q, int64_t ldq, int nf, const hv::FieldMap& qf, double* out,
              int64_t ldo, const hv::FieldMap& of, double scale, unsigned zero_mask, cudaStream_t st,
              int accumulate = 0) {
-  if (use_tiles(P, nf)) {
+  // the sweeps write output rows with 16-byte stores: an output not 16-byte aligned (a caller's
+  // offset view) takes the element-parallel path, which stores doubles
+  const bool aligned = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (use_tiles(P, nf) && aligned) {
     if (P->d_slot_ext && P->next > 0)
       HV_FAIL(HV_ERR_INVALID, "multi-GPU plan: use hv_lap_local / exchange / hv_lap_finish");
     int rc = lap_local(P, q, ldq, nf, qf, out, ldo, of, scale, zero_mask, st, accumulate);

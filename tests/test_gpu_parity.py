@@ -455,3 +455,25 @@ def test_euler_column_sweep_vs_element_path(monkeypatch):
         assert rel_l2(full, oe.rhs_full(rs)) <= TOL and rel_l2(full, full2) <= 1e-13, s
         assert rel_l2(hor, oe.rhs_horizontal_nohd(rs)) <= TOL and rel_l2(hor, hor2) <= 1e-13, s
         assert rel_l2(acc.cpu().numpy() - 1.0, full) <= 1e-12, s
+
+
+def test_misaligned_output_view():
+    """An output that is not 16-byte aligned (an offset view) takes the element-parallel path
+    (the sweeps store rows with 16-byte stores) and gives the same result."""
+    import torch
+
+    from product_cases import ProductProblem
+    from oracle_cases import OracleProblem
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    p = ProductProblem("box_p_n4")
+    o = OracleProblem("box_p_n4")
+    q = torch.from_numpy(o.state).cuda()
+    ref = hyperdiff.hyperdiffusion_apply(state.StateField("2C", q), p.cfg, p.vm, p.ops)
+    ng = q.shape[0]
+    big = torch.full((ng * 5 + 1,), float("nan"), dtype=torch.float64, device="cuda")
+    out = big[1:].view(ng, 5)
+    assert out.data_ptr() % 16 == 8
+    hyperdiff.hyperdiffusion_apply(state.StateField("2C", q), p.cfg, p.vm, p.ops, out=out)
+    assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
+    assert rel_l2(out.cpu().numpy(), o.hyper()) <= TOL
