@@ -195,6 +195,10 @@ int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* d_gt, const
                       void* stream);
 int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* d_elem, const double* d_W,
                         int64_t nloc, int layout, double* d_Wt, void* stream);
+/* Doubles per tile-layer of the plane kernel's packed metric in form wform (0: 6 components,
+ * 1: axis, 2: isotropic -- rows padded for conflict-free shared-memory reads where tuned);
+ * d_Wt of hv_tile_pack_metric holds ntiles * nlay of them.  -1 for bad arguments. */
+int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform);
 
 /* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
  * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].

@@ -114,9 +114,14 @@ extern "C" int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nl
   if (N < 1 || N > 8 || TX < 1 || TY < 1 || ntiles <= 0 || nlay <= 0 || !d_elem || !d_W || !d_Wt)
     HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_metric: bad arguments");
   if (layout >= 1 && layout <= 3 && hv::plane_supported(N, TX, TY, 4))
-    return hv::plane_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, layout - 1, d_Wt, (cudaStream_t)stream);
+    return hv::plane_pack(N, TX, TY, ntiles, nlay, d_elem, d_W, nloc, layout - 1, d_Wt, (cudaStream_t)stream);
   if (layout >= 2) HV_FAIL(HV_ERR_UNSUPPORTED, "hv_tile_pack_metric: axis / isotropic form needs the plane kernel");
   return hv::tile_pack(N, TX * TY, ntiles, nlay, d_elem, d_W, nloc, d_Wt, (cudaStream_t)stream);
+}
+
+extern "C" int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform) {
+  if (N < 1 || N > 7 || TX < 1 || TY < 1 || wform < 0 || wform > 2) return -1;
+  return hv::plane_metric_doubles(N, TX, TY, wform);
 }
 
 extern "C" int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* d_gt, const double* d_Minv,

@@ -97,17 +97,22 @@ struct PlaneCfg {
   // search (ablate/bank_search.py): every plane / eta-line access of a half-warp then hits
   // 16 distinct 8-byte banks.  Other shapes use the plain padded layout.
   static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2 && H == 1);
+  // N = 7 single-column tiles, H = 4 (tools/bank_search_n7.py: 2.6x fewer wavefronts than the plain layout)
+  static constexpr bool TUNED7 = (n == 8 && TX == 1 && TY == 1 && H == 4 && F == 4);
   static constexpr int pad16(int x) { return x + ((4 - (x % 16)) + 16) % 16; }
   static constexpr int KS = n;                                   // node column (k) stride
-  static constexpr int US = TUNED ? 46 : V * n;                  // u stride of s_q
-  static constexpr int QP = TUNED ? 415 : pad16(NODES);          // s_q field-plane stride
-  static constexpr int BS = n;                                   // scratch: [f][e][a][b][c]
-  static constexpr int AS = TUNED ? 28 : n * n;
-  static constexpr int ES = TUNED ? 147 : n * n * n;
-  static constexpr int SP = TUNED ? 588 : pad16(NE * n * n * n);
+  static constexpr int US = TUNED ? 46 : TUNED7 ? 65 : V * n;    // u stride of s_q
+  static constexpr int QP = TUNED ? 415 : TUNED7 ? 521 : pad16(NODES);   // s_q field-plane stride
+  static constexpr int BS = TUNED7 ? 9 : n;                      // scratch: [f][e][a][b][c]
+  static constexpr int AS = TUNED ? 28 : TUNED7 ? 75 : n * n;
+  static constexpr int ES = TUNED ? 147 : TUNED7 ? 600 : n * n * n;
+  static constexpr int SP = TUNED ? 588 : TUNED7 ? 600 : pad16(NE * n * n * n);
+  // isotropic metric (WF 2): [i][k][e][j] with an i-row stride padded where tuned
+  // (the packing must agree for every kernel variant of the shape: keyed on n and the tile only)
+  static constexpr int MIS = NE * n * n + ((n == 8 && TX == 1 && TY == 1) ? 1 : 0);
   static constexpr int SQ = QP * F;
   static constexpr int SE = SP * F;
-  static constexpr int WL = (WF == 2 ? 1 : WF == 1 ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
+  static constexpr int WL = WF == 2 ? n * MIS : (WF == 1 ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
   static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
   static constexpr int FI = UV * N;                      // output items per layer (k < N)
   static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
@@ -414,7 +419,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
         double d1[n], sv[n];
 #pragma unroll
         for (int k = 0; k < n; ++k) {
-          sv[k] = Sw[(i * n + k) * NE * n];
+          sv[k] = Sw[i * C::MIS + k * NE * n];
           d1[k] = s_s[sidx(e, i, jp, k)];
         }
 #pragma unroll
@@ -645,12 +650,18 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
 // axis form (axis == 1, W = U (3, nloc)): Wp[t][l][c][i][k][e][j] = U[c][...];
 // isotropic form (axis == 2, W = s (1, nloc)): Wp[t][l][i][k][e][j] = s[...].
 __global__ void plane_pack_metric(int n, int NE, int64_t ntiles, int nlay, const int32_t* __restrict__ elem,
-                                  const double* __restrict__ W, int64_t nloc, int axis, double* __restrict__ Wp) {
-  const int64_t per = (int64_t)(axis == 2 ? 1 : axis ? 3 : 6) * n * n * NE * n;
+                                  const double* __restrict__ W, int64_t nloc, int axis, int mis,
+                                  double* __restrict__ Wp) {
+  const int64_t per = axis == 2 ? (int64_t)n * mis : (int64_t)(axis ? 3 : 6) * n * n * NE * n;
   const int64_t total = ntiles * nlay * per;
   for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tl = id / per;
     int64_t r = id % per;
+    if (axis == 2) {   // [i][mis]: k, e, j in the first n * NE * n of a row, zero padding after
+      const int i = (int)(r / mis), rr = (int)(r % mis);
+      if (rr >= n * NE * n) { Wp[id] = 0.0; continue; }
+      r = (int64_t)(i * n + rr / (NE * n)) * NE * n + rr % (NE * n);
+    }
     int h = 0;
     if (!axis) { h = (int)(r % 2); r /= 2; }
     const int j = (int)(r % n); r /= n;
@@ -783,9 +794,21 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
   HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no instantiation for N=%d F=%d", N, F);
 }
 
-int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
+int plane_metric_row(int N, int TX, int TY) {
+  if (N == 7 && TX == 1 && TY == 1) return PlaneCfg<8, 1, 1, 4, 0, 4, 2>::MIS;
+  return (N + 1) * TX * TY * (N + 1);
+}
+
+int64_t plane_metric_doubles(int N, int TX, int TY, int wform) {
+  const int n = N + 1;
+  if (wform == 2) return (int64_t)n * plane_metric_row(N, TX, TY);
+  return (int64_t)(wform == 1 ? 3 : 6) * n * TX * TY * n * n;
+}
+
+int plane_pack(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
                int axis, double* Wp, cudaStream_t st) {
-  plane_pack_metric<<<148 * 8, 256, 0, st>>>(N + 1, NE, ntiles, nlay, elem, W, nloc, axis, Wp);
+  plane_pack_metric<<<148 * 8, 256, 0, st>>>(N + 1, TX * TY, ntiles, nlay, elem, W, nloc, axis,
+                                             plane_metric_row(N, TX, TY), Wp);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

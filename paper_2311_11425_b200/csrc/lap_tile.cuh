@@ -45,8 +45,9 @@ int slot_pack(const TileArgs& A, int F, cudaStream_t st);
 int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
-int plane_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
+int plane_pack(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
                int axis, double* Wp, cudaStream_t st);
+int64_t plane_metric_doubles(int N, int TX, int TY, int wform);
 int laplacian_tile(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* gt, const double* Minv, double* Mt, cudaStream_t st);
 int tile_pack(int N, int NE, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,
