@@ -97,16 +97,16 @@ struct PlaneCfg {
   // search (ablate/bank_search.py): every plane / eta-line access of a half-warp then hits
   // 16 distinct 8-byte banks.  Other shapes use the plain padded layout.
   static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2 && H == 1);
-  // N = 7 single-column tiles, H = 4 (tools/bank_search_n7.py: 2.6x fewer wavefronts than the plain layout)
+  // N = 7 single-column tiles, H = 4 (tools/bank_search_n7.py, half-warp model: ~2x fewer wavefronts than plain)
   static constexpr bool TUNED7 = (n == 8 && TX == 1 && TY == 1 && H == 4 && F == 4);
   static constexpr int pad16(int x) { return x + ((4 - (x % 16)) + 16) % 16; }
   static constexpr int KS = n;                                   // node column (k) stride
-  static constexpr int US = TUNED ? 46 : TUNED7 ? 65 : V * n;    // u stride of s_q
-  static constexpr int QP = TUNED ? 415 : TUNED7 ? 521 : pad16(NODES);   // s_q field-plane stride
-  static constexpr int BS = TUNED7 ? 9 : n;                      // scratch: [f][e][a][b][c]
-  static constexpr int AS = TUNED ? 28 : TUNED7 ? 75 : n * n;
-  static constexpr int ES = TUNED ? 147 : TUNED7 ? 600 : n * n * n;
-  static constexpr int SP = TUNED ? 588 : TUNED7 ? 600 : pad16(NE * n * n * n);
+  static constexpr int US = TUNED ? 46 : TUNED7 ? 66 : V * n;    // u stride of s_q
+  static constexpr int QP = TUNED ? 415 : TUNED7 ? 529 : pad16(NODES);   // s_q field-plane stride
+  static constexpr int BS = n;                                   // scratch: [f][e][a][b][c]
+  static constexpr int AS = TUNED ? 28 : TUNED7 ? 66 : n * n;
+  static constexpr int ES = TUNED ? 147 : TUNED7 ? 529 : n * n * n;
+  static constexpr int SP = TUNED ? 588 : TUNED7 ? 529 : pad16(NE * n * n * n);
   // isotropic metric (WF 2): [i][k][e][j] with an i-row stride padded where tuned
   // (the packing must agree for every kernel variant of the shape: keyed on n and the tile only)
   static constexpr int MIS = NE * n * n + ((n == 8 && TX == 1 && TY == 1) ? 1 : 0);

@@ -9,7 +9,13 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parent))
-from bank_search import wavefronts  # noqa: E402
+from bank_search import wavefronts as _wf_full  # noqa: E402
+
+
+def wavefronts(addrs):
+    """64-bit accesses are served per half-warp (ncu-confirmed on the N = 4 and N = 7 sweeps): the
+    wavefronts of a warp instruction are those of its two 16-lane halves."""
+    return _wf_full(addrs[:16]) + _wf_full(addrs[16:])
 
 n, N, F, H = 8, 7, 4, 4
 NR = n // H
