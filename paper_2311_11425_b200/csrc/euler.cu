@@ -173,7 +173,7 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
           const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
           const int ii = (m == 0) ? i : (m == 1) ? j : k;
           // D from shared memory: the lanes of a warp index it with different ii (LDC would serialise)
-          const double dw = sD[a * n + ii], ds = sD[ii * n + a];
+          const double dw = sD[a * n + ii], ds = sD[n * n + a * n + ii];   // D, D^T: lanes vary ii
           wk0 += dw * s[(m * 5 + 0) * nn + o];
           wk4 += dw * s[(m * 5 + 1) * nn + o];
 #pragma unroll
@@ -213,7 +213,7 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
         for (int a = 0; a < n; ++a) {
           const int o = (m == 0) ? (a * n + j) * n + k : (m == 1) ? (i * n + a) * n + k : (i * n + j) * n + a;
           const int ii = (m == 0) ? i : (m == 1) ? j : k;
-          const double dw = sD[a * n + ii], ds = sD[ii * n + a];
+          const double dw = sD[a * n + ii], ds = sD[n * n + a * n + ii];   // D, D^T: lanes vary ii
           wk0 += dw * s[m * nn + o];
 #pragma unroll
           for (int f = 0; f < 5; ++f) dd[f] += ds * s[(3 + f) * nn + o];
@@ -261,8 +261,11 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_elem_kernel(hv::D
   extern __shared__ double sm[];
   const int64_t e = blockIdx.x;
   const int t = threadIdx.x;
-  double* sD = sm + 15 * nn;                      // D (n x n), row-major
-  for (int x = t; x < n * n; x += blockDim.x) sD[x] = Dt.D[x / n][x % n];
+  double* sD = sm + 15 * nn;                      // D then D^T (n x n each)
+  for (int x = t; x < n * n; x += blockDim.x) {
+    sD[x] = Dt.D[x / n][x % n];
+    sD[n * n + x] = Dt.D[x % n][x / n];
+  }
   double acc[5];
   int g = 0;
   euler_node_acc<n>(Dt, K, nelem, e, t, gid, w3, Mt, q, ldq, sm, acc, g, elem_layer[e], nlay, sD);
@@ -291,10 +294,13 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::D
   extern __shared__ double sm[];
   double* s_carry = sm + 15 * nn;                 // [2][n*n][5]
   int* s_code = reinterpret_cast<int*>(s_carry + 2 * n * n * 5);   // [n*n]
-  double* sD = s_carry + 2 * n * n * 5 + (n * n + 1) / 2;           // D (n x n), row-major
+  double* sD = s_carry + 2 * n * n * 5 + (n * n + 1) / 2;           // D then D^T (n x n each)
   const int64_t tl = blockIdx.x;
   const int t = threadIdx.x;
-  for (int x = t; x < n * n; x += blockDim.x) sD[x] = Dt.D[x / n][x % n];
+  for (int x = t; x < n * n; x += blockDim.x) {
+    sD[x] = Dt.D[x / n][x % n];
+    sD[n * n + x] = Dt.D[x % n][x / n];
+  }
   const int i = t / (n * n), j = (t / n) % n, k = t % n;
   const int nlay = A.nlay;
   if (t < n * n) s_code[t] = A.code[tl * n * n + t];
@@ -340,7 +346,7 @@ int run_tile(const double* Drow, const EulerConsts& K, int64_t nelem, const int3
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;
-  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n * 5 + (n * n + 1) / 2 + n * n);
+  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n * 5 + (n * n + 1) / 2 + 2 * n * n);
   auto kern = euler_tile_kernel<n>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)A.ntiles, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
@@ -368,7 +374,7 @@ int run_elem(const double* Drow, const EulerConsts& K, int64_t nelem, const int3
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;
-  const size_t smem = sizeof(double) * (15 * nn + n * n);
+  const size_t smem = sizeof(double) * (15 * nn + 2 * n * n);
   auto kern = euler_elem_kernel<n>;
   if (smem > 48 * 1024) HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<(unsigned)nelem, ((nn + 31) / 32) * 32, smem, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, work, elem_layer, nlay);
