@@ -39,3 +39,16 @@ def test_abi_version():
 def test_sm100a_cubin_only():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_plane_metric_sizes():
+    """Doubles per tile-layer of the plane kernel's packed metric (host-only query): 6 / 3 / 1 components per
+    element node, N = 7 single-column isotropic rows padded to 65 for conflict-free reads; -1 on bad input."""
+    L = _lib.lib()
+    assert L.hv_plane_metric_doubles(4, 2, 2, 0) == 6 * 5 * 4 * 25
+    assert L.hv_plane_metric_doubles(4, 2, 2, 1) == 3 * 5 * 4 * 25
+    assert L.hv_plane_metric_doubles(4, 2, 2, 2) == 5 * 4 * 25
+    assert L.hv_plane_metric_doubles(7, 1, 1, 2) == 8 * 65
+    assert L.hv_plane_metric_doubles(7, 2, 2, 2) == 8 * 4 * 64
+    assert L.hv_plane_metric_doubles(8, 1, 1, 2) == -1
+    assert L.hv_plane_metric_doubles(4, 2, 2, 3) == -1
