@@ -383,19 +383,21 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
           }
         }
       }
-      // eta lines of element e with i = jp (zeta levels K0 .. K0 + NK): dq_eta(e, jp, a', k)
+      // eta lines of element e: H = 1: lines i = jp, all zeta levels; split planes: lines
+      // i = I0 .. I0 + NK at level k = jp (the lanes of a half-warp then vary i, as in the plane
+      // accesses, whose layout is bank-conflict-free): dq_eta(e, i, a', k)
 #pragma unroll
       for (int kk = 0; kk < NK; ++kk) {
-        const int k = K0 + kk;
+        const int li = (H == 1) ? jp : I0 + kk, k = (H == 1) ? K0 + kk : jp;
         double ql[n];
 #pragma unroll
-        for (int a = 0; a < n; ++a) ql[a] = s_q[tq(px * N + jp, py * N + a, k)];
+        for (int a = 0; a < n; ++a) ql[a] = s_q[tq(px * N + li, py * N + a, k)];
 #pragma unroll
         for (int a2 = 0; a2 < n; ++a2) {
           double s = 0.0;
 #pragma unroll
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], ql[a], s);
-          s_s[sidx(e, jp, a2, k)] = s;
+          s_s[sidx(e, li, a2, k)] = s;
         }
       }
     }
@@ -555,16 +557,16 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     if (run) {
 #pragma unroll
       for (int kk = 0; kk < NK; ++kk) {
-        const int k = K0 + kk;
+        const int li = (H == 1) ? jp : I0 + kk, k = (H == 1) ? K0 + kk : jp;   // the lines of step b
         double ql[n];
 #pragma unroll
-        for (int a = 0; a < n; ++a) ql[a] = s_s[sidx(e, jp, a, k)];
+        for (int a = 0; a < n; ++a) ql[a] = s_s[sidx(e, li, a, k)];
 #pragma unroll
         for (int a2 = 0; a2 < n; ++a2) {
           double s = 0.0;
 #pragma unroll
           for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], ql[a], s);
-          s_s[sidx(e, jp, a2, k)] = s;
+          s_s[sidx(e, li, a2, k)] = s;
         }
       }
     }
