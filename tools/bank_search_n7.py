@@ -1,7 +1,7 @@
 """Shared-memory bank search for the N = 7 split-plane sweep (1x1 tiles, H = 4, F = 4; dev helper).
 
-Thread order (jp, e, ih, f), f fastest; thread (jp, ih, f) owns xi rows 2 ih, 2 ih + 1 and eta-line zeta
-levels 2 ih, 2 ih + 1 of the single element.  Counts wavefronts per layer (bank model of tools/bank_search.py)
+Thread order (jp, e, ih, f), f fastest; thread (jp, ih, f) owns xi rows 2 ih, 2 ih + 1 of plane jp and the
+eta lines (i = 2 ih, 2 ih + 1; level jp) of the single element.  Counts wavefronts per layer (bank model of tools/bank_search.py)
 for candidate strides of s_q [f][u][v][k] (QP, US, KS), the scratch s_s [f][a][b][c] (SP, AS, BS) and the
 isotropic metric [i][k][j] (row stride MIS), and prints the best ones next to the plain padded layout.
 """
@@ -42,9 +42,9 @@ def cost_q(QP, KS, US):
         for r in range(NR):
             for k in range(n):
                 t += wavefronts([qa(f, ih * NR + r, jp, k) for jp, ih, f in lw])
-        for kk in range(NR):
+        for kk in range(NR):   # eta lines (i = 2 ih + kk, level jp)
             for a in range(n):
-                t += wavefronts([qa(f, jp, a, ih * NR + kk) for jp, ih, f in lw])
+                t += wavefronts([qa(f, ih * NR + kk, a, jp) for jp, ih, f in lw])
     for warp in range(NT // 32):   # gather (node-granular, all F fields per node)
         for it in range((U * V * n) // NT):
             nodes = [warp * 32 + ln + it * NT for ln in range(32)]
@@ -57,9 +57,9 @@ def cost_s(SP, AS, BS):
     sa = lambda f, a, b, c: f * SP + a * AS + b * BS + c
     t = 0
     for lw in lanes():
-        for kk in range(NR):
+        for kk in range(NR):   # eta lines (i = 2 ih + kk, level jp)
             for a2 in range(n):
-                t += 3 * wavefronts([sa(f, jp, a2, ih * NR + kk) for jp, ih, f in lw])
+                t += 3 * wavefronts([sa(f, ih * NR + kk, a2, jp) for jp, ih, f in lw])
         for r in range(NR):
             for k in range(n):
                 t += 4 * wavefronts([sa(f, ih * NR + r, jp, k) for jp, ih, f in lw])
