@@ -199,7 +199,9 @@ def laplacian_apply_fields(q, viscous, ops, fields):
     torch = torch_mod()
     qd, host = _as_device(q)
     plan = ops.lap_plan(viscous)
-    out = torch.zeros_like(qd)
+    # every column written by the pass: no need to zero the output first
+    full = qd.dim() == 2 and sorted(fields) == list(range(qd.shape[1]))
+    out = torch.empty_like(qd) if full else torch.zeros_like(qd)
     fl = (C.c_int32 * len(fields))(*fields)
     _lib.check(_lib.lib().hv_laplacian(C.byref(plan), qd.data_ptr(), qd.shape[1], len(fields), fl, out.data_ptr(),
                                        qd.shape[1], fl, 1.0, _lib.stream_handle()))
