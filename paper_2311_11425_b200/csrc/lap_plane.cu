@@ -113,6 +113,8 @@ struct PlaneCfg {
   static constexpr int SQ = QP * F;
   static constexpr int SE = SP * F;
   static constexpr int WL = WF == 2 ? n * MIS : (WF == 1 ? 3 : 6) * n * NE * n * n;   // packed metric doubles per tile-layer
+  // the bulk copy of a tile-layer's metric moves a multiple of 16 bytes (else its mbarrier never completes)
+  static_assert(WV != 0 || WL % 2 == 0, "packed metric per tile-layer must be a multiple of 16 bytes");
   static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
   static constexpr int FI = UV * N;                      // output items per layer (k < N)
   static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
