@@ -31,9 +31,11 @@ def lanes():
             if tid >= NT:
                 out.append(None)
             else:
+                # the kernel's thread order (jp, e, f), f fastest (lap_plane.cu); the tuned layout
+                # (QP, US) = (415, 46), (SP, ES, AS) = (588, 147, 28) is optimal under it
                 f = tid % F
-                jp = (tid // F) % n
-                e = tid // (F * n)
+                e = (tid // F) % NE
+                jp = tid // (F * NE)
                 out.append((e, jp, f))
         yield out
 
@@ -66,26 +68,7 @@ def layout_ok(L):
     return KS >= n and US >= V * KS and QP >= U * US and BS >= n and AS >= n * BS and ES >= n * AS and SP >= NE * ES
 
 
-cur = (420, 5, 45, 500, 125, 25, 5)
-c = cost(cur)
-print("current", dict(c), sum(c.values()))
-best = []
-for KS in (5, 6, 7):
-    for usp in range(0, 8):
-        US = V * KS + usp
-        base_q = U * US
-        for qpad in range(0, 16):
-            QP = base_q + qpad
-            for BS in (5, 6, 7):
-                for asp in range(0, 4):
-                    AS = n * BS + asp
-                    for esp in range(0, 8):
-                        ES = n * AS + esp
-                        for spp in range(0, 16):
-                            SP = NE * ES + spp
-                            L = (QP, KS, US, SP, ES, AS, BS)
-                            best.append(L)
-print(len(best), "candidates")
+
 
 
 def wf_half(addrs, width=1):
@@ -156,7 +139,33 @@ def cost_s(SP, ES, AS, BS, wf=wavefronts):
     return t
 
 
+def _enumerate_layouts():
+    """The candidate layouts of the original search (dev record)."""
+    cur = (420, 5, 45, 500, 125, 25, 5)
+    c = cost(cur)
+    print("current", dict(c), sum(c.values()))
+    best = []
+    for KS in (5, 6, 7):
+        for usp in range(0, 8):
+            US = V * KS + usp
+            base_q = U * US
+            for qpad in range(0, 16):
+                QP = base_q + qpad
+                for BS in (5, 6, 7):
+                    for asp in range(0, 4):
+                        AS = n * BS + asp
+                        for esp in range(0, 8):
+                            ES = n * AS + esp
+                            for spp in range(0, 16):
+                                SP = NE * ES + spp
+                                L = (QP, KS, US, SP, ES, AS, BS)
+                                best.append(L)
+    print(len(best), "candidates")
+    return best
+
+
 if __name__ == "__main__":
+    _enumerate_layouts()
     import sys
     for name, wf in (("full", wavefronts), ("half", wf_half)):
         cq = cost_q(420, 5, 45, wf); cs = cost_s(500, 125, 25, 5, wf)
