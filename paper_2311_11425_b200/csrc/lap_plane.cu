@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     qcol[p] = A.qf.f[p];
     ocol[p] = A.of.f[p];
   }
-  const bool row5 = (F == 4 && A.ldo == 5 && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
+  const bool row5 = (F == 4 && A.ldo == 5 && A.zero_mask == 1u && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
   auto sidx = [&](int ee, int a, int b, int c) { return f * C::SP + ee * C::ES + a * C::AS + b * C::BS + c; };
   auto tq = [&](int u, int v, int k) { return f * C::QP + u * C::US + v * C::KS + k; };
   // tile node (uv * n + k) -> s_q offset within a field plane
@@ -684,7 +684,7 @@ inline int output_mode(const TileArgs& A, int F) {
   const bool f0 = A.of.f[0] == 0 && A.of.f[1] == 1 && A.of.f[2] == 2 && A.of.f[3] == 3;
   const bool f1 = A.of.f[0] == 1 && A.of.f[1] == 2 && A.of.f[2] == 3 && A.of.f[3] == 4;
   if (A.ldo == 4 && !A.zero_mask && f0) return 1;
-  if (A.ldo == 5 && f1) return 2;
+  if (A.ldo == 5 && A.zero_mask == 1u && f1) return 2;   // the OM 2 rows zero column 0
   return 0;
 }
 

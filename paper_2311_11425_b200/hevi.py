@@ -60,11 +60,13 @@ class LheviState:
         if ref is None:
             raise StageSolveError("LHEVI-RS needs a reference state")
         band = vop.column_jacobian(ref, lam)
+        # factor the fresh band first: on SingularMatrixError the cached factorisation, ipiv and lam stay
+        # intact (the reference assigns its cache only after a successful factorisation, hevi.py:254-262)
+        ipiv, _ = linalg.banded_lu_factor_batch(band, vop.kl, vop.ku)
         if self.band is not None and tuple(self.band.shape) == tuple(band.shape):
             self.band.copy_(band)          # in place: captured graphs keep pointing at it
         else:
             self.band = band
-        ipiv, _ = linalg.banded_lu_factor_batch(self.band, vop.kl, vop.ku)
         if self.ipiv is not None and tuple(self.ipiv.shape) == tuple(ipiv.shape):
             self.ipiv.copy_(ipiv)
         else:

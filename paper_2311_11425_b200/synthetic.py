@@ -4,9 +4,12 @@ No public benchmark suite is involved: BASELINE.json names only synthetic
 meshes and states, so these generators stand in for them.
 All arrays are generated on the HOST with ``numpy.random.default_rng(seed)``
 (PCG64) and copied to the device, so the CUDA path and the CPU oracle see
-bitwise-identical inputs.  Elementwise arithmetic only (no reductions whose
-order could vary between numpy builds), so the generated bits are
-reproducible on any host running this image.
+bitwise-identical inputs within one process.  The smooth states go through
+numpy's transcendental functions and a BLAS contraction (``T @ A``), whose
+last-ulp rounding can depend on the host CPU's SIMD level; the parity
+fixtures therefore store the exact input bytes (tests/golden/*.npz
+``state``, checked against this generator in the build container by
+tests/test_oracle_golden.py) and the GPU-side tests read those.
 
 Interpretation choices for the config text (recorded, not guessed silently;
 DESIGN.md §7 repeats them):

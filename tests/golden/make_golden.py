@@ -68,6 +68,8 @@ def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, l
     mets = rmet.project_metrics_to_columns(mets0, m)
     consts = rstate.PhysConstants(omega=omega)
     out["ng"] = np.array(m.nglobal)
+    out["state"] = state                       # the exact input bytes (tests use these on any host)
+    out["sha_state"] = np.array(sha(state))
     out["sha_gid"] = np.array(sha(m.gid))
     out["sha_xg"] = np.array(sha(m.xg))
     out["sha_col_gid"] = np.array(sha(m.col_gid))
@@ -142,7 +144,8 @@ def lhevi_fixture():
     hd = rhd.HyperDiffConfig(**LHEVI["hd"])
     vm = rhd.build_viscous_metric(m, mets, hd, dt=LHEVI["dt"])
     ops = reuler.EulerOps(m, mets, rstate.PhysConstants(omega=0.0), "2C", hyper=(hd, vm))
-    q0 = lhevi_state(m.xg)
+    q0 = lhevi_state(m.xg, stored=False)
+    out["q0"] = q0
     for name in LHEVI["tabs"]:
         ls = rhevi.LheviState(update_interval=LHEVI["update_interval"], mode="PS")
         q = q0.copy()
@@ -183,7 +186,28 @@ def diag_fixture():
     print("diag", "bytes", (HERE / "diag.npz").stat().st_size)
 
 
+def add_states():
+    """Add the regenerated input states to existing fixtures without re-running the reference
+    (``--states-only``; tests/test_oracle_golden.py proves they are the bytes the fixtures were
+    made from: the oracle reproduces every stored output bit for bit from them)."""
+    for name, c in CASES.items():
+        f = HERE / f"{name}.npz"
+        z = dict(np.load(f))
+        coords_mesh = ref_mesh(c)
+        st = make_state(c, coords_mesh.xg)
+        z["state"], z["sha_state"] = st, np.array(sha(st))
+        np.savez_compressed(f, **z)
+        print(name, "state", st.shape, f.stat().st_size)
+    f = HERE / "lhevi.npz"
+    z = dict(np.load(f))
+    z["q0"] = lhevi_state(ref_mesh(CASES[LHEVI["case"]]).xg, stored=False)
+    np.savez_compressed(f, **z)
+
+
 def main():
+    if "--states-only" in sys.argv:
+        add_states()
+        return
     diag_fixture()
     lhevi_fixture()
     for name, c in CASES.items():

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from cases import CASES, make_state
+from cases import CASES, case_state
 from oracle import hevi_oracle as O
 from paper_2311_11425_b200 import synthetic
 
@@ -40,7 +40,7 @@ class OracleProblem:
         self.alpha = alpha
         self.Gnu, self.lam, self.evecs = O.viscous_metric(m, self.grad, alpha, dt=c["dt"], **hd)
         self.Jg_e = O.gather(m.gid, self.Jg)
-        self.state = make_state(c, m.xg)
+        self.state = case_state(name, m.xg, None if case is None else c)
 
     def hyper(self, data=None):
         return O.hyperdiffusion(self.m, self.Gnu, self.Jg_e, self.Minv,

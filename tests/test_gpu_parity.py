@@ -477,3 +477,30 @@ def test_misaligned_output_view():
     hyperdiff.hyperdiffusion_apply(state.StateField("2C", q), p.cfg, p.vm, p.ops, out=out)
     assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) <= 1e-14
     assert rel_l2(out.cpu().numpy(), o.hyper()) <= TOL
+
+
+@pytest.mark.parametrize("case", ["box_p_n4", "box_n7"])
+def test_laplacian_leaves_unlisted_columns(case):
+    """hv_laplacian writes only the listed output columns: with ldo = 5, fields 1..4 and no zero
+    mask, column 0 of the output keeps the caller's values on every node (the 16-byte (ng, 5) row
+    stores of the sweeps zero column 0 only for H_nu's zero mask)."""
+    import ctypes as C
+
+    import torch
+
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import _lib, hyperdiff
+
+    p = ProductProblem(case)
+    o = OracleProblem(case)
+    q = torch.from_numpy(o.state).cuda()
+    out = torch.full_like(q, 7.0)
+    fl = (C.c_int32 * 4)(1, 2, 3, 4)
+    plan = p.ops.lap_plan(p.vm)
+    _lib.check(_lib.lib().hv_laplacian(C.byref(plan), q.data_ptr(), 5, 4, fl, out.data_ptr(), 5, fl, 1.0,
+                                       _lib.stream_handle()))
+    got = out.cpu().numpy()
+    assert np.all(got[:, 0] == 7.0)
+    ref = hyperdiff.laplacian_apply_fields(q, p.vm, p.ops, (1, 2, 3, 4)).cpu().numpy()
+    assert np.array_equal(got[:, 1:], ref[:, 1:])

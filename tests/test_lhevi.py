@@ -91,3 +91,34 @@ def test_step_lhevi_numpy_io(lhevi_ops):
     q1 = step_lhevi(ops, Tab(z, "ARK2"), lhevi_state(p.m.xg), LHEVI["dt"], LheviState())
     assert isinstance(q1, np.ndarray)
     assert rel_l2(q1, z["step_ARK2_0"]) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_failed_rebuild_keeps_cache(lhevi_ops):
+    """A rebuild whose factorisation fails leaves the cached band, pivots, lam and age intact
+    (the reference assigns its cache only after a successful factorisation, hevi.py:254-262)."""
+    import torch
+
+    from paper_2311_11425_b200.hevi import LheviState
+    from paper_2311_11425_b200.linalg import SingularMatrixError
+
+    p, ops = lhevi_ops
+    vop = ops
+    q = torch.from_numpy(lhevi_state(p.m.xg)).cuda()
+    qcol = q[torch.from_numpy(np.ascontiguousarray(p.m.col_gid, dtype=np.int64)).cuda()]
+    ls = LheviState(update_interval=5)
+    ls.rebuild(vop, qcol, 0.05)
+    band0, ipiv0 = ls.band.clone(), ls.ipiv.clone()
+    ls.age = 3
+
+    class Zero:
+        kl, ku, ncol = vop.kl, vop.ku, vop.ncol
+
+        def column_jacobian(self, ref, lam):
+            return torch.zeros_like(vop.column_jacobian(ref, lam))
+
+    with pytest.raises(SingularMatrixError):
+        ls.rebuild(Zero(), qcol, 0.07)
+    assert torch.equal(ls.band, band0) and torch.equal(ls.ipiv, ipiv0)
+    assert ls.lam == 0.05 and ls.age == 3
+    assert not ls.needs_rebuild(0.05)
