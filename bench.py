@@ -191,26 +191,20 @@ def time_secondary(name, steps=5, warmup=3):
     return res
 
 
-def _cpu_problem(name):
-    """The oracle problem of the CPU sample: a 16x16 column block (all layers, same element size,
-    generator and state) of the workload's per-GPU mesh."""
+def _cpu_problem(name, sx=16, sy=16):
+    """The oracle problem of the CPU sample: an sx x sy column block (all layers, the same element
+    size, geometry generator and state generator) of the workload's per-GPU mesh, set up with the
+    ORACLE alone (KD-tree numbering, metrics, G_nu, mass: oracle/hevi_oracle.py restating
+    mesh.py:86-145, metrics.py:79-142, hyperdiff.py:54-81, assembly.py:54-64); no product code or
+    library is loaded on this path.  Returns (run, ng, description)."""
     from oracle import hevi_oracle as O
-    from paper_2311_11425_b200 import synthetic
+    from paper_2311_11425_b200 import synthetic   # input generators only (pure numpy)
 
     w = synthetic.workload(name)
-    sx, sy = min(16, w.nx or w.ne), min(16, w.ny or w.ne)
+    sx, sy = min(sx, w.nx or w.ne), min(sy, w.ny or w.ne)
     ext = (w.extents[0] * sx / w.nx, w.extents[1] * sy / w.ny, w.extents[2])
     coords, layer, hcol = synthetic.perturbed_box_coords(sx, sy, w.nv, w.N, ext, perturb=w.perturb)
-    tol = O.dedupe_tol("box", max(sx, sy), extents=ext)
-    # numbering through the (bit-exact, tested) host C++ builder keeps the sample setup short
-    from paper_2311_11425_b200 import basis, mesh as hm
-
-    b = basis.lobatto(w.N)
-    pm = hm.Mesh(hm.MeshConfig("box", panels_per_edge=max(sx, sy), n_elem_vertical=w.nv, degree=w.N,
-                               box_extents=ext), coords, (b, b, b), layer, hcol)
-    x, wq, D = O.lgl(w.N)
-    om = O.OracleMesh("box", w.N, coords, layer, hcol, pm.gid, pm.nglobal, pm.xg, pm.col_gid, pm.flux_mask,
-                      D=D, w=wq)
+    om = O.OracleMesh.from_coords("box", w.N, coords, layer, hcol, O.dedupe_tol("box", max(sx, sy), extents=ext))
     _, J, grad = O.curl_metrics(om)
     Jg, _ = O.project_columns(om, J, grad)
     _, Minv = O.lumped_mass(om, J)
@@ -218,93 +212,105 @@ def _cpu_problem(name):
     Jg_e = O.gather(om.gid, Jg)
     q = synthetic.fourier_state(om.xg, ext)
     run = lambda: O.hyperdiffusion(om, Gnu, Jg_e, Minv, q, w.alpha)  # noqa: E731
-    return run, om.ng, f"{sx}x{sy}x{w.nv} element block of {name} (N={w.N}, ng={om.ng})"
+    return run, om.ng, f"{sx}x{sy}x{w.nv} element column block of {name} (N={w.N}, ng={om.ng})"
 
 
-def _cpu_worker(name, seconds, barrier, out):
+def _cpu_worker(name, warmup, steps, barrier, out):
     os.environ["OMP_NUM_THREADS"] = os.environ["OPENBLAS_NUM_THREADS"] = "1"
     sys.path.insert(0, str(ROOT))
     run, ng, desc = _cpu_problem(name)
-    run()                                  # warm-up
-    barrier.wait()
-    t0 = time.perf_counter()
-    k = 0
-    while True:
+    for _ in range(warmup):
         run()
-        k += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    out.put((4 * ng * k / (time.perf_counter() - t0), k, ng, desc))
+    barrier.wait()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    out.put((times, ng, desc))
 
 
-def cpu_sample(name, seconds=8.0, procs=None):
-    """Reference algorithm's CPU port (oracle, numpy) on a bounded sample of the workload.
+def cpu_sample(name, warmup=1, steps=3, procs=None):
+    """The reference algorithm (oracle port, numpy) on a bounded sample of the workload.
 
-    The reference is serial (numpy einsum / add.at); to use every host core, `procs`
-    worker processes each run the same sample concurrently (independent problems,
-    like an ensemble) and their throughputs add.  Returns (DOF-updates/s, description,
-    ops per worker, ng, cores).
-    """
+    The reference is serial (numpy einsum / add.at, GIL-bound); to use every host core, ``procs``
+    worker processes each run one copy of the sample concurrently (independent problems, like an
+    ensemble).  A step = one H_nu op on the sample in every worker; the step time is the slowest
+    worker's.  Returns dict(value DOF-updates/s, ms_per_step, step_times, ng, cores, sample)."""
     import multiprocessing as mp
 
     procs = procs or max(1, len(os.sched_getaffinity(0)))
     ctx = mp.get_context("spawn")
     barrier = ctx.Barrier(procs)
     out = ctx.Queue()
-    ps = [ctx.Process(target=_cpu_worker, args=(name, seconds, barrier, out)) for _ in range(procs)]
+    ps = [ctx.Process(target=_cpu_worker, args=(name, warmup, steps, barrier, out)) for _ in range(procs)]
     for p in ps:
         p.start()
-    res = [out.get(timeout=600) for _ in ps]
+    res = [out.get(timeout=1800) for _ in ps]
     for p in ps:
         p.join(timeout=60)
-    rate = sum(r[0] for r in res)
-    ng, desc = res[0][2], res[0][3]
-    kmin = min(r[1] for r in res)
-    desc = (f"{desc}, oracle port (numpy), {procs} concurrent single-thread worker processes, "
-            f">= {kmin} ops each over {seconds:.0f} s")
-    return rate, desc, kmin, ng, procs
+    ng, desc = res[0][1], res[0][2]
+    step_s = [max(r[0][k] for r in res) for k in range(steps)]      # slowest worker per step
+    total = sum(step_s)
+    value = 4 * ng * procs * steps / total
+    desc = (f"{desc}: one H_nu op per step in each of {procs} concurrent single-thread worker processes "
+            f"(oracle port of the reference, numpy); {warmup} warm-up + {steps} timed ops; setup untimed")
+    return dict(value=value, ms_per_step=1e3 * total / steps, step_times=step_s, ng=ng, cores=procs, sample=desc)
 
 
 # ---------------------------------------------------------------------- arms
-def bench_config(w, world, **extra):
-    """The `config` object of both arms (same workload description)."""
-    cfg = {"workload": f"{w.name}: H_nu alpha=2, {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, "
-                       f"perturbed box, c={w.c}, dt={w.dt}",
-           "fields": 4, "l2": "inputs (11.7 GB/op) exceed L2; no flush",
-           "parallelism": (f"x-slabs x{world} of a ({w.nx}*{world})x{w.ny}x{w.nv} box, slab-face "
-                           "DSS over NCCL p2p" if world > 1 else "single GPU")}
-    cfg.update(extra)
-    return cfg
+def bench_config(w, world):
+    """The `config` object of both arms (identical: the same workload; sample sizes and per-GPU
+    node counts live outside it)."""
+    return {"workload": f"{w.name}: H_nu alpha=2, {w.nx}x{w.ny}x{w.nv} elem/GPU, N={w.N}, "
+                        f"perturbed box, c={w.c}, dt={w.dt}",
+            "fields": 4, "l2": "inputs (11.7 GB/op) exceed L2; no flush",
+            "parallelism": (f"x-slabs x{world} of a ({w.nx}*{world})x{w.ny}x{w.nv} box, slab-face "
+                            "DSS over NCCL p2p" if world > 1 else "single GPU")}
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU algorithm on the host cores (oracle port; the reference package itself
+    does not exist on the GPU box).  Rank 0 only; a step = one H_nu op on a bounded column-block
+    sample of the workload in each worker process."""
     if rank != 0:
         return
     from paper_2311_11425_b200 import synthetic
 
     w = synthetic.workload(args.workload)
-    for _ in range(args.warmup):
-        pass
-    rate, desc, reps, ng, cores = cpu_sample(args.workload, seconds=max(5.0, min(30.0, 1.0 * args.steps)))
+    one = cpu_sample(args.workload, warmup=1, steps=2, procs=1)          # the single-core rate
+    r = cpu_sample(args.workload, warmup=max(1, args.warmup), steps=args.steps)
     line = {
         "impl": "reference",
         "metric": "fp64 DOF-updates/s of H_nu (alpha=2)",
-        "value": rate,
+        "value": r["value"],
         "unit": "DOF-updates/s",
         "n_gpus": args.gpus,
         "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": 4 * ng * cores / rate * 1e3,
+        "warmup": max(1, args.warmup),
+        "ms_per_step": r["ms_per_step"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (seeded, host-generated)",
-        "config": bench_config(w, world, sample=desc),
-        "cpu_baseline": {"value": rate, "unit": "DOF-updates/s", "cores": cores, "kind": "port", "sample": desc},
-        "e2e": {"value": rate, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic (seeded, host-generated geometry; Fourier state)",
+        "config": bench_config(w, world),
+        "cpu_baseline": {"value": r["value"], "unit": "DOF-updates/s", "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"], "value_1core": one["value"],
+                         "host_cpu": _host_cpu()},
+        "e2e": {"value": r["value"], "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _host_cpu():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_ours(args, rank, world, local):
@@ -333,7 +339,10 @@ def run_ours(args, rank, world, local):
         transport = parallel.DistTransport(rank, world)
         sop = parallel.setup_distributed(layout, cfg, w.dt, transport)
         m, vm, ops = sop.mesh, sop.vm, sop.ops
-        q_host = synthetic.fourier_state(m.xg, layout.extents, device=torch.device("cuda"))
+        # white noise keyed on the global lattice node, so the slab-face nodes two ranks share hold
+        # the same state on both (the smooth part depends on the bitwise-shared coordinates only)
+        q_host = synthetic.fourier_state(m.xg, layout.extents, device=torch.device("cuda"),
+                                         noise_keys=layout.lattice_keys(m))
         P = dict(w=w, m=m, q=q_host, t_mesh=time.time() - t0)
 
         def hyperdiffusion_apply(st_, cfg_, vm_, ops_, out=None):
@@ -479,8 +488,9 @@ def run_ours(args, rank, world, local):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
-            rate, desc, reps, _, cores = cpu_sample(args.workload, seconds=10.0)
-            cpu = {"value": rate, "unit": "DOF-updates/s", "cores": cores, "kind": "port", "sample": desc}
+            r = cpu_sample(args.workload, warmup=1, steps=4)
+            cpu = {"value": r["value"], "unit": "DOF-updates/s", "cores": r["cores"], "kind": "port",
+                   "sample": r["sample"], "host_cpu": _host_cpu()}
         line = {
             "metric": "fp64 DOF-updates/s of H_nu (alpha=2)",
             "value": value,
@@ -494,7 +504,8 @@ def run_ours(args, rank, world, local):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded, host-generated geometry; Fourier state)",
-            "config": bench_config(w, world, nglobal_per_gpu=ng, nelem_per_gpu=m.nelem),
+            "config": bench_config(w, world),
+            "workload_size": {"nglobal_per_gpu": ng, "nelem_per_gpu": m.nelem},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": kern_name, "kernel_ms_per_launch": kern_ms,

@@ -252,3 +252,15 @@ def build_box_lattice(nx, ny, nv, N, extents, perturb=True, frac=0.1, seed=0):
                      box_extents=tuple(float(e) for e in extents))
     b = lobatto(N)
     return Mesh(cfg, coords, (b, b, b), layer, hcol, hgrid=(1, nx, ny))
+
+
+def build_box_window(ne, nv_full, N, extents, ia0, nx, ib0, ny, nv):
+    """A window of ``build_box``'s elements at their own coordinates (synthetic.box_window_coords):
+    parity cases at a large configuration's element geometry (config 4)."""
+    from .synthetic import box_window_coords
+
+    coords, layer, hcol = box_window_coords(ne, nv_full, N, extents, ia0, nx, ib0, ny, nv)
+    cfg = MeshConfig("box", panels_per_edge=max(nx, ny), n_elem_vertical=nv, degree=N,
+                     box_extents=tuple(float(e) for e in extents))
+    b = lobatto(N)
+    return Mesh(cfg, coords, (b, b, b), layer, hcol, hgrid=(1, nx, ny))

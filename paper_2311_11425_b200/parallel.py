@@ -80,6 +80,28 @@ class SlabLayout:
         return {int(c): side * self.face + jf for side, cols in self.face_columns(mesh).items()
                 for jf, c in enumerate(cols)}
 
+    def lattice_keys(self, mesh):
+        """Global vertex-lattice index of every local node, (I * (ny N + 1) + J) * (nv N + 1) + K with
+        I = ia_global N + i, J = ib N + j, K = l N + k: the same key on every rank that holds the node
+        (state generation keyed on it, synthetic.fourier_state(noise_keys=...))."""
+        N, ny, nv = self.N, self.ny, self.nv
+        n = N + 1
+        keys = np.empty(mesh.nglobal, dtype=np.int64)
+        ii, jj, kk = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+        ii, jj, kk = ii.reshape(-1), jj.reshape(-1), kk.reshape(-1)
+        nyl, nzl = ny * N + 1, nv * N + 1
+        step = 1 << 16
+        for e0 in range(0, mesh.nelem, step):
+            e = np.arange(e0, min(mesh.nelem, e0 + step))
+            ia = e // (ny * nv) + self.rank * self.nx_per
+            ib = (e // nv) % ny
+            l = e % nv
+            I = ia[:, None] * N + ii[None, :]
+            J = ib[:, None] * N + jj[None, :]
+            K = l[:, None] * N + kk[None, :]
+            keys[mesh.gid[e0:e0 + len(e)].reshape(len(e), -1)] = (I * nyl + J) * nzl + K
+        return keys
+
     def local_to_global(self, mesh, global_mesh):
         """Global gid of every local node (tests / gathering results)."""
         N3 = mesh.gid.shape[1:]

@@ -94,6 +94,37 @@ def perturbed_box_coords(nx, ny, nv, N, extents, frac=0.1, seed=GEOM_SEED, pertu
     return coords, layer, hcol
 
 
+def box_window_coords(ne, nv_full, N, extents, ia0, nx, ib0, ny, nv):
+    """Elements [ia0, ia0+nx) x [ib0, ib0+ny) x layers [0, nv) of the ne x ne x nv_full box of
+    ``build_box`` (mesh.py:231-258), with the same node coordinates bit for bit (the same
+    linspace breakpoints and node formula), numbered locally e = (ia*ny + ib)*nv + l.
+
+    Parity cases at a large config's own element geometry (config 4: 156.25 x 156.25 x 625 m
+    elements) without the full mesh.  Returns coords (nelem,3,n,n,n), elem_layer, elem_hcol.
+    """
+    x1 = lobatto(N).nodes
+    Lx, Ly, Lz = extents
+    xs = np.linspace(0.0, Lx, ne + 1)
+    ys = np.linspace(0.0, Ly, ne + 1)
+    lev = np.linspace(0.0, 1.0, nv_full + 1) * Lz
+    n = N + 1
+    coords = np.empty((nx * ny * nv, 3, n, n, n))
+    e = 0
+    for a in range(nx):
+        ia = ia0 + a
+        x = 0.5 * (xs[ia] + xs[ia + 1]) + 0.5 * (xs[ia + 1] - xs[ia]) * x1
+        for b in range(ny):
+            ib = ib0 + b
+            y = 0.5 * (ys[ib] + ys[ib + 1]) + 0.5 * (ys[ib + 1] - ys[ib]) * x1
+            for l in range(nv):
+                z = 0.5 * (lev[l] + lev[l + 1]) + 0.5 * (lev[l + 1] - lev[l]) * x1
+                X, Y, Z = np.meshgrid(x, y, z, indexing="ij")
+                coords[e] = np.stack([X, Y, Z])
+                e += 1
+    idx = np.arange(nx * ny * nv)
+    return coords, (idx % nv).astype(np.int64), (idx // nv).astype(np.int64)
+
+
 # ------------------------------------------------------------------- states
 def _eval_modes(axes_fn, A, npts, nk, nfields, chunk, device):
     """out[p, f] = sum_k c0[p, kx] * (T[p, (rest)] @ A)[kx, f] chunk by chunk.
@@ -123,8 +154,32 @@ def _eval_modes(axes_fn, A, npts, nk, nfields, chunk, device):
     return out.cpu().numpy()
 
 
-def fourier_state(xg, extents, kmax=8, noise=1e-3, seed=STATE_SEED, nfields=5, chunk=1 << 16, device=None):
-    """Random Fourier modes (|k|^-2 amplitudes) plus white noise, (ng, nfields)."""
+def keyed_normal(keys, nfields, seed=STATE_SEED, block_bits=20):
+    """N(0,1) samples indexed by integer node keys instead of by local node order: key k takes row
+    k mod 2^b of the block rng(seed, k >> b).  Ranks that share a node (slab faces) draw the same
+    value for it without generating the whole global array."""
+    keys = np.asarray(keys, dtype=np.int64)
+    out = np.empty((keys.shape[0], nfields))
+    blk = keys >> block_bits
+    order = np.argsort(blk, kind="stable")
+    bs = blk[order]
+    cuts = np.flatnonzero(np.diff(bs)) + 1
+    for part in np.split(order, cuts):
+        if part.size == 0:
+            continue
+        b = int(blk[part[0]])
+        draw = np.random.default_rng([seed, b]).standard_normal((1 << block_bits, nfields))
+        out[part] = draw[keys[part] & ((1 << block_bits) - 1)]
+    return out
+
+
+def fourier_state(xg, extents, kmax=8, noise=1e-3, seed=STATE_SEED, nfields=5, chunk=1 << 16, device=None,
+                  noise_keys=None):
+    """Random Fourier modes (|k|^-2 amplitudes) plus white noise, (ng, nfields).
+
+    ``noise_keys`` (ng,) int64: draw the white noise per global node key (keyed_normal) instead of
+    in local node order -- multi-GPU slabs, whose shared face nodes must hold the same state on both
+    ranks (the smooth part is a function of the coordinates, which agree bitwise on the faces)."""
     rng = np.random.default_rng(seed)
     nk = kmax + 1
     amp = rng.standard_normal((nfields, nk, nk, nk))
@@ -133,7 +188,8 @@ def fourier_state(xg, extents, kmax=8, noise=1e-3, seed=STATE_SEED, nfields=5, c
     k2[0, 0, 0] = np.inf
     amp = amp / k2[None]
     phase = rng.uniform(0.0, 2.0 * np.pi, size=(3, nk))
-    white = rng.standard_normal((xg.shape[0], nfields))
+    white = rng.standard_normal((xg.shape[0], nfields)) if noise_keys is None else keyed_normal(
+        noise_keys, nfields, seed)
     A = np.ascontiguousarray(amp.transpose(2, 3, 1, 0).reshape(nk * nk, nk * nfields))   # [(ky,kz),(kx,f)]
     if device is not None:
         import torch

@@ -64,7 +64,18 @@ CASES = {
     "sphere_n7": dict(kind="sphere", ne=1, nv=2, N=7, radius=6.371e6, z_top=1.0e4,
                       hd=dict(alpha=2, c=(0.1, 0.1, 0.01)), dt=300.0, state="sphere",
                       sets=("2C", "3C"), omega=7.292e-5, lap_fields=None),
+    # config 4 at its OWN element geometry (156.25 x 156.25 x 625 m elements, N = 7, the c4 bubble,
+    # c = 0.02, dt = 0.1): a 4 x 4 x 4 window of the 64 x 64 x 16 box around the bubble centre
+    # (5, 5, 2) km, bottom at z = 0; the target quantity is S(q) + H_nu(q) on the bubble state
+    "c4_win": dict(kind="window", ne=64, nv_full=16, N=7, extents=(1.0e4, 1.0e4, 1.0e4),
+                   ia0=30, nx=4, ib0=30, ny=4, nv=4,
+                   hd=dict(alpha=2, c=(0.02, 0.02, 0.02)), dt=0.1, state="bubble",
+                   sets=("2C",), omega=0.0, lap_fields=None, c4_target=True),
 }
+
+
+def window_args(c):
+    return (c["ne"], c["nv_full"], c["N"], c["extents"], c["ia0"], c["nx"], c["ib0"], c["ny"], c["nv"])
 
 
 def make_state(case, xg):

@@ -42,7 +42,7 @@ from hevicore import state as rstate  # noqa: E402
 from paper_2311_11425_b200 import synthetic  # noqa: E402
 
 sys.path.insert(0, str(HERE.parent))
-from cases import CASES, LHEVI, diag_state, lhevi_state, make_state, random_state  # noqa: E402
+from cases import CASES, LHEVI, window_args, diag_state, lhevi_state, make_state, random_state  # noqa: E402
 
 
 def sha(a):
@@ -61,7 +61,8 @@ JAC_COLS = 24
 JAC_LAM = 0.37
 
 
-def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, lap_fields=None, jac=False):
+def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, lap_fields=None, jac=False,
+         c4_target=False):
     """Reference outputs for one mesh; inputs are regenerated from the seeds by the tests."""
     out = {}
     mets0 = rmet.curl_invariant_metrics(m)
@@ -90,6 +91,11 @@ def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, l
     if lap_fields is not None:
         out["lap"] = np.stack([rhd.laplacian_apply(state[:, f], vm, ops) for f in lap_fields], axis=1)
     out["hyper"] = rhd.hyperdiffusion_apply(st, hd_cfg, vm, ops)
+    if c4_target:
+        # config 4's quantity on the case state itself: rhs_full + hyperdiffusion_apply
+        # (euler.py:111-118 + hyperdiff.py:97-106); near-hydrostatic, so S alone is ill-conditioned
+        out["c4_target"] = ops.rhs_full(st) + out["hyper"]
+        out["rhs_full_state"] = ops.rhs_full(st)
     for s in sets:
         o = reuler.EulerOps(m, mets, consts, s, hyper=(hd_cfg, vm))
         rs = random_state(m.nglobal, s, seed=7)
@@ -119,6 +125,12 @@ def case(name, m, hd_cfg, dt, state, sets=("2C",), omega=0.0, store_full=True, l
 
 
 def ref_mesh(c):
+    if c["kind"] == "window":
+        coords, layer, hcol = synthetic.box_window_coords(*window_args(c))
+        cfg = rmesh.MeshConfig("box", panels_per_edge=max(c["nx"], c["ny"]), n_elem_vertical=c["nv"],
+                               degree=c["N"], box_extents=tuple(float(e) for e in c["extents"]))
+        b = rbasis.lobatto(c["N"])
+        return rmesh.Mesh(cfg, coords, (b, b, b), layer, hcol)
     if c["kind"] == "lattice":
         return ref_mesh_lattice(c["nx"], c["ny"], c["nv"], c["N"], c["extents"], perturb=True)
     if c["kind"] == "sphere":
@@ -208,12 +220,22 @@ def main():
     if "--states-only" in sys.argv:
         add_states()
         return
+    only = [a for a in sys.argv[1:] if not a.startswith("-")]
+    if only:   # regenerate the named cases only
+        for name in only:
+            c = CASES[name]
+            m = ref_mesh(c)
+            case(name, m, rhd.HyperDiffConfig(**c["hd"]), c["dt"], make_state(c, m.xg), sets=c["sets"],
+                 omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"], jac=(name != "c1"),
+                 c4_target=c.get("c4_target", False))
+        return
     diag_fixture()
     lhevi_fixture()
     for name, c in CASES.items():
         m = ref_mesh(c)
         case(name, m, rhd.HyperDiffConfig(**c["hd"]), c["dt"], make_state(c, m.xg), sets=c["sets"],
-             omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"], jac=(name != "c1"))
+             omega=c["omega"], store_full=(name != "c1"), lap_fields=c["lap_fields"], jac=(name != "c1"),
+             c4_target=c.get("c4_target", False))
     # basis constants
     np.savez_compressed(HERE / "basis.npz", **{f"D{N}": rbasis.lobatto(N).diff_matrix for N in range(1, 9)},
                         **{f"w{N}": rbasis.lobatto(N).weights for N in range(1, 9)},

@@ -4,7 +4,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from cases import CASES, case_state
+from cases import CASES, case_state, window_args
 from oracle import hevi_oracle as O
 from paper_2311_11425_b200 import synthetic
 
@@ -13,6 +13,10 @@ def oracle_mesh(name, case=None):
     c = CASES[name] if case is None else case
     if c["kind"] == "lattice":
         coords, layer, hcol = synthetic.perturbed_box_coords(c["nx"], c["ny"], c["nv"], c["N"], c["extents"])
+        tol = O.dedupe_tol("box", max(c["nx"], c["ny"]), extents=c["extents"])
+        return O.OracleMesh.from_coords("box", c["N"], coords, layer, hcol, tol)
+    if c["kind"] == "window":
+        coords, layer, hcol = synthetic.box_window_coords(*window_args(c))
         tol = O.dedupe_tol("box", max(c["nx"], c["ny"]), extents=c["extents"])
         return O.OracleMesh.from_coords("box", c["N"], coords, layer, hcol, tol)
     if c["kind"] == "sphere":

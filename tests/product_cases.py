@@ -2,7 +2,7 @@
 
 from __future__ import annotations
 
-from cases import CASES
+from cases import CASES, window_args
 from paper_2311_11425_b200 import euler, hyperdiff, mesh as hm, metrics, state
 
 
@@ -10,6 +10,8 @@ def product_mesh(name, case=None):
     c = CASES[name] if case is None else case
     if c["kind"] == "lattice":
         return hm.build_box_lattice(c["nx"], c["ny"], c["nv"], c["N"], c["extents"])
+    if c["kind"] == "window":
+        return hm.build_box_window(*window_args(c))
     if c["kind"] == "sphere":
         return hm.build_cubed_sphere(hm.MeshConfig("sphere", panels_per_edge=c["ne"], n_elem_vertical=c["nv"],
                                                    degree=c["N"], radius=c["radius"], z_top=c["z_top"]))

@@ -241,7 +241,7 @@ def test_rhs_full_plus_hyperdiffusion(pair):
 
     s = "2C"
     ops = euler.EulerOps(p.m, p.mets, p.consts, s, hyper=(p.cfg, p.vm))
-    rs = o.state if name == "box_n7" else random_state(p.m.nglobal, s)
+    rs = o.state if p.c["state"] == "bubble" else random_state(p.m.nglobal, s)
     oe = o.euler(s)
     ref = oe.rhs_full(rs) + o.hyper(rs)
     got = ops.rhs_full_hyper(state.StateField(s, rs))

@@ -80,6 +80,18 @@ def test_rhs_bitwise(prob):
         assert np.array_equal(e.rhs_vertical(rs), g[f"rhs_v_{s}"]), s
 
 
+def test_c4_target_bitwise(prob):
+    """Config 4's quantity rhs_full(q) + hyperdiffusion_apply(q) on the case's own (near-hydrostatic)
+    state, at config 4's element geometry (case c4_win)."""
+    p, g = prob
+    if "c4_target" not in g:
+        pytest.skip("no config-4 target fixture")
+    e = p.euler("2C")
+    S = e.rhs_full(p.state)
+    assert np.array_equal(S, g["rhs_full_state"])
+    assert np.array_equal(S + p.hyper(), g["c4_target"])
+
+
 def test_column_system_bitwise(prob):
     """LHEVI column Jacobian band, its pivoted band LU and the back-solve (euler.py:274-417,
     linalg.py:112-194) against the reference on the first golden columns."""

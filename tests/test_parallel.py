@@ -93,6 +93,29 @@ def test_local_to_global_map_and_counts():
     assert np.sum(seen == 2) == (world - 1) * n_face and np.all(seen >= 1)
 
 
+def test_lattice_keyed_state_agrees_on_slab_faces():
+    """The multi-GPU bench state (synthetic.fourier_state with noise keyed on the global lattice node,
+    SlabLayout.lattice_keys) is one global field: every rank holds, on every node, exactly the value
+    the single global mesh holds there, so the slab-face nodes two ranks share agree bitwise."""
+    from paper_2311_11425_b200 import mesh as hm, synthetic
+
+    world, nxp, ny, nv, N = 3, 2, 3, 2, 3
+    esz = (100.0, 120.0, 50.0)
+    ext = (esz[0] * nxp * world, esz[1] * ny, esz[2] * nv)
+    g = hm.build_box_lattice(nxp * world, ny, nv, N, ext)
+    G = parallel.SlabLayout(0, 1, nxp * world, ny, nv, N, elem_size=esz)
+    gkeys = G.lattice_keys(g)
+    assert len(np.unique(gkeys)) == g.nglobal
+    qg = synthetic.fourier_state(g.xg, ext, noise_keys=gkeys)
+    for r in range(world):
+        L = parallel.SlabLayout(r, world, nxp, ny, nv, N, elem_size=esz)
+        m = L.build_mesh()
+        l2g = L.local_to_global(m, g)
+        assert np.array_equal(L.lattice_keys(m), gkeys[l2g])
+        q = synthetic.fourier_state(m.xg, L.extents, noise_keys=L.lattice_keys(m))
+        assert np.array_equal(q, qg[l2g])
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world,nxp", [(2, 2), (3, 2), (2, 6)])
 def test_slab_pipeline_matches_single_mesh(world, nxp):
