@@ -24,6 +24,14 @@ def sha(a):
 TOL = 1e-12
 
 
+def xtol(p):
+    """Agreement bar between two of OUR kernel paths (different summation orders).  1e-14, except
+    at config 4's element geometry (kind "window": 156 x 156 x 625 m elements, N = 7), where a
+    reordering of the same sums moves H_nu by ~5e-14 (kernel-internal re-ordering
+    1.2-1.6e-13 on c4-like elements); parity with the reference stays at TOL."""
+    return 2e-13 if p.c["kind"] == "window" else 1e-14
+
+
 @pytest.fixture(scope="module", params=list(CASES))
 def pair(request):
     from oracle_cases import OracleProblem
@@ -165,12 +173,12 @@ def test_tile_path_used_and_matches_element_path(pair):
     a = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops)
     b = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops_v1)
     c = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops_line)
-    assert rel_l2(a, b) <= 1e-14 and rel_l2(c, b) <= 1e-14
+    assert rel_l2(a, b) <= xtol(p) and rel_l2(c, b) <= xtol(p)
     for f in range(1, 5):
         la = hyperdiff.laplacian_apply(o.state[:, f], p.vm, p.ops)
         lb = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops_v1)
         lc = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops_line)
-        assert rel_l2(la, lb) <= 1e-14 and rel_l2(lc, lb) <= 1e-14
+        assert rel_l2(la, lb) <= xtol(p) and rel_l2(lc, lb) <= xtol(p)
 
 
 def test_axis_form_matches_six_components(pair, monkeypatch):
@@ -196,12 +204,12 @@ def test_axis_form_matches_six_components(pair, monkeypatch):
     st = state.StateField("2C", o.state)
     a = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops)
     b = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops6)
-    assert rel_l2(a, b) <= 1e-14
+    assert rel_l2(a, b) <= xtol(p)
     assert rel_l2(a, o.hyper()) <= TOL
     for f in (1, 4):
         la = hyperdiff.laplacian_apply(o.state[:, f], p.vm, p.ops)
         lb = hyperdiff.laplacian_apply(o.state[:, f], p.vm, ops6)
-        assert rel_l2(la, lb) <= 1e-14
+        assert rel_l2(la, lb) <= xtol(p)
 
 
 def test_all_five_fields_one_pass(pair):
