@@ -123,6 +123,38 @@ def algorithmic_bytes_c4(ng, nloc):
     return A + B
 
 
+def flops_hnu(nelem, N, F=4, alpha=2):
+    """per element per field per pass 2*(6 n^4 + 9 n^3) + n^3 FP64 operations."""
+    n = N + 1
+    return alpha * F * nelem * (2 * (6 * n ** 4 + 9 * n ** 3) + n ** 3)
+
+
+def fp64_peak_tflops(reps=3):
+    """Measured FP64 FMA throughput (hv_probe_dfma: 8 independent DFMA chains per thread, 148 x 8 CTAs
+    of 256 threads), best of ``reps`` CUDA-event timings, TFLOP/s."""
+    import torch
+
+    from paper_2311_11425_b200 import _lib
+
+    blocks, threads, iters = 148 * 8, 256, 4096
+    out = torch.empty(blocks * threads, dtype=torch.float64, device="cuda")
+    L = _lib.lib()
+    run = lambda: _lib.check(L.hv_probe_dfma(out.data_ptr(), iters, blocks, threads,  # noqa: E731
+                                             _lib.stream_handle()))
+    run()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return 2.0 * 8 * iters * blocks * threads / (best * 1e-3) / 1e12
+
+
 def build_workload(name, rank, world, scale=1):
     from paper_2311_11425_b200 import euler, hyperdiff, metrics, state, synthetic
 
@@ -447,7 +479,7 @@ def run_ours(args, rank, world, local):
     alg = algorithmic_bytes_hnu(ng, nloc)
     achieved_op = alg / (ms * 1e-3) / 1e9
     # dominant kernel alone: the tile sweep of one pass (pass 1, q -> L q), CUDA events on its stream
-    kern_ms, kern_name, traffic, wform = None, None, None, 0
+    kern_ms, kern_name, traffic, wform, pass_ms, traffic_src = None, None, None, 0, {}, None
     if world == 1 and getattr(ops, "_plans", None):
         import ctypes as C
 
@@ -459,32 +491,56 @@ def run_ours(args, rank, world, local):
             oa = (C.c_int32 * nv_)(*range(nv_))
             L = _lib.lib()
 
-            def one_pass():
-                _lib.check(L.hv_lap_local(C.byref(plan), qd.data_ptr(), 5, nv_, qa, y.data_ptr(), nv_, oa, 1.0, 0, 0,
-                                          _lib.stream_handle()))
+            out5 = torch.empty((ng, 5), dtype=torch.float64, device="cuda")
+            va = (C.c_int32 * nv_)(*cfg.variables)
 
-            for _ in range(3):
-                one_pass()
-            torch.cuda.synchronize()
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            def one_pass(k):
+                if k == 1:    # pass 1: q (ng, 5) fields 1..4 -> y (ng, 4)
+                    _lib.check(L.hv_lap_local(C.byref(plan), qd.data_ptr(), 5, nv_, qa, y.data_ptr(), nv_, oa, 1.0,
+                                              0, 0, _lib.stream_handle()))
+                else:         # pass 2: y -> -L y into (ng, 5) fields 1..4, column 0 zeroed
+                    _lib.check(L.hv_lap_local(C.byref(plan), y.data_ptr(), nv_, nv_, oa, out5.data_ptr(), 5, va,
+                                              -1.0, 1, 0, _lib.stream_handle()))
+
             nk = max(5, args.steps)
-            k0.record(stream)
-            for _ in range(nk):
-                one_pass()
-            k1.record(stream)
-            torch.cuda.synchronize()
-            kern_ms = k0.elapsed_time(k1) / nk
+            pass_ms = {}
+            for k in (1, 2):
+                for _ in range(3):
+                    one_pass(k)
+                torch.cuda.synchronize()
+                k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                k0.record(stream)
+                for _ in range(nk):
+                    one_pass(k)
+                k1.record(stream)
+                torch.cuda.synchronize()
+                pass_ms[k] = k0.elapsed_time(k1) / nk
+            kern_ms = 0.5 * (pass_ms[1] + pass_ms[2])      # average launch of the dominant kernel
             kern_name = "lap_plane_kernel" if plan.kernel == 1 else "lap_tile_kernel"
             wform = int(plan.wform)
-            prof = ROOT / "profiles" / "r01_dominant_kernel.json"
+            prof = ROOT / "profiles" / "r02_dominant_kernel.json"
+            if not prof.exists():
+                prof = ROOT / "profiles" / "r01_dominant_kernel.json"
             if prof.exists():
                 traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-            del y
+                traffic_src = str(prof.relative_to(ROOT))
+            del y, out5
     alg_launch = alg / 2                       # one pass = one sweep launch
     achieved = alg_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else achieved_op
     # what the kernel must move with its metric form (axis form: 3 of the 6 metric doubles)
     own_launch = algorithmic_bytes_hnu(ng, nloc, ncomp=3 if wform == 1 else 6) / 2
     own_achieved = own_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else None
+    fp64 = None
+    if world == 1:
+        pk = fp64_peak_tflops()
+        fl_launch = flops_hnu(m.nelem, w.N) / 2
+        ach = fl_launch / (kern_ms * 1e-3) / 1e12 if kern_ms else None
+        fp64 = {"peak_tflops": pk, "peak_kind": "measured (hv_probe_dfma, DFMA chains, best of 3)",
+                "flops_per_op": flops_hnu(m.nelem, w.N), "flops_per_launch": fl_launch,
+                "kernel_achieved_tflops": ach, "kernel_frac": (ach / pk) if ach else None,
+                "op_achieved_tflops": flops_hnu(m.nelem, w.N) / (ms * 1e-3) / 1e12,
+                "arithmetic_intensity_flop_per_byte": flops_hnu(m.nelem, w.N) / alg,
+                "ridge_flop_per_byte": pk * 1e3 / peak}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu:
@@ -509,6 +565,7 @@ def run_ours(args, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": kern_name, "kernel_ms_per_launch": kern_ms,
+                         "kernel_ms_pass1": pass_ms.get(1), "kernel_ms_pass2": pass_ms.get(2),
                          "algorithmic_bytes_per_launch": alg_launch, "algorithmic_bytes_per_op": alg,
                          "op_achieved": achieved_op, "op_frac": achieved_op / peak,
                          "kernel_share_of_step": (2 * kern_ms / ms) if kern_ms else None,
@@ -516,11 +573,13 @@ def run_ours(args, rank, world, local):
                          "kernel_form_bytes_per_launch": own_launch,
                          "kernel_form_achieved": own_achieved,
                          "kernel_form_frac": (own_achieved / peak) if own_achieved else None,
-                         "scope": "dominant kernel = tile sweep of one Laplacian pass (2 per H_nu op); "
-                                  "achieved/frac use SURVEY 8(d)'s bytes (6 metric doubles per element node); "
-                                  "kernel_form_* the bytes of the metric form the kernel reads; "
-                                  "op_* = whole op incl. perimeter fix-ups; traffic = ncu dram bytes per "
-                                  "launch (profiles/r01_dominant_kernel.json)"},
+                         "scope": "dominant kernel = tile sweep of one Laplacian pass (2 per H_nu op), "
+                                  "kernel_ms_per_launch = mean of the pass-1 and pass-2 launches (CUDA events on "
+                                  "the launching stream); achieved/frac use SURVEY 8(d)'s bytes (6 metric doubles "
+                                  "per element node); kernel_form_* the bytes of the metric form the kernel reads; "
+                                  "op_* = whole op incl. perimeter fix-ups; traffic = ncu dram bytes per launch "
+                                  f"from one ncu --set full capture ({traffic_src})"},
+            "fp64": fp64,
             "cpu_baseline": cpu,
             "e2e": {"value": dof / (ms_e2e * 1e-3), "unit": "DOF-updates/s",
                     "h2d_bytes_per_step": ng * 5 * 8, "d2h_bytes_per_step": ng * 5 * 8,

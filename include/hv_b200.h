@@ -45,6 +45,10 @@ int hv_abi_version(void);
 const char* hv_last_error(void);
 /* Number of CUDA kernels this library has launched in the process (bench.py's gpu_launches). */
 int64_t hv_launch_count(void);
+/* Measurement probe, not on the operator path: `blocks` x `threads` threads each run 8 independent
+ * chains of `iters` dependent FP64 FMAs (2 * 8 * iters * blocks * threads FLOPs); bench.py times it
+ * with CUDA events for the measured FP64 peak.  d_out: >= blocks * threads doubles. */
+int hv_probe_dfma(double* d_out, int64_t iters, int blocks, int threads, void* stream);
 
 /* ---------------------------------------------------------------- host mesh
  * Replaces Mesh._number_gridpoints (mesh.py:86-107): bit-exact gid
@@ -153,8 +157,9 @@ typedef struct hv_lap_plan {
   const int32_t* d_ext_slots;  /* (next) slots with d_slot_ext >= 0                             */
   int64_t next;
   int face;                    /* column nodes per slab face                                   */
-  double* d_send;              /* (2*face, n_z, 5) local interface sums (NCCL send payload)    */
-  double* d_recv;              /* (2*face, n_z, 5) neighbour sums (NCCL receive buffer)        */
+  double* d_send;              /* (2*face, n_z, F) local interface sums (NCCL send payload),   *
+                                * F = fields of the pass; allocate for 5                        */
+  double* d_recv;              /* (2*face, n_z, F) neighbour sums (NCCL receive buffer)        */
   /* form of d_Wt for the plane kernel (kernel == 1): 0 = the 6 components of W;
    * 1 = axis form (scaled mode with c_1 == c_2, hyperdiff.py:71-80: G_nu = k_h I + (k_v - k_h) e_3 e_3^T):
    * u = sqrt(w3 Jg[gid]) e_3 (3 components, hv_viscous_axis) and W = kh |u|^2 I + kd u u^T;
@@ -270,6 +275,13 @@ int hv_band_solve(const double* d_data, const int32_t* d_ipiv, int64_t nb, int k
 int hv_euler_rhs_tiles(const hv_lap_plan* plan, const int32_t* d_elem, const double* d_w3, int set_id, int dirs,
                        int coriolis, double P_A, double R, double gamma, double omega, const double* d_M,
                        const double* d_q, int64_t ldq, double* d_out, int64_t ldo, int accumulate, void* stream);
+
+/* Multi-GPU Euler RHS (SURVEY §8(e) "other phases"): each rank runs hv_euler_rhs /
+ * hv_euler_rhs_tiles with a unit mass (the raw DSS sums of its slab, euler.py:101-103 before the
+ * division), the slab-face rows are exchanged and added in rank order, then
+ * out[g, f] (+)= Minv[g] * raw[g, f] for f < nf (accumulate != 0: added, e.g. onto H_nu). */
+int hv_rows_minv(double* d_out, int64_t ldo, const double* d_raw, int64_t ldr, const double* d_Minv, int64_t ng,
+                 int nf, int accumulate, void* stream);
 
 /* EulerOps.diagnostics (euler.py:421-456): d_out[7] = mass, energy_internal, energy_kinetic,
  * energy_potential, energy_total, p_surface_min, w_vertical_max.  d_M: the global mass (nglobal),

@@ -77,6 +77,9 @@ _SIGS = {
     "hv_abi_version": (C.c_int, []),
     "hv_last_error": (C.c_char_p, []),
     "hv_launch_count": (C.c_int64, []),
+    "hv_probe_dfma": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
+    "hv_rows_minv": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int,
+                               C.c_void_p]),
     "hv_number_gridpoints": (C.c_int, [_P, _I64, C.c_int, C.c_int, C.c_int, _D, _P, _P]),
     "hv_last_writer_coords": (C.c_int, [_P, _P, _I64, C.c_int, C.c_int, C.c_int, _I64, _P]),
     "hv_build_columns": (C.c_int, [_P, _I64, C.c_int, C.c_int, C.c_int, _P, _P, _I64, _I64, _P, _P, _P, _P, _P]),

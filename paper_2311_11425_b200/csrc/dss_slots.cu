@@ -70,7 +70,7 @@ __global__ void slot_pack_kernel(TileArgs A) {
   const int z = (int)(id % A.n_z);
   double acc[F];
   local_sum<F>(A, s, z, acc);
-  double* o = A.send + ((int64_t)A.slot_ext[s] * A.n_z + z) * 5;
+  double* o = A.send + ((int64_t)A.slot_ext[s] * A.n_z + z) * F;   // halo rows: F doubles
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) o[ff] = acc[ff];
 }
@@ -95,7 +95,7 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   local_sum<F>(A, s, z, acc);
   if (A.slot_ext && A.slot_ext[s] >= 0) {
     const int ext = A.slot_ext[s];
-    const double* rm = A.recv + ((int64_t)ext * A.n_z + z) * 5;
+    const double* rm = A.recv + ((int64_t)ext * A.n_z + z) * F;
     const bool lower_side = ext < A.face;   // side 0: the neighbour has the lower rank
 #pragma unroll
     for (int ff = 0; ff < F; ++ff) acc[ff] = lower_side ? rm[ff] + acc[ff] : acc[ff] + rm[ff];

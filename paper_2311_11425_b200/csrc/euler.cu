@@ -735,3 +735,34 @@ extern "C" int hv_euler_rhs_tiles(const hv_lap_plan* P, const int32_t* d_elem, c
   if (rc) return rc;
   return hv::slot_fixup(A, 5, st);   // shared side-face nodes: fixed-order sums of the partial rows
 }
+
+// ---------------------------------------------------------------- slab Euler RHS (parallel.py)
+namespace {
+
+// out[g, f] (+)= Minv[g] * raw[g, f]: the division by the global mass after the slab-face sums of
+// the raw DSS rows were completed across ranks (euler.py:101-103 with the DSS split over slabs);
+// explicit __dmul_rn / __dadd_rn: the same rounding as the single-GPU DSS kernel's Minv * sum
+// followed by the accumulate
+__global__ void rows_minv_kernel(double* __restrict__ out, int64_t ldo, const double* __restrict__ raw,
+                                 int64_t ldr, const double* __restrict__ Minv, int64_t ng, int nf, int accumulate) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= ng * nf) return;
+  const int64_t g = id / nf;
+  const int f = (int)(id - g * nf);
+  const double v = __dmul_rn(__ldg(Minv + g), __ldg(raw + g * ldr + f));
+  out[g * ldo + f] = accumulate ? __dadd_rn(out[g * ldo + f], v) : v;
+}
+
+}  // namespace
+
+extern "C" int hv_rows_minv(double* d_out, int64_t ldo, const double* d_raw, int64_t ldr, const double* d_Minv,
+                            int64_t ng, int nf, int accumulate, void* stream) {
+  if (!d_out || !d_raw || !d_Minv || ng < 0 || nf < 1 || ldo < nf || ldr < nf)
+    HV_FAIL(HV_ERR_INVALID, "hv_rows_minv: bad arguments");
+  if (ng == 0) return HV_OK;
+  const int64_t tot = ng * nf;
+  rows_minv_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_out, ldo, d_raw, ldr, d_Minv, ng,
+                                                                                     nf, accumulate);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}

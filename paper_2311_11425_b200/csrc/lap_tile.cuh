@@ -33,8 +33,8 @@ struct TileArgs {
   const int32_t* ext_slots; // (next) slots with slot_ext >= 0
   int64_t next;
   int face;                 // column nodes per slab face
-  double* send;             // (2 * face, n_z, 5) local sums for the neighbours
-  const double* recv;       // (2 * face, n_z, 5) neighbours' sums
+  double* send;             // (2 * face, n_z, F) local sums for the neighbours (F = fields of the pass)
+  const double* recv;       // (2 * face, n_z, F) neighbours' sums
   int wform;                // Wt form (plane kernel): 0 = 6 components, 1 = axis form u (W = kh|u|^2 I + kd u u^T)
   double kh, kd;
   const double* Ms;         // (nslot, n_z) Minv in slot order (coalesced in slot_fixup), or nullptr

@@ -1,0 +1,37 @@
+// Measurement probe (not on the operator path): FP64 FMA peak of the device.
+//
+// bench.py reports the sweep's FP64 work against a MEASURED DFMA throughput
+// (north_star: "FP64 pipe utilisation against peak").  Each thread runs 8
+// independent dependent-FMA chains (enough ILP to cover the DFMA latency at
+// 8+ warps per SM), the grid is a multiple of the SM count, and the result is
+// stored so the compiler cannot drop the chains.  FLOPs = 2 x threads x 8 x iters.
+#include <cuda_runtime.h>
+
+#include "hv_common.h"
+
+namespace {
+
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int64_t iters, double b, double c) {
+  double a[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) a[r] = 1e-3 * (threadIdx.x + r);
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) a[r] = fma(a[r], b, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) s += a[r];
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;   // practically never true
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = s;
+}
+
+}  // namespace
+
+extern "C" int hv_probe_dfma(double* d_out, int64_t iters, int blocks, int threads, void* stream) {
+  if (!d_out || iters <= 0 || blocks <= 0 || threads <= 0 || threads > 256)
+    HV_FAIL(HV_ERR_INVALID, "hv_probe_dfma: bad arguments");
+  dfma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(d_out, iters, 0.999999, 1e-7);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}

@@ -31,7 +31,8 @@ from . import _lib
 from .basis import lobatto
 from .device import torch_mod
 
-__all__ = ["SlabLayout", "DistTransport", "LoopbackTransport", "SlabHyperDiffusion", "run_loopback"]
+__all__ = ["SlabLayout", "DistTransport", "HostStagedTransport", "LoopbackTransport", "SlabHyperDiffusion",
+           "run_loopback", "run_loopback_euler", "halo_views"]
 
 ELEM_SIZE_C5 = (3125.0, 3125.0, 1250.0)
 
@@ -142,6 +143,40 @@ class DistTransport:
 
     def exchange(self, send, recv):
         self.wait(self.start(send, recv))
+
+
+class HostStagedTransport(DistTransport):
+    """DistTransport over a CPU backend (gloo) for CUDA halo buffers: the send buffer is copied to
+    the host after the work queued on the current stream, exchanged, and copied back onto the
+    current stream in ``wait``.  Multi-process tests on one GPU (no kernel ever waits on another
+    process's kernel) and hosts without NCCL peers."""
+
+    def start(self, send, recv):
+        import torch.distributed as dist
+
+        hs = send.detach().to("cpu")                   # synchronises with the producing stream
+        hr = torch_mod().empty_like(hs)
+        ops = []
+        if self.rank > 0:
+            ops += [dist.P2POp(dist.isend, hs[0], self.rank - 1), dist.P2POp(dist.irecv, hr[0], self.rank - 1)]
+        if self.rank < self.world - 1:
+            ops += [dist.P2POp(dist.isend, hs[1], self.rank + 1), dist.P2POp(dist.irecv, hr[1], self.rank + 1)]
+        return (dist.batch_isend_irecv(ops) if ops else [], hs, hr, recv)
+
+    @staticmethod
+    def wait(works):
+        reqs, hs, hr, recv = works
+        for r in reqs:
+            r.wait()
+        recv.copy_(hr.to(recv.device), non_blocking=False)
+
+
+def halo_views(halo, F):
+    """(send, recv) as (2, face * n_z * F) views of the plan's halo buffers: the pass packs F-wide
+    rows (slot_pack / slot_fixup), so only F of the 5 allocated doubles per row travel."""
+    send, recv = halo
+    per = send.shape[1] * send.shape[2] * F
+    return send.view(-1)[:2 * per].view(2, per), recv.view(-1)[:2 * per].view(2, per)
 
 
 class LoopbackTransport:
@@ -283,13 +318,56 @@ class SlabHyperDiffusion:
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 self.pass_local(k, q, out, "ext")
-                send, recv = self.halo
+                send, recv = halo_views(self.halo, len(self.cfg.variables))
                 works = transport.start(send, recv)
             self.pass_local(k, q, out, "int")
             main.wait_stream(side)
             transport.wait(works)
             self.pass_finish()
         return out
+
+
+    # ---- Euler RHS across slabs (the same face exchange, 5 fields)
+    def _raw_euler(self):
+        """EulerOps of this slab whose DSS divides by a unit mass: its rhs_full gives the slab's raw
+        DSS sums of the element accumulators (euler.py:101-103 before Minv)."""
+        if getattr(self, "_eraw", None) is None:
+            from . import euler
+            from .state import PhysConstants
+
+            torch = torch_mod()
+            ones = torch.ones(self.mesh.nglobal, dtype=torch.float64, device="cuda")
+            self._eraw = euler.EulerOps(self.mesh, self.mets, PhysConstants(omega=0.0), self.set_name,
+                                        mass=SlabMass(ones, ones))
+            self._raw = torch.empty((self.mesh.nglobal, 5), dtype=torch.float64, device="cuda")
+            self._esend = torch.zeros((2, self.layout.face * self.mesh.n_z * 5), dtype=torch.float64, device="cuda")
+            self._erecv = torch.zeros_like(self._esend)
+        return self._eraw
+
+    def euler_local(self, q):
+        """Raw slab sums of S(q) and their face rows packed into the send buffer."""
+        eo = self._raw_euler()
+        eo._rhs(q, 7, 0, out=self._raw)
+        for s, gi in self.face_gid.items():
+            self._esend[s].view(-1, 5).copy_(self._raw[gi])
+        return self._esend, self._erecv
+
+    def euler_finish(self, out, accumulate=True):
+        """Complete the face rows in global rank order, then out (+)= Minv * raw."""
+        for s, gi in self.face_gid.items():
+            self._raw[gi] = combine_interface(self._raw[gi], self._erecv[s].view(-1, 5), s)
+        _lib.check(_lib.lib().hv_rows_minv(out.data_ptr(), out.shape[1], self._raw.data_ptr(), 5,
+                                           self.ops.mass.d_Minv.data_ptr(), self.mesh.nglobal, 5, int(bool(accumulate)),
+                                           _lib.stream_handle()))
+        return out
+
+    def rhs_full_hyper(self, q, out, transport):
+        """S(q) + H_nu(q) on this slab (config 4's quantity, euler.py:111-118 + hyperdiff.py:97-106), both
+        DSS's completed across the slab faces."""
+        self.apply(q, out, transport)
+        send, recv = self.euler_local(q)
+        transport.exchange(send, recv)
+        return self.euler_finish(out)
 
 
 def setup_distributed(layout, cfg, dt, transport):
@@ -306,11 +384,21 @@ def run_loopback(ops, qs, outs):
     for k in range(alpha):
         for op, q, o in zip(ops, qs, outs):
             op.pass_local(k, q, o, "ext")
-        LoopbackTransport.exchange_all([op.halo for op in ops])
+        LoopbackTransport.exchange_all([halo_views(op.halo, len(op.cfg.variables)) for op in ops])
         for op, q, o in zip(ops, qs, outs):
             op.pass_local(k, q, o, "int")
         for op in ops:
             op.pass_finish()
+    return outs
+
+
+def run_loopback_euler(ops, qs, outs):
+    """S + H_nu on all slabs of one process (1-GPU test of the slab Euler pipeline)."""
+    run_loopback(ops, qs, outs)
+    bufs = [op.euler_local(q) for op, q in zip(ops, qs)]
+    LoopbackTransport.exchange_all(bufs)
+    for op, o in zip(ops, outs):
+        op.euler_finish(o)
     return outs
 
 

@@ -198,3 +198,142 @@ def test_slab_apply_stream_overlap_matches_sequential():
     torch.cuda.synchronize()
     assert torch.equal(out1, out2)
     assert NoNeighbour.calls == cfg.alpha
+
+
+def _global_problem(world, nxp, ny, nv, N, esz, cfg, dt, set_name="2C"):
+    from paper_2311_11425_b200 import euler, hyperdiff, mesh as hm, metrics, state
+
+    ext = (esz[0] * nxp * world, esz[1] * ny, esz[2] * nv)
+    g = hm.build_box_lattice(nxp * world, ny, nv, N, ext)
+    gm = metrics.project_metrics_to_columns(metrics.curl_invariant_metrics(g), g)
+    gvm = hyperdiff.build_viscous_metric(g, gm, cfg, dt=dt)
+    gops = euler.EulerOps(g, gm, state.PhysConstants(omega=0.0), set_name, hyper=(cfg, gvm))
+    return g, gops, gvm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,nxp,N", [(2, 2, 4), (3, 2, 3), (2, 1, 7)])
+def test_slab_euler_rhs_matches_single_mesh(world, nxp, N):
+    """S + H_nu across slabs (SURVEY §8(e) "other phases": the 5-field face exchange of the Euler
+    RHS DSS) equals the single-mesh rhs_full_hyper; interface rows bitwise equal on both owners."""
+    import torch
+
+    from cases import random_state, rel_l2
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    ny, nv = 2, 2
+    esz = (100.0, 120.0, 50.0)
+    cfg = hyperdiff.HyperDiffConfig(alpha=2, c=(0.05, 0.05, 0.0))
+    g, gops, gvm = _global_problem(world, nxp, ny, nv, N, esz, cfg, 0.5)
+    q = random_state(g.nglobal, "2C")
+    ref = gops.rhs_full_hyper(state.StateField("2C", q))
+    layouts = [parallel.SlabLayout(r, world, nxp, ny, nv, N, elem_size=esz) for r in range(world)]
+    ops = parallel.setup_loopback(layouts, cfg, 0.5)
+    maps = [L.local_to_global(op.mesh, g) for L, op in zip(layouts, ops)]
+    qs = [torch.from_numpy(q[l2g]).cuda() for l2g in maps]
+    outs = [torch.empty_like(x) for x in qs]
+    parallel.run_loopback_euler(ops, qs, outs)
+    got = np.zeros_like(ref)
+    vals = {}
+    for o, l2g in zip(outs, maps):
+        oo = o.cpu().numpy()
+        got[l2g] = oo
+        for li, gi in enumerate(l2g):
+            if gi in vals:
+                assert np.array_equal(vals[gi], oo[li])
+            vals[gi] = oo[li]
+    assert rel_l2(got, ref) <= 1e-13, rel_l2(got, ref)
+
+
+def _slab_proc(rank, world, port, nxp, N, q_global_path, outq):
+    """One rank of the 2-process test: gloo process group, halos staged through host memory
+    (HostStagedTransport), both ranks on cuda:0 (no kernel waits on the other process)."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2311_11425_b200 import hyperdiff
+
+        torch.cuda.set_device(0)
+        ny, nv, esz = 2, 2, (100.0, 120.0, 50.0)
+        cfg = hyperdiff.HyperDiffConfig(alpha=2, c=(0.05, 0.05, 0.0))
+        L = parallel.SlabLayout(rank, world, nxp, ny, nv, N, elem_size=esz)
+        tr = parallel.HostStagedTransport(rank, world)
+        op = parallel.setup_distributed(L, cfg, 0.5, tr)
+        z = np.load(q_global_path)
+        l2g = z[f"l2g{rank}"]
+        q = torch.from_numpy(np.ascontiguousarray(z["q"][l2g])).cuda()
+        h = torch.empty_like(q)
+        op.apply(q, h, tr)
+        s = torch.empty_like(q)
+        op.rhs_full_hyper(q, s, tr)
+        torch.cuda.synchronize()
+        outq.put((rank, h.cpu().numpy(), s.cpu().numpy(), op.ops.mass.d_M.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [4, 7])
+def test_two_process_slabs_host_staged(tmp_path, N):
+    """Two processes (torch.distributed gloo, world 2), each building its slab with
+    setup_distributed (cross-rank mass / projection) and applying H_nu and S + H_nu through the
+    DistTransport API, against the single-mesh results and the CPU oracle."""
+    import torch.multiprocessing as mp
+
+    from cases import random_state, rel_l2
+    from oracle import hevi_oracle as O
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    world, nxp, ny, nv = 2, 2, 2, 2
+    esz = (100.0, 120.0, 50.0)
+    cfg = hyperdiff.HyperDiffConfig(alpha=2, c=(0.05, 0.05, 0.0))
+    g, gops, gvm = _global_problem(world, nxp, ny, nv, N, esz, cfg, 0.5)
+    q = random_state(g.nglobal, "2C")
+    maps = [parallel.SlabLayout(r, world, nxp, ny, nv, N, elem_size=esz).local_to_global(
+        parallel.SlabLayout(r, world, nxp, ny, nv, N, elem_size=esz).build_mesh(), g) for r in range(world)]
+    path = tmp_path / "q.npz"
+    np.savez(path, q=q, **{f"l2g{r}": m for r, m in enumerate(maps)})
+    ctx = mp.get_context("spawn")
+    outq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_proc, args=(r, world, port, nxp, N, str(path), outq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted((outq.get(timeout=300) for _ in procs), key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    H = np.zeros((g.nglobal, 5))
+    S = np.zeros((g.nglobal, 5))
+    M = np.zeros(g.nglobal)
+    for (r, h, s, m), l2g in zip(res, maps):
+        for arr, loc in ((H, h), (S, s)):
+            arr[l2g] = loc
+        M[l2g] = m
+    # the two ranks agree bitwise on the shared face nodes
+    shared = np.intersect1d(maps[0], maps[1])
+    pos0 = {v: i for i, v in enumerate(maps[0])}
+    pos1 = {v: i for i, v in enumerate(maps[1])}
+    i0 = np.array([pos0[v] for v in shared])
+    i1 = np.array([pos1[v] for v in shared])
+    assert np.array_equal(res[0][1][i0], res[1][1][i1]) and np.array_equal(res[0][2][i0], res[1][2][i1])
+    st = state.StateField("2C", q)
+    assert rel_l2(M, gops.mass.M) <= 1e-15
+    assert rel_l2(H, hyperdiff.hyperdiffusion_apply(st, cfg, gvm, gops)) <= 1e-13
+    assert rel_l2(S, gops.rhs_full_hyper(st)) <= 1e-13
+    # and the CPU oracle on the global mesh
+    coords, layer, hcol = g.coords, g.elem_layer, g.elem_hcol
+    om = O.OracleMesh.from_coords("box", N, coords, layer, hcol,
+                                  O.dedupe_tol("box", max(g.cfg.panels_per_edge, 1), extents=g.cfg.box_extents))
+    _, J, grad = O.curl_metrics(om)
+    Jg, gz = O.project_columns(om, J, grad)
+    _, Minv = O.lumped_mass(om, J)
+    Gnu, _, _ = O.viscous_metric(om, grad, 2, c=cfg.c, dt=0.5)
+    Ho = O.hyperdiffusion(om, Gnu, O.gather(om.gid, Jg), Minv, q, 2)
+    assert rel_l2(H, Ho) <= 1e-12
+    So = O.OracleEuler(om, J, grad, Jg, gz, O.Consts(omega=0.0), "2C").rhs_full(q) + Ho
+    assert rel_l2(S, So) <= 1e-12
