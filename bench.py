@@ -480,41 +480,39 @@ def run_ours(args, rank, world, local):
     achieved_op = alg / (ms * 1e-3) / 1e9
     # dominant kernel alone: the tile sweep of one pass (pass 1, q -> L q), CUDA events on its stream
     kern_ms, kern_name, traffic, wform, pass_ms, traffic_src = None, None, None, 0, {}, None
+    fix_ms, yt_mode = {}, False
     if world == 1 and getattr(ops, "_plans", None):
         import ctypes as C
 
         plan = ops.lap_plan(vm)
         if plan.d_gt:
             nv_ = len(cfg.variables)
-            y = torch.empty((ng, nv_), dtype=torch.float64, device="cuda")
-            qa = (C.c_int32 * nv_)(*cfg.variables)
-            oa = (C.c_int32 * nv_)(*range(nv_))
-            L = _lib.lib()
-
-            out5 = torch.empty((ng, 5), dtype=torch.float64, device="cuda")
             va = (C.c_int32 * nv_)(*cfg.variables)
+            L = _lib.lib()
+            out5 = torch.empty((ng, 5), dtype=torch.float64, device="cuda")
 
-            def one_pass(k):
-                if k == 1:    # pass 1: q (ng, 5) fields 1..4 -> y (ng, 4)
-                    _lib.check(L.hv_lap_local(C.byref(plan), qd.data_ptr(), 5, nv_, qa, y.data_ptr(), nv_, oa, 1.0,
-                                              0, 0, _lib.stream_handle()))
-                else:         # pass 2: y -> -L y into (ng, 5) fields 1..4, column 0 zeroed
-                    _lib.check(L.hv_lap_local(C.byref(plan), y.data_ptr(), nv_, nv_, oa, out5.data_ptr(), 5, va,
-                                              -1.0, 1, 0, _lib.stream_handle()))
+            # one kernel of the op at a time through hv_hyperdiffusion_stage (the op's own launches, the
+            # op's own buffers): stage 1 = pass-1 sweep, 3 = pass-2 sweep, 2 / 4 = their fix-ups
+            def one_stage(k):
+                _lib.check(L.hv_hyperdiffusion_stage(C.byref(plan), qd.data_ptr(), 5, nv_, va, out5.data_ptr(), 5, k,
+                                                     _lib.stream_handle()))
 
             nk = max(5, args.steps)
             pass_ms = {}
-            for k in (1, 2):
+            for k in (1, 2, 3, 4):
                 for _ in range(3):
-                    one_pass(k)
+                    for kk in (1, 2, 3, 4):   # keep the intermediate of a whole op in place
+                        one_stage(kk)
                 torch.cuda.synchronize()
                 k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 k0.record(stream)
                 for _ in range(nk):
-                    one_pass(k)
+                    one_stage(k)
                 k1.record(stream)
                 torch.cuda.synchronize()
                 pass_ms[k] = k0.elapsed_time(k1) / nk
+            fix_ms = {1: pass_ms.pop(2), 2: pass_ms.pop(4)}
+            pass_ms = {1: pass_ms[1], 2: pass_ms[3]}
             kern_ms = 0.5 * (pass_ms[1] + pass_ms[2])      # average launch of the dominant kernel
             kern_name = "lap_plane_kernel" if plan.kernel == 1 else "lap_tile_kernel"
             wform = int(plan.wform)
@@ -524,7 +522,8 @@ def run_ours(args, rank, world, local):
             if prof.exists():
                 traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
                 traffic_src = str(prof.relative_to(ROOT))
-            del y, out5
+            yt_mode = bool(plan.d_yt)
+            del out5
     alg_launch = alg / 2                       # one pass = one sweep launch
     achieved = alg_launch / (kern_ms * 1e-3) / 1e9 if kern_ms else achieved_op
     # what the kernel must move with its metric form (axis form: 3 of the 6 metric doubles)
@@ -566,6 +565,9 @@ def run_ours(args, rank, world, local):
                          "frac": achieved / peak, "peak_kind": peak_kind, "traffic": traffic,
                          "kernel": kern_name, "kernel_ms_per_launch": kern_ms,
                          "kernel_ms_pass1": pass_ms.get(1), "kernel_ms_pass2": pass_ms.get(2),
+                         "fixup_ms_pass1": fix_ms.get(1), "fixup_ms_pass2": fix_ms.get(2),
+                         "intermediate": ("tile-ordered blocks (pass 1 writes L q in the sweep's block layout, "
+                                          "pass 2 bulk-copies it)") if yt_mode else "(nglobal, 4) rows",
                          "algorithmic_bytes_per_launch": alg_launch, "algorithmic_bytes_per_op": alg,
                          "op_achieved": achieved_op, "op_frac": achieved_op / peak,
                          "kernel_share_of_step": (2 * kern_ms / ms) if kern_ms else None,
@@ -574,8 +576,9 @@ def run_ours(args, rank, world, local):
                          "kernel_form_achieved": own_achieved,
                          "kernel_form_frac": (own_achieved / peak) if own_achieved else None,
                          "scope": "dominant kernel = tile sweep of one Laplacian pass (2 per H_nu op), "
-                                  "kernel_ms_per_launch = mean of the pass-1 and pass-2 launches (CUDA events on "
-                                  "the launching stream); achieved/frac use SURVEY 8(d)'s bytes (6 metric doubles "
+                                  "kernel_ms_per_launch = mean of the pass-1 and pass-2 launches, each timed alone "
+                                  "through hv_hyperdiffusion_stage (CUDA events on the launching stream, the op's "
+                                  "own buffers); achieved/frac use SURVEY 8(d)'s bytes (6 metric doubles "
                                   "per element node); kernel_form_* the bytes of the metric form the kernel reads; "
                                   "op_* = whole op incl. perimeter fix-ups; traffic = ncu dram bytes per launch "
                                   f"from one ncu --set full capture ({traffic_src})"},

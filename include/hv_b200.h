@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define HV_ABI_VERSION 5
+#define HV_ABI_VERSION 6
 
 #define HV_OK 0
 #define HV_ERR_INVALID 1        /* ValueError: bad argument / config                  */
@@ -167,6 +167,16 @@ typedef struct hv_lap_plan {
   int wform;
   double kh, kd;
   const double* d_Ms;          /* (nslot, n_z) Minv of the shared column nodes in slot order, or NULL */
+  /* tile-ordered intermediate of H_nu's alpha = 2 (plane kernel, N = 4, 2x2 tiles, 4 fields; DESIGN.md
+   * §4.2): pass 1 writes L q of the tile-owned nodes into d_yt in the sweep's own per-tile-layer
+   * block layout and the perimeter nodes' partial sums into d_part; the slot fix-up writes their
+   * final values as compact rows d_sv; pass 2 loads blocks and slot rows with bulk copies instead
+   * of gathering by gid.  d_yt == NULL keeps the (nglobal, F) path. */
+  const int32_t* d_tper;       /* (ntiles, NPER + 96): per tile the level offsets u*YUS + v of its slot
+                                * columns in slot order, then 32 runs (first slot, count, position)   */
+  double* d_yt;                /* (ntiles, nlay + 1, block) doubles (hv_plane_yt_layout)             */
+  double* d_sv;                /* (nslot * n_z * 4) final values of the slot column nodes: [nslot][4]
+                                * for z = 0, then per layer lb [nslot][N][4] for z = lb*N + 1 + kk   */
 } hv_lap_plan;
 
 /* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the
@@ -204,6 +214,12 @@ int hv_tile_pack_metric(int N, int TX, int TY, int64_t ntiles, int nlay, const i
  * 1: axis, 2: isotropic -- rows padded for conflict-free shared-memory reads where tuned);
  * d_Wt of hv_tile_pack_metric holds ntiles * nlay of them.  -1 for bad arguments. */
 int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform);
+/* Block layout of the tile-ordered intermediate (d_yt): out[0..4] = (level stride, u stride, field
+ * stride, doubles per tile-layer block, perimeter columns NPER per tile); the v stride is 1.
+ * Perimeter column p of a tile: p < V: (u, v) = (0, p); p < 2V: (U-1, p-V); then (1 + r % (U-2),
+ * 0 or V-1) for r = p - 2V (U = TX*N+1, V = TY*N+1).  Returns 0, or -1 when the plane kernel has
+ * no tile-ordered mode for (N, TX, TY, F). */
+int hv_plane_yt_layout(int N, int TX, int TY, int F, int64_t* out);
 
 /* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
  * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].
@@ -218,6 +234,12 @@ int hv_laplacian(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nf
  * euler.py:130-133), other columns untouched. */
 int hv_hyperdiffusion(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nvar, const int32_t* h_vars,
                       int alpha, double* d_out, int64_t ldo, int accumulate, void* stream);
+/* One kernel of hv_hyperdiffusion's alpha = 2 on a single-GPU tile plan, for per-kernel timing
+ * (bench.py): stage 1 = pass-1 sweep, 2 = pass-1 fix-up, 3 = pass-2 sweep, 4 = pass-2 fix-up;
+ * stages 1..4 in order equal hv_hyperdiffusion(alpha = 2, accumulate = 0).  HV_ERR_UNSUPPORTED
+ * for plans without a tile sweep. */
+int hv_hyperdiffusion_stage(const hv_lap_plan* plan, const double* d_q, int64_t ldq, int nvar, const int32_t* h_vars,
+                            double* d_out, int64_t ldo, int stage, void* stream);
 
 /* ------------------------------------------------------------ Euler RHS
  * EulerOps._precompute element part (euler.py:39-59): per element node the

@@ -69,6 +69,9 @@ class LapPlan(C.Structure):
         ("kh", C.c_double),
         ("kd", C.c_double),
         ("d_Ms", _P),
+        ("d_tper", _P),
+        ("d_yt", _P),
+        ("d_sv", _P),
     ]
 
 
@@ -94,11 +97,13 @@ _SIGS = {
     "hv_tile_pack_minv": (C.c_int, [_I64, C.c_int, C.c_int, _P, _P, _P, _P]),
     "hv_viscous_axis": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, C.c_int, _D, _P, _P]),
     "hv_plane_metric_doubles": (_I64, [C.c_int, C.c_int, C.c_int, C.c_int]),
+    "hv_plane_yt_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, C.c_int, _P, _P]),
     "hv_lap_local": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, C.c_uint32, C.c_int,
                                _P]),
     "hv_lap_finish": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _D, C.c_uint32, C.c_int, _P]),
     "hv_hyperdiffusion": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, C.c_int, _P, _I64, C.c_int, _P]),
+    "hv_hyperdiffusion_stage": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, C.c_int, _P]),
     "hv_euler_setup": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, _P, _P, _P, _P, C.c_int, _P, _P]),
     "hv_euler_vertical": (C.c_int, [C.c_int, _P, _P, C.c_int, _D, _D, _D, _I64, C.c_int, C.c_int, _P, _P, _P, _P, _P,
                                     _P, _I64, _P, _I64, C.c_int, _P]),
@@ -120,7 +125,7 @@ _SIGS = {
 }
 
 _lib = None
-ABI_VERSION = 5          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
+ABI_VERSION = 6          # include/hv_b200.h HV_ABI_VERSION (LapPlan layout above)
 
 
 def lib():

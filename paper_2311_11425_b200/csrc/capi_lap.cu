@@ -37,6 +37,7 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
   A.wform = P->wform; A.kh = P->kh; A.kd = P->kd; A.Ms = P->d_Ms;
+  A.io = 0; A.tper = P->d_tper; A.sv = P->d_sv;
   return A;
 }
 
@@ -49,6 +50,13 @@ bool use_plane(const hv_lap_plan* P, int nf) {
 bool use_tiles(const hv_lap_plan* P, int nf) {
   return use_plane(P, nf) ||
          (P->d_gt && P->d_Mt && P->kernel == 0 && hv::tile_supported(P->N, P->TX, P->TY, nf));
+}
+
+// alpha = 2 through the tile-ordered intermediate (plane kernel, N = 4, 2x2 tiles, 4 fields, one GPU)
+bool use_yt(const hv_lap_plan* P, int nf, const double* out) {
+  int64_t lay[5];
+  return P->d_yt && P->d_tper && P->d_sv && use_plane(P, nf) && hv::plane_yt_layout(P->N, P->TX, P->TY, nf, lay) &&
+         !(P->d_slot_ext && P->next > 0) && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 }
 
 // tile sweep over [t0, t1) (+ packing of the interface sums when pack != 0; no-op on one GPU)
@@ -124,6 +132,11 @@ extern "C" int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform) {
   return hv::plane_metric_doubles(N, TX, TY, wform);
 }
 
+extern "C" int hv_plane_yt_layout(int N, int TX, int TY, int F, int64_t* out) {
+  if (!out) return -1;
+  return hv::plane_yt_layout(N, TX, TY, F, out) ? 0 : -1;
+}
+
 extern "C" int hv_tile_pack_minv(int64_t rows, int gts, int mts, const int32_t* d_gt, const double* d_Minv,
                                  double* d_Mt, void* stream) {
   if (rows <= 0 || gts <= 0 || mts <= 0 || !d_gt || !d_Minv || !d_Mt) HV_FAIL(HV_ERR_INVALID, "hv_tile_pack_minv: bad args");
@@ -182,15 +195,17 @@ extern "C" int hv_laplacian(const hv_lap_plan* P, const double* d_q, int64_t ldq
   return lap_pass(P, d_q, ldq, nf, qf, d_out, ldo, of, scale, 0u, (cudaStream_t)stream);
 }
 
-extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar,
-                                 const int32_t* h_vars, int alpha, double* d_out, int64_t ldo, int accumulate,
-                                 void* stream) {
+namespace {
+
+// hv_hyperdiffusion; stage 0 = the whole op, stages 1..4 = one kernel of alpha = 2 on a tile plan
+// (pass-1 sweep, pass-1 fix-up, pass-2 sweep, pass-2 fix-up; hv_hyperdiffusion_stage)
+int hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar, const int32_t* h_vars, int alpha,
+                   double* d_out, int64_t ldo, int accumulate, cudaStream_t st, int stage) {
   int rc = check_plan(P);
   if (rc) return rc;
   if (alpha != 1 && alpha != 2) HV_FAIL(HV_ERR_INVALID, "alpha must be 1 or 2");
   if (nvar < 0 || nvar > 5 || !d_q || !d_out || ldo < 1 || ldo > 32 || ldq < 1)
     HV_FAIL(HV_ERR_INVALID, "hv_hyperdiffusion: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
   unsigned keep = 0;
   hv::FieldMap qf{}, of{}, yf{};
   for (int v = 0; v < nvar; ++v) {
@@ -201,6 +216,9 @@ extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_
     keep |= 1u << h_vars[v];
   }
   const unsigned zmask = ((ldo >= 32) ? 0xffffffffu : ((1u << ldo) - 1u)) & ~keep;
+  if (stage && (alpha != 2 || nvar == 0 || !use_tiles(P, nvar) || (P->d_slot_ext && P->next > 0) ||
+                (reinterpret_cast<uintptr_t>(d_out) & 15) != 0))
+    HV_FAIL(HV_ERR_UNSUPPORTED, "hv_hyperdiffusion_stage: alpha = 2 on a single-GPU tile plan only");
   if (nvar == 0) {
     if (accumulate) return HV_OK;
     const int64_t tot = P->nglobal * ldo;
@@ -210,7 +228,42 @@ extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_
   }
   const double sign = (alpha % 2 == 1) ? 1.0 : -1.0;  // (-1)^(alpha+1)
   if (alpha == 1) return lap_pass(P, d_q, ldq, nvar, qf, d_out, ldo, of, sign, zmask, st, accumulate);
-  rc = lap_pass(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, 0u, st);
-  if (rc) return rc;
-  return lap_pass(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st, accumulate);
+  const bool all = stage == 0;
+  if (use_yt(P, nvar, d_out)) {
+    // pass 1: q -> tile-ordered y blocks + perimeter partial rows, whose fix-up writes the compact slot
+    // rows; pass 2: blocks and slot rows by bulk copy -> out rows (+ the usual slot fix-up)
+    hv::TileArgs A1 = tile_args(P, d_q, ldq, qf, P->d_yt, 0, yf, 1.0, 0u, 0);
+    A1.io = 1;
+    if ((all || stage == 1) && (rc = hv::laplacian_plane(A1, P->N, nvar, P->D, st))) return rc;
+    if ((all || stage == 2) && (rc = hv::slot_fixup(A1, nvar, st))) return rc;
+    hv::TileArgs A2 = tile_args(P, P->d_yt, 0, yf, d_out, ldo, of, sign, zmask, accumulate);
+    A2.io = 2;
+    if ((all || stage == 3) && (rc = hv::laplacian_plane(A2, P->N, nvar, P->D, st))) return rc;
+    if (all || stage == 4) return lap_finish(P, nvar, d_out, ldo, of, sign, zmask, st, accumulate);
+    return HV_OK;
+  }
+  if (all) {
+    rc = lap_pass(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, 0u, st);
+    if (rc) return rc;
+    return lap_pass(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st, accumulate);
+  }
+  if (stage == 1) return lap_local(P, d_q, ldq, nvar, qf, P->d_y, nvar, yf, 1.0, 0u, st, 0);
+  if (stage == 2) return lap_finish(P, nvar, P->d_y, nvar, yf, 1.0, 0u, st, 0);
+  if (stage == 3) return lap_local(P, P->d_y, nvar, nvar, yf, d_out, ldo, of, sign, zmask, st, accumulate);
+  if (stage == 4) return lap_finish(P, nvar, d_out, ldo, of, sign, zmask, st, accumulate);
+  HV_FAIL(HV_ERR_INVALID, "hv_hyperdiffusion_stage: stage must be 1..4");
+}
+
+}  // namespace
+
+extern "C" int hv_hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar,
+                                 const int32_t* h_vars, int alpha, double* d_out, int64_t ldo, int accumulate,
+                                 void* stream) {
+  return hyperdiffusion(P, d_q, ldq, nvar, h_vars, alpha, d_out, ldo, accumulate, (cudaStream_t)stream, 0);
+}
+
+extern "C" int hv_hyperdiffusion_stage(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nvar,
+                                       const int32_t* h_vars, double* d_out, int64_t ldo, int stage, void* stream) {
+  if (stage < 1 || stage > 4) HV_FAIL(HV_ERR_INVALID, "hv_hyperdiffusion_stage: stage must be 1..4");
+  return hyperdiffusion(P, d_q, ldq, nvar, h_vars, 2, d_out, ldo, 0, (cudaStream_t)stream, stage);
 }

@@ -80,12 +80,31 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (id >= A.nslot * A.n_z) return;
   const unsigned nz = (unsigned)A.n_z;
-  const int64_t s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
-  const int z = (int)((unsigned)id - (unsigned)s * nz);
+  int64_t s;     // slot
+  int z;         // level
+  double* o;
+  if (row_mode == 3) {
+    // the slot rows of the tile-ordered intermediate, in their own order (lap_tile.cuh: [nslot][F] for
+    // z = 0, then per layer block [nslot][N][F]): thread id writes row id
+    const int N = (A.n_z - 1) / A.nlay;
+    if (id < A.nslot) {
+      s = id;
+      z = 0;
+    } else {
+      const int64_t r = id - A.nslot, lb = r / (A.nslot * N), w = r - lb * (A.nslot * N);
+      s = w / N;
+      z = (int)(lb * N + 1 + (w - s * N));
+    }
+    o = A.sv + id * F;
+  } else {
+    s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
+    z = (int)((unsigned)id - (unsigned)s * nz);
+    o = nullptr;
+  }
   const int c = A.slot_col[s];
   const int g = A.col_gid[(int64_t)c * A.n_z + z];
-  double* o = A.out + (int64_t)g * A.ldo;
-  const double mi = A.Ms ? __ldg(A.Ms + id) : __ldg(A.Minv + g);
+  if (row_mode != 3) o = A.out + (int64_t)g * A.ldo;
+  const double mi = A.Ms ? __ldg(A.Ms + s * A.n_z + z) : __ldg(A.Minv + g);
   double prev[F];
   if (A.accumulate) {
 #pragma unroll
@@ -104,7 +123,7 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
 #pragma unroll
   for (int ff = 0; ff < F; ++ff) r[ff] = A.scale * (mi * acc[ff]);
   if constexpr (F == 4) {
-    if (row_mode == 1) {             // (ng, 4) rows, fields 0..3
+    if (row_mode == 1 || row_mode == 3) {   // (ng, 4) rows, fields 0..3 / slot rows
       st2(o, r[0], r[1]);
       st2(o + 2, r[2], r[3]);
       return;
@@ -144,7 +163,10 @@ int fixup_f(const TileArgs& A, cudaStream_t st) {
   const int64_t tot = A.nslot * A.n_z;
   if (tot >= (int64_t)1 << 31) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: %lld slot rows", (long long)tot);
   int row_mode = 0;
-  if (F == 4 && !A.accumulate && A.out && ((uintptr_t)A.out & 15) == 0) {
+  if (A.io == 1) {
+    if (F != 4 || A.accumulate || !A.sv || A.slot_ext) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: slot rows need F = 4");
+    row_mode = 3;
+  } else if (F == 4 && !A.accumulate && A.out && ((uintptr_t)A.out & 15) == 0) {
     if (A.ldo == 4 && !A.zero_mask && A.of.f[0] == 0 && A.of.f[1] == 1 && A.of.f[2] == 2 && A.of.f[3] == 3)
       row_mode = 1;
     else if (A.ldo == 5 && A.zero_mask == 1u && A.of.f[0] == 1 && A.of.f[1] == 2 && A.of.f[2] == 3 &&

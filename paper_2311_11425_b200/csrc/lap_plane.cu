@@ -81,7 +81,7 @@ __device__ __forceinline__ double2 ldg_stream2(const double* p) {
 // WF: form of the packed metric.  0: the 6 components of W as 3 pairs; 1: axis form (scaled
 // mode with c_1 == c_2): u = sqrt(w3 Jg) e_3 (3 doubles per node), W d = kh |u|^2 d + kd u (u . d);
 // 2: isotropic form (c_1 == c_2 == c_3): s = kh w3 Jg (1 double per node), W d = s d.
-template <int n, int TX, int TY, int F, int WV, int H = 1, int WF = 0>
+template <int n, int TX, int TY, int F, int WV, int H = 1, int WF = 0, int IO = 0>
 struct PlaneCfg {
   static constexpr int N = n - 1;
   static constexpr int U = TX * N + 1, V = TY * N + 1, UV = U * V;
@@ -118,16 +118,37 @@ struct PlaneCfg {
   static constexpr int PN = (NODES + NT - 1) / NT;       // gather node items per thread
   static constexpr int FI = UV * N;                      // output items per layer (k < N)
   static constexpr int PF = (FI + NT - 1) / NT;          // output items per thread
-  // shared memory (doubles): q | W (WV 0) | scratch | ctab (int4) | code | mbarrier
-  static constexpr int OFF_W = (SQ + 1) & ~1;
+  // tile-ordered intermediate (IO 1 writes it, IO 2 reads it): one block per tile-layer, level-major
+  // [k < N][f][u][v] (block nlay: the top level of the columns, k = 0).  A half-warp's lanes vary
+  // (f, e) in the plane and eta-line reads: field stride = 1 (mod 4) and u stride = 2 (mod 4) put
+  // them on 16 distinct 8-byte banks (f*YFS + px*N*YUS + py*N spans 0..15 mod 16 at N = 4).  A
+  // level of all fields is whole 16-byte units, so levels 1..N-1 and a level 0 are single bulk copies.
+  static constexpr int YUS = V + ((2 - V % 4) + 4) % 4;
+  static constexpr int YFS = U * YUS + ((1 - (U * YUS) % 4) + 4) % 4;
+  static constexpr int YLS = F * YFS + (F * YFS) % 2;
+  static constexpr int YBLK = N * YLS;
+  static constexpr int FIY = N * UV;                     // block items per layer, (k, u, v) order
+  static constexpr int PFY = (FIY + NT - 1) / NT;
+  // perimeter column nodes of a tile (shared with other tiles): their final values come from the
+  // slot fix-up's compact (slot, z, F) rows, staged per layer (levels 1..N of the layer; the
+  // prologue stages levels 0..N) and patched into the level buffers
+  static constexpr int NPER = 2 * V + 2 * (U - 2);
+  // shared memory (doubles): q (IO 2: levels 1..N-1 | level 0 ring [2] | perimeter stage) | W (WV 0) |
+  // scratch | ctab (int4) | code | mbarriers (metric, IO 2 loads)
+  static constexpr int QB_L0 = (N - 1) * YLS;            // IO 2: the two level-0 planes
+  static constexpr int QB_S = QB_L0 + 2 * YLS;           // IO 2: perimeter stage [NPER][N][F]
+  static constexpr int SQB = IO == 2 ? QB_S + NPER * N * F : SQ;
+  static constexpr int TPW = NPER + 3 * 32;              // IO 2: ints per tile of TileArgs::tper
+  static constexpr int OFF_W = (SQB + 1) & ~1;
   static constexpr int OFF_S = OFF_W + (WV == 0 ? WL : 0);
   static constexpr int OFF_T = (OFF_S + SE + 1) & ~1;
   static constexpr int OFF_C = OFF_T + 2 * UV;
   static constexpr int OFF_P = OFF_C + (UV + 1) / 2;
-  static constexpr int OFF_BAR = (OFF_P + (UV + 1) / 2 + 1) & ~1;
+  static constexpr int OFF_PD = OFF_P + (UV + 1) / 2;  // IO 2: [NPER] level offset of the stage's slot columns
+  static constexpr int OFF_BAR = (OFF_PD + (IO == 2 ? (NPER + 1) / 2 : 0) + 1) & ~1;
   // split planes (H > 1): D in shared memory for the xi exchange, whose row / column offsets vary
   // across the lanes of a warp (constant-bank loads would serialise)
-  static constexpr int OFF_D = OFF_BAR + 2;
+  static constexpr int OFF_D = OFF_BAR + 4;
   static constexpr size_t SMEM = sizeof(double) * (OFF_D + (H > 1 ? n * n : 0));
 };
 
@@ -142,10 +163,15 @@ struct PlaneCfg {
 // OM: output rows, fixed at compile time for the hot passes (smaller code): 0 = any (runtime
 // checks below), 1 = (ng, 4) rows of fields 0..3 written, 2 = (ng, 5) rows of fields 1..4 written
 // with column 0 zeroed (H_nu's second pass)
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0>
-__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
-  using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
-  constexpr int N = C::N, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
+// IO: 0 = q gathered by gid and results written to (nglobal, ld) rows; 1 = results written to the
+// tile-ordered intermediate at A.out (final values for tile-owned nodes, raw partial sums for the
+// perimeter nodes other tiles share: slot_fixup_yt completes them in place); 2 = q read from the
+// tile-ordered intermediate at A.q, one bulk copy per tile-layer block into a two-slot ring
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
+__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
+  using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
+  static_assert(IO == 0 || (H == 1 && F == 4 && AB == 0), "tile-ordered intermediate: H = 1, 4 fields");
+  constexpr int N = C::N, U = C::U, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                                    // [F][QP] gathered q of the current layer
   double* s_w = sm + C::OFF_W;                         // metric of the current layer (WV 0, TMA)
@@ -153,7 +179,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
   int4* s_ct = reinterpret_cast<int4*>(sm + C::OFF_T); // [UV] element-copy offsets
   int* s_code = reinterpret_cast<int*>(sm + C::OFF_C); // [UV] partial row or -1
   int* s_perm = reinterpret_cast<int*>(sm + C::OFF_P); // [UV] output column order: tile-owned first
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // metric stage (WV 0)
+  int* s_pdst = reinterpret_cast<int*>(sm + C::OFF_PD);  // IO 2: [stage position] u * YUS + v of the slot column
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);  // [0] metric stage (WV 0), [1] IO 2 loads
   double* sD = sm + C::OFF_D;                          // [n][n] (H > 1)
   const int tid = threadIdx.x;
   const int f = tid % F;
@@ -209,6 +236,80 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
       }
     }
     cp_async_commit();
+  };
+  const int64_t chain = (int64_t)(nlay + 1) * C::YBLK;
+  // IO 2: the tile's slot columns (perimeter columns other tiles share), staged in slot order: run r of
+  // consecutive slots (lane r of warp 0: first slot, count, first stage position); nper = their number
+  const int32_t* tper = A.tper + t * C::TPW;
+  int r_start = 0, r_cnt = 0, r_pos = 0, nper = 0;
+  if constexpr (IO == 2) {
+    if (tid < 32) {
+      r_start = tper[C::NPER + 3 * tid];
+      r_cnt = tper[C::NPER + 3 * tid + 1];
+      r_pos = tper[C::NPER + 3 * tid + 2];
+    }
+    for (int j = 0; j < C::NPER; ++j) nper += (tper[j] >= 0) ? 1 : 0;
+  }
+  // IO 2 loads of layer l: levels 1..N-1 of block l -> s_q, level 0 of block l+1 -> level-0 plane
+  // (l+1)&1, the slot rows of levels z = l*N+1 .. l*N+N (slot-row block l: [slot][N][F]) -> the stage;
+  // l = -1 (prologue): level 0 of block 0 -> plane 0, slot rows of z = 0 -> the stage.  One mbarrier
+  // phase, issued by warp 0 (lane r: run r of consecutive slots).
+  auto issue_loads = [&](int l, int nper) {
+    const int lane = tid & 31;
+    const int nlev = (l < 0) ? 1 : N;
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)((l < 0 ? 1 : N) * C::YLS * 8 + nper * nlev * F * 8);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + 1)), "r"(bytes)
+                   : "memory");
+      const double* base = A.q + t * chain;
+      if (l < 0) {
+        tma_copy(s_q + C::QB_L0, base, C::YLS * 8, bar + 1);                              // block 0, level 0
+      } else {
+        tma_copy(s_q, base + (int64_t)l * C::YBLK + C::YLS, (N - 1) * C::YLS * 8, bar + 1);
+        tma_copy(s_q + C::QB_L0 + ((l + 1) & 1) * C::YLS, base + (int64_t)(l + 1) * C::YBLK, C::YLS * 8, bar + 1);
+      }
+    }
+    if (r_cnt > 0) {
+      const double* src = (l < 0) ? A.sv + (int64_t)r_start * F
+                                  : A.sv + A.nslot * F + ((int64_t)l * A.nslot + r_start) * N * F;
+      tma_copy(s_q + C::QB_S + r_pos * nlev * F, src, (uint32_t)(r_cnt * nlev * F * 8), bar + 1);
+    }
+  };
+  // IO 2: stage -> level buffers (layer l: levels 1..N; prologue: level 0 -> plane 0); an item =
+  // (stage position j, level kk): its F fields in two 16-byte loads, stored at the column's offset
+  auto patch = [&](int l, int nper) {
+    const int nit = (l < 0) ? nper : nper * N;
+    for (int x = tid; x < nit; x += C::NT) {
+      const int j = (l < 0) ? x : x / N, kk = (l < 0) ? 0 : 1 + x % N;
+      const int o = s_pdst[j];
+      const double* src = s_q + C::QB_S + ((l < 0) ? j : j * N + kk - 1) * F;
+      const double2 a = *reinterpret_cast<const double2*>(src);
+      const double2 b = *reinterpret_cast<const double2*>(src + 2);
+      double* dst = (kk == 0) ? s_q + C::QB_L0
+                              : (kk == N ? s_q + C::QB_L0 + ((l + 1) & 1) * C::YLS : s_q + (kk - 1) * C::YLS);
+      dst[o] = a.x;
+      dst[o + C::YFS] = a.y;
+      dst[o + 2 * C::YFS] = b.x;
+      dst[o + 3 * C::YFS] = b.y;
+    }
+  };
+  // q at tile node (u, v, k) of the current layer (IO 2: level 0 from plane l&1, levels 1..N-1 from
+  // the level buffer, the top level k = N from plane (l+1)&1)
+  auto qrd = [&](const double* lo, const double* hi, int u, int v, int k) -> double {
+    if constexpr (IO == 2) {
+      const int o = f * C::YFS + u * C::YUS + v;
+      return (k == 0) ? lo[o] : (k == N ? hi[o] : s_q[(k - 1) * C::YLS + o]);
+    } else {
+      return s_q[tq(u, v, k)];
+    }
+  };
+  // sum of the (up to four) element copies of a tile node, fixed order (c0 + c1) + (c2 + c3)
+  auto csum = [&](const int4 ct, const double* sp) -> double {
+    const double c0 = sp[ct.x];
+    const double c1 = (ct.y >= 0) ? sp[ct.y] : 0.0;
+    const double c2 = (ct.z >= 0) ? sp[ct.z] : 0.0;
+    const double c3 = (ct.z >= 0) ? sp[ct.w] : 0.0;
+    return (c0 + c1) + (c2 + c3);
   };
   auto issue_metric = [&](int l) {
     if (AB & 4) return;
@@ -284,11 +385,17 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
   };
 
   int gcur[PN], gnext[PN];
-  load_gids(0, gcur);
+  if constexpr (IO != 2) load_gids(0, gcur);
   if (WV == 0 && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
+  if (IO == 2 && tid == 0) {
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  if constexpr (IO == 2)
+    for (int j = tid; j < C::NPER; j += C::NT) s_pdst[j] = tper[j];
   if (WV == 1 && tid == 0) l2_prefetch(Wt_t, C::WL * 8);
   for (int uv = tid; uv < UV; uv += C::NT) {
     const int u = uv / V, v = uv % V;
@@ -301,8 +408,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
     s_code[uv] = A.code[t * UV + uv];
   }
-  issue_gather(gcur);
-  if (nlay > 1) load_gids(1, gnext);
+  if constexpr (IO != 2) {
+    issue_gather(gcur);
+    if (nlay > 1) load_gids(1, gnext);
+  }
   if constexpr (H > 1)
     for (int x = tid; x < n * n; x += C::NT) sD[x] = Dt.D[x / n][x % n];
   __syncthreads();
@@ -314,6 +423,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
   }
   __syncthreads();
   if (WV == 0 && tid == 0) issue_metric(0);
+  if constexpr (IO == 2) {   // prologue: level 0 of block 0 (+ its perimeter rows); then layer 0's loads
+    if (tid < 32) issue_loads(-1, nper);
+    mbar_wait(bar + 1, 0);
+    patch(-1, nper);
+    __syncthreads();
+    if (tid < 32) {
+      fence_proxy_async();
+      issue_loads(0, nper);
+    }
+  }
+  int nown = 0;   // IO 1: tile-owned columns (s_perm lists them first)
+  if constexpr (IO == 1)
+    for (int uv = 0; uv < UV; ++uv) nown += (s_code[uv] < 0) ? 1 : 0;
   double carry[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) carry[r] = 0.0;
@@ -323,12 +445,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
 
   for (int l = 0; l < nlay; ++l) {
     // ---- a: q(l) has landed
-    cp_async_wait_all();
+    if constexpr (IO == 2) {   // layer l's loads (levels 1..N-1, level 0 of block l+1, perimeter rows)
+      mbar_wait(bar + 1, (uint32_t)((l + 1) & 1));
+      patch(l, nper);
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();
+    const double* sq_lo = s_q + C::QB_L0 + (l & 1) * C::YLS;
+    const double* sq_hi = s_q + C::QB_L0 + ((l + 1) & 1) * C::YLS;
     if (WV == 1 && tid == 0 && l + 1 < nlay) l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
     if (tid == C::NT - 1 && l + 1 < nlay) {   // output-item gid / Minv of the next layer -> L2
       l2_prefetch(Mt_t + (int64_t)(l + 1) * C::MTS, C::MTS * 8);
-      l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
+      if (IO != 1) l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
     }
     // ---- b: plane derivatives in registers, eta lines (i = jp) strong
     double p0[NR][n], p2[NR][n];   // [row][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
@@ -337,7 +466,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
       for (int r = 0; r < NR; ++r) {
         double ql[n];
 #pragma unroll
-        for (int k = 0; k < n; ++k) ql[k] = s_q[tq(px * N + I0 + r, py * N + jp, k)];
+        for (int k = 0; k < n; ++k) ql[k] = qrd(sq_lo, sq_hi, px * N + I0 + r, py * N + jp, k);
 #pragma unroll
         for (int k = 0; k < n; ++k) {
           double s = 0.0;
@@ -393,7 +522,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
         const int li = (H == 1) ? jp : I0 + kk, k = (H == 1) ? K0 + kk : jp;
         double ql[n];
 #pragma unroll
-        for (int a = 0; a < n; ++a) ql[a] = s_q[tq(px * N + li, py * N + a, k)];
+        for (int a = 0; a < n; ++a) ql[a] = qrd(sq_lo, sq_hi, px * N + li, py * N + a, k);
 #pragma unroll
         for (int a2 = 0; a2 < n; ++a2) {
           double s = 0.0;
@@ -404,8 +533,16 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
       }
     }
     __syncthreads();
-    // s_q of layer l is dead: gather q(l+1)
-    if (l + 1 < nlay) issue_gather(gnext);
+    // s_q of layer l is dead: gather q(l+1) (IO 2: the loads of layer l + 1; plane l&1 takes level 0 of
+    // block l + 2, the level buffer and the stage the rest)
+    if constexpr (IO == 2) {
+      if (tid < 32 && l + 1 < nlay) {
+        fence_proxy_async();
+        issue_loads(l + 1, nper);
+      }
+    } else {
+      if (l + 1 < nlay) issue_gather(gnext);
+    }
     if (AB & 8) {
 #pragma unroll
       for (int r = 0; r < NR; ++r)
@@ -576,12 +713,26 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     // ---- e: element accumulator (+ vertical carry) -> scratch; gid / Minv of the output items
     int gf[PF];
     double mf[PF];
+    double my[C::PFY];   // IO 1: scale * Minv of tile-owned block items, 1 for perimeter (raw partial sums)
+    constexpr int FI_ = C::FI;
+    if constexpr (IO == 1) {
 #pragma unroll
-    for (int it = 0; it < PF; ++it) {
-      const int qi = tid + it * C::NT;
-      const int node = (qi < C::FI) ? s_perm[qi / N] * n + qi % N : 0;
-      gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
-      mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
+      for (int it = 0; it < C::PFY; ++it) {
+        const int qi = tid + it * C::NT;
+        my[it] = 1.0;
+        if (qi < C::FIY) {
+          const int k = qi / UV, uv = qi - k * UV;
+          if (s_code[uv] < 0) my[it] = A.scale * __ldg(Mt_t + (int64_t)l * C::MTS + uv * n + k);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < PF; ++it) {
+        const int qi = tid + it * C::NT;
+        const int node = (qi < C::FI) ? s_perm[qi / N] * n + qi % N : 0;
+        gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
+        mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
+      }
     }
     if (act) {
 #pragma unroll
@@ -604,7 +755,65 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
     // ---- f: node owners (items (column, k < N); k = N only on the top layer) sum the
     // element copies of all F fields (predicated loads, fixed order (c0 + c1) + (c2 + c3)),
     // then one row store per item
-    if (!(AB & 1)) {
+    if constexpr (IO == 1) {
+      // block items in (k, u, v) order: consecutive lanes store consecutive v.  Perimeter (slot) items:
+      // raw partial sums into their partial rows (the fix-up sums them into the compact slot rows that
+      // pass 2 stages); their block entries are never read, the raw sums keep the block's sectors whole
+      double* yb = A.out + t * chain + (int64_t)l * C::YBLK;
+#pragma unroll
+      for (int it = 0; it < C::PFY; ++it) {
+        const int qi = tid + it * C::NT;
+        if (qi >= C::FIY) continue;
+        const int k = qi / UV, uv = qi - k * UV, u = uv / V, v = uv - u * V;
+        const int4 ct = s_ct[uv];
+#pragma unroll
+        for (int p = 0; p < F; ++p) yb[k * C::YLS + p * C::YFS + u * C::YUS + v] = my[it] * csum(ct, s_s + p * C::SP + k);
+      }
+      // the layout's padding (v = V..YUS-1 of every u row, u*YUS >= U*YUS up to YFS): zeros, so that
+      // every sector of the block is written whole (no partial-sector read-modify-write in L2)
+      {
+        constexpr int PV = C::YUS - V, PT = C::YFS - U * C::YUS, PP = U * PV + PT;
+        for (int x = tid; x < N * F * PP; x += C::NT) {
+          const int kf = x / PP, j = x - kf * PP;
+          yb[(kf / F) * C::YLS + (kf % F) * C::YFS + ((j < U * PV) ? (j / PV) * C::YUS + V + j % PV : U * C::YUS + j - U * PV)] = 0.0;
+        }
+      }
+      // the perimeter items again, column by column (s_perm: slot columns after the tile-owned ones), so
+      // that 4 lanes write one 128-byte run of partial rows
+      for (int qi = nown * N + tid; qi < FI_; qi += C::NT) {
+        const int uv = s_perm[qi / N], k = qi % N;
+        const int4 ct = s_ct[uv];
+        double* o = A.part + ((int64_t)s_code[uv] * A.n_z + l * N + k) * F;
+        st_v2(o, csum(ct, s_s + 0 * C::SP + k), csum(ct, s_s + 1 * C::SP + k));
+        st_v2(o + 2, csum(ct, s_s + 2 * C::SP + k), csum(ct, s_s + 3 * C::SP + k));
+      }
+      if (l == nlay - 1) {        // top level of the columns -> level 0 of block nlay
+        double* yt = yb + C::YBLK;
+        for (int uv = tid; uv < UV; uv += C::NT) {
+          const int u = uv / V, v = uv % V;
+          const int4 ct = s_ct[uv];
+          const int cd = s_code[uv];
+          const double m = (cd < 0) ? A.scale * __ldg(Mt_t + (int64_t)l * C::MTS + uv * n + N) : 1.0;
+          hv::Vec<F> val;
+#pragma unroll
+          for (int p = 0; p < F; ++p) {
+            val.v[p] = m * csum(ct, s_s + p * C::SP + N);
+            yt[p * C::YFS + u * C::YUS + v] = val.v[p];
+          }
+          if (cd >= 0) {
+            double* o = A.part + ((int64_t)cd * A.n_z + l * N + N) * F;
+            st_v2(o, val.v[0], val.v[1]);
+            st_v2(o + 2, val.v[2], val.v[3]);
+          }
+        }
+        // the top block holds level 0 only: its padding, and levels 1..N-1 left unwritten (never read)
+        constexpr int PV = C::YUS - V, PT = C::YFS - U * C::YUS, PP = U * PV + PT;
+        for (int x = tid; x < F * PP; x += C::NT) {
+          const int ff = x / PP, j = x - ff * PP;
+          yt[ff * C::YFS + ((j < U * PV) ? (j / PV) * C::YUS + V + j % PV : U * C::YUS + j - U * PV)] = 0.0;
+        }
+      }
+    } else if (!(AB & 1)) {
 #pragma unroll
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
@@ -643,7 +852,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF>::NT, MB) lap
         }
       }
     }
-    if (l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
+    if (IO != 2 && l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
     // the next step's barrier (a) orders these reads before the scratch is rewritten
   }
 }
@@ -688,10 +897,10 @@ inline int output_mode(const TileArgs& A, int F) {
   return 0;
 }
 
-template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0>
+template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
 int run_plane_om(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
-  using C = PlaneCfg<n, TX, TY, F, WV, H, WF>;
-  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF, OM>;
+  using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
+  auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF, OM, IO>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   if (A.tile1 <= A.tile0) return HV_OK;
   kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
@@ -751,6 +960,18 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
       }
     }
 #endif
+    if constexpr (n == 5 && TX == 2 && TY == 2 && F == 4) {   // tile-ordered intermediate passes
+      if (A.io == 1 || A.io == 2) {
+        const bool w = A.io == 1;
+        if (A.wform == 1) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 1>(A, Dt, st)
+                                   : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 2>(A, Dt, st);
+        if (A.wform == 2) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 1>(A, Dt, st)
+                                   : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 2>(A, Dt, st);
+        return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 1>(A, Dt, st)
+                 : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 2>(A, Dt, st);
+      }
+    }
+    if (A.io) HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no tile-ordered mode for this shape");
     if (A.wform == 1) {
 #ifdef HV_PLANE_ABLATE
       const char* v = getenv("HV_PLANE_VARIANT");
@@ -796,6 +1017,17 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
   HV_PLANE_CASE(4)
 #undef HV_PLANE_CASE
   HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no instantiation for N=%d F=%d", N, F);
+}
+
+bool plane_yt_layout(int N, int TX, int TY, int F, int64_t* lay) {
+  if (N != 4 || TX != 2 || TY != 2 || F != 4) return false;
+  using C = PlaneCfg<5, 2, 2, 4, 0, 1, 1, 1>;
+  lay[0] = C::YLS;
+  lay[1] = C::YUS;
+  lay[2] = C::YFS;
+  lay[3] = C::YBLK;
+  lay[4] = C::NPER;
+  return true;
 }
 
 int plane_metric_row(int N, int TX, int TY) {

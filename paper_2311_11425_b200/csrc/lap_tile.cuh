@@ -38,11 +38,21 @@ struct TileArgs {
   int wform;                // Wt form (plane kernel): 0 = 6 components, 1 = axis form u (W = kh|u|^2 I + kd u u^T)
   double kh, kd;
   const double* Ms;         // (nslot, n_z) Minv in slot order (coalesced in slot_fixup), or nullptr
+  // tile-ordered intermediate (plane kernel, hv_lap_plan::d_yt): io 1 = the pass writes its result
+  // into the block chain at out (tile-owned nodes) and the perimeter nodes' raw partial sums into
+  // their partial rows, whose fix-up writes the compact slot rows sv; io 2 = the pass reads its
+  // input from the block chain at q and the slot rows sv by bulk copies; 0 = (nglobal, ld) rows
+  int io;
+  const int32_t* tper;      // (ntiles, NPER + 96) per tile: [stage position] u*YUS + v of its slot columns
+                            // (in slot order), then 32 runs of consecutive slots (first slot, count, position)
+  double* sv;               // final values of the slot column nodes: [nslot][F] (z = 0), then per layer
+                            // block lb: [nslot][N][F] (z = lb*N + 1 + kk)
 };
 
 bool tile_supported(int N, int TX, int TY, int F);
 int slot_pack(const TileArgs& A, int F, cudaStream_t st);
 int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
+bool plane_yt_layout(int N, int TX, int TY, int F, int64_t* lay);
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int plane_pack(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,

@@ -87,6 +87,47 @@ class EulerOps:
         cols = d["col_gid"][d["slot_col"].long()].long()
         return self.mass.d_Minv[cols].contiguous()
 
+    def _yt_chain(self, tp, d):
+        """(tper, yt, sv) for H_nu's tile-ordered intermediate (hv_lap_plan.d_yt), or
+        None when the plane kernel has no tile-ordered mode for this plan (or HV_YT=0)."""
+        if os.environ.get("HV_YT", "1") == "0":
+            return None
+        lay = np.zeros(5, dtype=np.int64)
+        if _lib.lib().hv_plane_yt_layout(tp.N, tp.TX, tp.TY, 4, lay.ctypes.data) != 0:
+            return None
+        torch = torch_mod()
+        blk, nper = int(lay[3]), int(lay[4])
+        U, V = tp.U, tp.V
+        # perimeter column p -> (u, v), the order of hv_plane_yt_layout
+        pu = [0] * V + [U - 1] * V + list(range(1, U - 1)) * 2
+        pv = list(range(V)) * 2 + [0] * (U - 2) + [V - 1] * (U - 2)
+        assert len(pu) == nper
+        rows = tp.code[:, pu, pv]                                             # (ntiles, NPER) partial row or -1
+        slot = np.searchsorted(tp.slot_row0, np.maximum(rows, 0), side="right") - 1
+        slot = np.where(rows >= 0, slot, -1)
+        yus = int(lay[1])
+        off = np.asarray(pu) * yus + np.asarray(pv)
+        # per tile: its slot columns in slot order (the stage), runs of consecutive slots (one bulk copy each)
+        tper = np.full((tp.ntiles, nper + 96), -1, dtype=np.int32)
+        tper[:, nper:] = 0
+        for t in range(tp.ntiles):
+            m = slot[t] >= 0
+            order = np.argsort(slot[t][m], kind="stable")
+            s_sorted = slot[t][m][order]
+            tper[t, :len(s_sorted)] = off[m][order]
+            if len(s_sorted):
+                brk = np.nonzero(np.diff(s_sorted) != 1)[0] + 1
+                starts = np.concatenate([[0], brk])
+                cnts = np.diff(np.concatenate([starts, [len(s_sorted)]]))
+                if len(starts) > 32:
+                    return None
+                tper[t, nper:nper + 3 * len(starts):3] = s_sorted[starts]
+                tper[t, nper + 1:nper + 3 * len(starts):3] = cnts
+                tper[t, nper + 2:nper + 3 * len(starts):3] = starts
+        yt = torch.zeros(tp.ntiles * (tp.nlay + 1) * blk, dtype=torch.float64, device="cuda")
+        sv = torch.zeros(max(1, tp.nslot) * tp.n_z * 4, dtype=torch.float64, device="cuda")
+        return to_dev(tper), yt, sv
+
     def lap_plan(self, viscous):
         """hv_lap_plan for this (viscous metric, operator set) pair."""
         key = id(viscous)
@@ -156,6 +197,10 @@ class EulerOps:
                 Ms = self._slot_minv(d)
                 p.d_Ms = _lib.ptr(Ms)
                 keep += [Wt, Mt, Ms]
+                yt = self._yt_chain(tp, d) if layout == 1 and not self.ext_cols else None
+                if yt is not None:
+                    p.d_tper, p.d_yt, p.d_sv = (x.data_ptr() for x in yt)
+                    keep += list(yt)
                 if self.ext_cols:
                     face = self.ext_face
                     p.d_slot_ext, p.d_ext_slots = d["slot_ext"].data_ptr(), d["ext_slots"].data_ptr()

@@ -33,7 +33,7 @@ def test_ctypes_signatures_cover_header():
 
 
 def test_abi_version():
-    assert _lib.lib().hv_abi_version() == _lib.ABI_VERSION == 5
+    assert _lib.lib().hv_abi_version() == _lib.ABI_VERSION == 6
 
 
 def test_sm100a_cubin_only():

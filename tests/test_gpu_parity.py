@@ -212,6 +212,37 @@ def test_axis_form_matches_six_components(pair, monkeypatch):
         assert rel_l2(la, lb) <= xtol(p)
 
 
+def test_tile_ordered_intermediate_bitwise(pair, monkeypatch):
+    """H_nu alpha=2 through the tile-ordered intermediate (pass 1 writes L q in the sweep's block
+    layout, the fix-up completes the perimeter nodes in place, pass 2 bulk-copies the blocks) is
+    bitwise the (nglobal, 4) path: same sums in the same order, only the storage differs."""
+    name, p, o = pair
+    from paper_2311_11425_b200 import euler, hyperdiff, state
+
+    plan = p.ops.lap_plan(p.vm)
+    if not plan.d_yt:
+        pytest.skip("no tile-ordered mode for this plan (N != 4 or not the plane kernel)")
+    monkeypatch.setenv("HV_YT", "0")
+    ops0 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+    assert not ops0.lap_plan(p.vm).d_yt
+    cfg2 = hyperdiff.HyperDiffConfig(**{**p.c["hd"], "alpha": 2})
+    st = state.StateField("2C", o.state)
+    a = hyperdiff.hyperdiffusion_apply(st, cfg2, p.vm, p.ops)
+    b = hyperdiff.hyperdiffusion_apply(st, cfg2, p.vm, ops0)
+    assert np.array_equal(a, b)
+    if p.cfg.alpha == 2:
+        assert rel_l2(a, o.hyper()) <= TOL
+    # accumulate into an existing output, device-resident
+    import torch
+
+    qd = torch.from_numpy(o.state).cuda()
+    base = torch.randn_like(qd)
+    oa, ob = base.clone(), base.clone()
+    hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg2, p.vm, p.ops, out=oa, accumulate=True)
+    hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg2, p.vm, ops0, out=ob, accumulate=True)
+    assert torch.equal(oa, ob)
+
+
 def test_all_five_fields_one_pass(pair):
     """F=5 tile kernel (config 1 applies L to all five fields)."""
     name, p, o = pair
