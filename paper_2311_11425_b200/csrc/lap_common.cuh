@@ -25,6 +25,64 @@ inline void fill_dtab(DTab<n>& t, const double* Drow) {
     for (int a = 0; a < n; ++a) t.D[i][a] = Drow[i * n + a];
 }
 
+// D plus its even-odd form and that of -D^T (the plane kernel's line contractions, lap_plane.cu).
+// The LGL derivative matrix is centro-antisymmetric (A[N-i][N-a] = -A[i][a] for A = D and A = -D^T),
+// so y = A x follows from the top rows only: with xd_a = x_a - x_{N-a}, xs_a = x_a + x_{N-a} (a < M = n/2),
+//   e_i = sum_a ce[i][a] xd_a,  o_i = sum_a co[i][a] xs_a + cm[i] x_M (n odd),
+//   y_i = e_i + o_i,  y_{N-i} = e_i - o_i  (i < M),  y_M = sum_a ce[M][a] xd_a  (n odd),
+// ce = (A[i][a] - A[i][N-a]) / 2, co = (A[i][a] + A[i][N-a]) / 2, cm = A[i][M]: n^2 - n + (n odd) line
+// FMAs + adds instead of n^2 (20 instead of 25 at n = 5).  Index 0: A = D, index 1: A = -D^T.
+template <int n>
+struct DTabEO : DTab<n> {
+  double ce[2][(n + 1) / 2][n / 2 > 0 ? n / 2 : 1], co[2][n / 2 > 0 ? n / 2 : 1][n / 2 > 0 ? n / 2 : 1],
+      cm[2][n / 2 > 0 ? n / 2 : 1];
+};
+
+template <int n>
+inline void fill_dtab_eo(DTabEO<n>& t, const double* Drow) {
+  fill_dtab<n>(t, Drow);
+  constexpr int N = n - 1, M = n / 2;
+  for (int w = 0; w < 2; ++w) {
+    auto A = [&](int i, int a) { return w == 0 ? Drow[i * n + a] : -Drow[a * n + i]; };
+    for (int i = 0; i < (n + 1) / 2; ++i)
+      for (int a = 0; a < M; ++a) {
+        t.ce[w][i][a] = 0.5 * (A(i, a) - A(i, N - a));
+        if (i < M) t.co[w][i][a] = 0.5 * (A(i, a) + A(i, N - a));
+      }
+    for (int i = 0; i < M; ++i) t.cm[w][i] = (n % 2) ? A(i, M) : 0.0;
+  }
+}
+
+// y = A x with A = D (W = 0) or -D^T (W = 1), even-odd form (DTabEO)
+template <int n, int W>
+__device__ __forceinline__ void eo_mv(const DTabEO<n>& Dt, const double (&x)[n], double (&y)[n]) {
+  constexpr int N = n - 1, M = n / 2;
+  double xd[M], xs[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) {
+    xd[a] = x[a] - x[N - a];
+    xs[a] = x[a] + x[N - a];
+  }
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double e = Dt.ce[W][i][0] * xd[0], o = Dt.co[W][i][0] * xs[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) {
+      e = fma(Dt.ce[W][i][a], xd[a], e);
+      o = fma(Dt.co[W][i][a], xs[a], o);
+    }
+    if constexpr (n % 2 == 1) o = fma(Dt.cm[W][i], x[M], o);
+    y[i] = e + o;
+    y[N - i] = e - o;
+  }
+  if constexpr (n % 2 == 1) {
+    double e = Dt.ce[W][M][0] * xd[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) e = fma(Dt.ce[W][M][a], xd[a], e);
+    y[M] = e;
+  }
+}
+
 // Up to five (state column) indices.
 struct FieldMap {
   int f[5];

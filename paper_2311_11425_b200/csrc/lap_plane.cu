@@ -168,9 +168,12 @@ struct PlaneCfg {
 // perimeter nodes other tiles share: slot_fixup_yt completes them in place); 2 = q read from the
 // tile-ordered intermediate at A.q, one bulk copy per tile-layer block into a two-slot ring
 template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
-__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTab<n> Dt, TileArgs A) {
+__global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTabEO<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
   static_assert(IO == 0 || (H == 1 && F == 4 && AB == 0), "tile-ordered intermediate: H = 1, 4 fields");
+  // whole planes (H = 1): line contractions in the even-odd form (DTabEO); step d then stores -D^T
+  // sums and step e adds them
+  constexpr bool EO = (H == 1);
   constexpr int N = C::N, U = C::U, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                                    // [F][QP] gathered q of the current layer
@@ -467,12 +470,16 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         double ql[n];
 #pragma unroll
         for (int k = 0; k < n; ++k) ql[k] = qrd(sq_lo, sq_hi, px * N + I0 + r, py * N + jp, k);
+        if constexpr (EO) {
+          hv::eo_mv<n, 0>(Dt, ql, p2[r]);
+        } else {
 #pragma unroll
-        for (int k = 0; k < n; ++k) {
-          double s = 0.0;
+          for (int k = 0; k < n; ++k) {
+            double s = 0.0;
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[k][a], ql[a], s);
-          p2[r][k] = s;
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[k][a], ql[a], s);
+            p2[r][k] = s;
+          }
         }
 #pragma unroll
         for (int k = 0; k < n; ++k) p0[r][k] = ql[k];   // q plane, xi-differentiated below
@@ -480,16 +487,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         if constexpr (H == 1) {
-          double ql[n];
+          double ql[n], yl[n];
 #pragma unroll
           for (int i = 0; i < n; ++i) ql[i] = p0[i][k];
+          hv::eo_mv<n, 0>(Dt, ql, yl);
 #pragma unroll
-          for (int i = 0; i < n; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < n; ++a) s = fma(Dt.D[i][a], ql[a], s);
-            p0[i][k] = s;
-          }
+          for (int i = 0; i < n; ++i) p0[i][k] = yl[i];
         } else {
           // own rows, then the other H - 1 blocks of the xi line from the shuffle partners
           double co[NR], cp[H - 1][NR];
@@ -523,12 +526,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         double ql[n];
 #pragma unroll
         for (int a = 0; a < n; ++a) ql[a] = qrd(sq_lo, sq_hi, px * N + li, py * N + a, k);
+        if constexpr (EO) {
+          double yl[n];
+          hv::eo_mv<n, 0>(Dt, ql, yl);
 #pragma unroll
-        for (int a2 = 0; a2 < n; ++a2) {
-          double s = 0.0;
+          for (int a2 = 0; a2 < n; ++a2) s_s[sidx(e, li, a2, k)] = yl[a2];
+        } else {
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], ql[a], s);
-          s_s[sidx(e, li, a2, k)] = s;
+          for (int a2 = 0; a2 < n; ++a2) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], ql[a], s);
+            s_s[sidx(e, li, a2, k)] = s;
+          }
         }
       }
     }
@@ -643,16 +653,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
       for (int k = 0; k < n; ++k) {
         if constexpr (H == 1) {
-          double c[n];
+          double c[n], yl[n];
 #pragma unroll
           for (int a = 0; a < n; ++a) c[a] = p0[a][k];
+          hv::eo_mv<n, 1>(Dt, c, yl);
 #pragma unroll
-          for (int i = 0; i < n; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < n; ++a) s = fma(Dt.D[a][i], c[a], s);
-            p0[i][k] = -s;
-          }
+          for (int i = 0; i < n; ++i) p0[i][k] = yl[i];
         } else {
           double co[NR], cp[H - 1][NR];
 #pragma unroll
@@ -678,14 +684,22 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       }
       // weak zeta (rows of p2) accumulated into p0
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
+      for (int r = 0; r < NR; ++r) {
+        if constexpr (EO) {
+          double yl[n];
+          hv::eo_mv<n, 1>(Dt, p2[r], yl);
 #pragma unroll
-        for (int k = 0; k < n; ++k) {
-          double s = 0.0;
+          for (int k = 0; k < n; ++k) p0[r][k] += yl[k];
+        } else {
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], p2[r][a], s);
-          p0[r][k] -= s;
+          for (int k = 0; k < n; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[a][k], p2[r][a], s);
+            p0[r][k] -= s;
+          }
         }
+      }
     }
     __syncthreads();
     if (WV == 0 && tid == 0 && l + 1 < nlay) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
@@ -700,12 +714,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         double ql[n];
 #pragma unroll
         for (int a = 0; a < n; ++a) ql[a] = s_s[sidx(e, li, a, k)];
+        if constexpr (EO) {   // -D^T: step e adds
+          double yl[n];
+          hv::eo_mv<n, 1>(Dt, ql, yl);
 #pragma unroll
-        for (int a2 = 0; a2 < n; ++a2) {
-          double s = 0.0;
+          for (int a2 = 0; a2 < n; ++a2) s_s[sidx(e, li, a2, k)] = yl[a2];
+        } else {
 #pragma unroll
-          for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], ql[a], s);
-          s_s[sidx(e, li, a2, k)] = s;
+          for (int a2 = 0; a2 < n; ++a2) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < n; ++a) s = fma(Dt.D[a][a2], ql[a], s);
+            s_s[sidx(e, li, a2, k)] = s;
+          }
         }
       }
     }
@@ -739,7 +760,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       for (int r = 0; r < NR; ++r) {
         const int i = I0 + r;
 #pragma unroll
-        for (int k = 0; k < n; ++k) p0[r][k] -= s_s[sidx(e, i, jp, k)];
+        for (int k = 0; k < n; ++k) p0[r][k] = EO ? p0[r][k] + s_s[sidx(e, i, jp, k)] : p0[r][k] - s_s[sidx(e, i, jp, k)];
         p0[r][0] += carry[r];
         carry[r] = p0[r][N];
 #pragma unroll
@@ -898,7 +919,7 @@ inline int output_mode(const TileArgs& A, int F) {
 }
 
 template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
-int run_plane_om(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
+int run_plane_om(const TileArgs& A, const hv::DTabEO<n>& Dt, cudaStream_t st) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
   auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF, OM, IO>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -909,7 +930,7 @@ int run_plane_om(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
 }
 
 template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0>
-int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
+int run_plane_v(const TileArgs& A, const hv::DTabEO<n>& Dt, cudaStream_t st) {
   // N = 7 hot passes (c4: 6.17 -> 6.02 ms); at N = 4 the specialised code measured slower
   // (c5 sweep 1.76 -> 1.90 ms, scheduling), so N <= 4 keeps the runtime checks
   if constexpr (F == 4 && n == 8 && AB == 0) {
@@ -926,8 +947,8 @@ int run_plane_v(const TileArgs& A, const hv::DTab<n>& Dt, cudaStream_t st) {
 // of single steps; tools_time_plane.py).
 template <int n, int TX, int TY, int F>
 int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
-  hv::DTab<n> Dt;
-  hv::fill_dtab(Dt, Drow);
+  hv::DTabEO<n> Dt;
+  hv::fill_dtab_eo(Dt, Drow);
   if constexpr (n == 8) {
     const char* hs = getenv("HV_N7_SPLIT");
     if (A.wform == 1) {
