@@ -171,9 +171,9 @@ template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, i
 __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTabEO<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
   static_assert(IO == 0 || (H == 1 && F == 4 && AB == 0), "tile-ordered intermediate: H = 1, 4 fields");
-  // whole planes (H = 1): line contractions in the even-odd form (DTabEO); step d then stores -D^T
-  // sums and step e adds them
-  constexpr bool EO = (H == 1);
+  // line contractions held whole in a thread's registers (zeta, eta; xi too for whole planes, H = 1)
+  // in the even-odd form (DTabEO); step d then stores -D^T sums and step e adds them
+  constexpr bool EO = true;
   constexpr int N = C::N, U = C::U, V = C::V, NE = C::NE, UV = C::UV, PN = C::PN, PF = C::PF, NR = C::NR, NK = C::NK;
   extern __shared__ __align__(16) double sm[];
   double* s_q = sm;                                    // [F][QP] gathered q of the current layer

@@ -26,10 +26,11 @@ TOL = 1e-12
 
 def xtol(p):
     """Agreement bar between two of OUR kernel paths (different summation orders).  1e-14, except
-    at config 4's element geometry (kind "window": 156 x 156 x 625 m elements, N = 7), where a
-    reordering of the same sums moves H_nu by ~5e-14 (kernel-internal re-ordering
+    for config 4's stratified bubble state (state "bubble", N = 7: the c4 window and box_n7), where
+    a reordering of the same sums -- e.g. the plane kernel's even-odd line contractions against the
+    element kernel's plain ones -- moves H_nu by 1-5e-14 (kernel-internal re-ordering
     1.2-1.6e-13 on c4-like elements); parity with the reference stays at TOL."""
-    return 2e-13 if p.c["kind"] == "window" else 1e-14
+    return 2e-13 if (p.c["kind"] == "window" or p.c.get("state") == "bubble") else 1e-14
 
 
 @pytest.fixture(scope="module", params=list(CASES))
