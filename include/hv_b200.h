@@ -175,6 +175,10 @@ typedef struct hv_lap_plan {
   const int32_t* d_tper;       /* (ntiles, NPER + 96): per tile the level offsets u*YUS + v of its slot
                                 * columns in slot order, then 32 runs (first slot, count, position)   */
   double* d_yt;                /* (ntiles, nlay + 1, block) doubles (hv_plane_yt_layout)             */
+  const int32_t* d_tchunk;     /* (ntiles, U*V + 1 + 128) or NULL: per tile the row-buffer row of each
+                                * column's level 1, the number of runs, then 32 x (gid at layer 1, gid
+                                * stride per layer, rows, row) -- pass 1 then bulk-copies its input's
+                                * (nglobal, 5) rows (lattice-numbered meshes, tiles.build_chunk_table) */
   double* d_sv;                /* (nslot * n_z * 4) final values of the slot column nodes: [nslot][4]
                                 * for z = 0, then per layer lb [nslot][N][4] for z = lb*N + 1 + kk   */
 } hv_lap_plan;
@@ -220,6 +224,9 @@ int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform);
  * 0 or V-1) for r = p - 2V (U = TX*N+1, V = TY*N+1).  Returns 0, or -1 when the plane kernel has
  * no tile-ordered mode for (N, TX, TY, F). */
 int hv_plane_yt_layout(int N, int TX, int TY, int F, int64_t* out);
+/* Row-buffer capacity (rows) of the plane kernel's bulk-copied pass-1 input (d_tchunk), -1 when the
+ * plane kernel has no such mode for (N, TX, TY). */
+int hv_plane_chunk_rows(int N, int TX, int TY);
 
 /* y = scale * Minv * DSS(sum_m weak_m(W_mn d_n q)) on nf fields.
  * Input field f is d_q[g*ldq + h_qf[f]], output d_out[g*ldo + h_of[f]].

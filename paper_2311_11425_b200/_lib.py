@@ -71,6 +71,7 @@ class LapPlan(C.Structure):
         ("d_Ms", _P),
         ("d_tper", _P),
         ("d_yt", _P),
+        ("d_tchunk", _P),
         ("d_sv", _P),
     ]
 
@@ -98,6 +99,7 @@ _SIGS = {
     "hv_viscous_axis": (C.c_int, [C.c_int, _P, _I64, _P, _P, _P, C.c_int, _D, _P, _P]),
     "hv_plane_metric_doubles": (_I64, [C.c_int, C.c_int, C.c_int, C.c_int]),
     "hv_plane_yt_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    "hv_plane_chunk_rows": (C.c_int, [C.c_int, C.c_int, C.c_int]),
     "hv_tile_pack_metric": (C.c_int, [C.c_int, C.c_int, C.c_int, _I64, C.c_int, _P, _P, _I64, C.c_int, _P, _P]),
     "hv_lap_local": (C.c_int, [C.POINTER(LapPlan), _P, _I64, C.c_int, _P, _P, _I64, _P, _D, C.c_uint32, C.c_int,
                                _P]),

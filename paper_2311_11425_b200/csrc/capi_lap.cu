@@ -37,7 +37,7 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
   A.wform = P->wform; A.kh = P->kh; A.kd = P->kd; A.Ms = P->d_Ms;
-  A.io = 0; A.tper = P->d_tper; A.sv = P->d_sv;
+  A.io = 0; A.tper = P->d_tper; A.sv = P->d_sv; A.tchunk = P->d_tchunk; A.ng = P->nglobal;
   return A;
 }
 
@@ -131,6 +131,8 @@ extern "C" int64_t hv_plane_metric_doubles(int N, int TX, int TY, int wform) {
   if (N < 1 || N > 7 || TX < 1 || TY < 1 || wform < 0 || wform > 2) return -1;
   return hv::plane_metric_doubles(N, TX, TY, wform);
 }
+
+extern "C" int hv_plane_chunk_rows(int N, int TX, int TY) { return hv::plane_chunk_rows(N, TX, TY); }
 
 extern "C" int hv_plane_yt_layout(int N, int TX, int TY, int F, int64_t* out) {
   if (!out) return -1;
@@ -233,7 +235,8 @@ int hyperdiffusion(const hv_lap_plan* P, const double* d_q, int64_t ldq, int nva
     // pass 1: q -> tile-ordered y blocks + perimeter partial rows, whose fix-up writes the compact slot
     // rows; pass 2: blocks and slot rows by bulk copy -> out rows (+ the usual slot fix-up)
     hv::TileArgs A1 = tile_args(P, d_q, ldq, qf, P->d_yt, 0, yf, 1.0, 0u, 0);
-    A1.io = 1;
+    // the input by bulk copies of its gid runs when the plan has a chunk table (rows of 5 doubles)
+    A1.io = (P->d_tchunk && ldq == 5 && (reinterpret_cast<uintptr_t>(d_q) & 15) == 0) ? 3 : 1;
     if ((all || stage == 1) && (rc = hv::laplacian_plane(A1, P->N, nvar, P->D, st))) return rc;
     if ((all || stage == 2) && (rc = hv::slot_fixup(A1, nvar, st))) return rc;
     hv::TileArgs A2 = tile_args(P, P->d_yt, 0, yf, d_out, ldo, of, sign, zmask, accumulate);

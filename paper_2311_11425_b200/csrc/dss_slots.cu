@@ -163,7 +163,7 @@ int fixup_f(const TileArgs& A, cudaStream_t st) {
   const int64_t tot = A.nslot * A.n_z;
   if (tot >= (int64_t)1 << 31) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: %lld slot rows", (long long)tot);
   int row_mode = 0;
-  if (A.io == 1) {
+  if (A.io == 1 || A.io == 3) {   // pass 1 into the tile-ordered intermediate
     if (F != 4 || A.accumulate || !A.sv || A.slot_ext) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: slot rows need F = 4");
     row_mode = 3;
   } else if (F == 4 && !A.accumulate && A.out && ((uintptr_t)A.out & 15) == 0) {

@@ -137,7 +137,13 @@ struct PlaneCfg {
   // scratch | ctab (int4) | code | mbarriers (metric, IO 2 loads)
   static constexpr int QB_L0 = (N - 1) * YLS;            // IO 2: the two level-0 planes
   static constexpr int QB_S = QB_L0 + 2 * YLS;           // IO 2: perimeter stage [NPER][N][F]
-  static constexpr int SQB = IO == 2 ? QB_S + NPER * N * F : SQ;
+  // IO 3 (pass 1 with bulk-copied input, tiles.build_chunk_table): the state's (nglobal, 5) rows of
+  // levels 1..N in a row buffer (whole rows, runs of consecutive gids), level 0 in two planes laid
+  // out like a Yt level [f][u][v]
+  static constexpr int CRR = 362;                        // row-buffer rows (the table places <= 360)
+  static constexpr int QB_P = CRR * 5;                   // IO 3: the two level-0 planes
+  static constexpr int TCW = UV + 1 + 4 * 32;            // IO 3: ints per tile of TileArgs::tchunk
+  static constexpr int SQB = IO == 2 ? QB_S + NPER * N * F : (IO == 3 ? QB_P + 2 * YLS : SQ);
   static constexpr int TPW = NPER + 3 * 32;              // IO 2: ints per tile of TileArgs::tper
   static constexpr int OFF_W = (SQB + 1) & ~1;
   static constexpr int OFF_S = OFF_W + (WV == 0 ? WL : 0);
@@ -145,7 +151,7 @@ struct PlaneCfg {
   static constexpr int OFF_C = OFF_T + 2 * UV;
   static constexpr int OFF_P = OFF_C + (UV + 1) / 2;
   static constexpr int OFF_PD = OFF_P + (UV + 1) / 2;  // IO 2: [NPER] level offset of the stage's slot columns
-  static constexpr int OFF_BAR = (OFF_PD + (IO == 2 ? (NPER + 1) / 2 : 0) + 1) & ~1;
+  static constexpr int OFF_BAR = (OFF_PD + (IO == 2 ? (NPER + 1) / 2 : (IO == 3 ? (UV + 1) / 2 : 0)) + 1) & ~1;
   // split planes (H > 1): D in shared memory for the xi exchange, whose row / column offsets vary
   // across the lanes of a warp (constant-bank loads would serialise)
   static constexpr int OFF_D = OFF_BAR + 4;
@@ -170,7 +176,10 @@ struct PlaneCfg {
 template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
 __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTabEO<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
-  static_assert(IO == 0 || (H == 1 && F == 4 && AB == 0), "tile-ordered intermediate: H = 1, 4 fields");
+  static_assert(IO == 0 || (H == 1 && F == 4 && (AB == 0 || (IO == 1 && AB == 2))),
+                "tile-ordered intermediate: H = 1, 4 fields");
+  constexpr bool OUT_YT = (IO == 1 || IO == 3);   // results into the tile-ordered intermediate
+  constexpr bool GATHER = (IO == 0 || IO == 1);   // q gathered by gid every layer (IO 3: layer 0 only)
   // line contractions held whole in a thread's registers (zeta, eta; xi too for whole planes, H = 1)
   // in the even-odd form (DTabEO); step d then stores -D^T sums and step e adds them
   constexpr bool EO = true;
@@ -206,6 +215,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     qcol[p] = A.qf.f[p];
     ocol[p] = A.of.f[p];
   }
+  int myqc = qcol[0];   // the thread's field column in a q row
+#pragma unroll
+  for (int p = 1; p < F; ++p)
+    if (p == f) myqc = qcol[p];
   const bool row5 = (F == 4 && A.ldo == 5 && A.zero_mask == 1u && ocol[0] == 1 && ocol[1] == 2 && ocol[2] == 3 && ocol[3] == 4);
   auto sidx = [&](int ee, int a, int b, int c) { return f * C::SP + ee * C::ES + a * C::AS + b * C::BS + c; };
   auto tq = [&](int u, int v, int k) { return f * C::QP + u * C::US + v * C::KS + k; };
@@ -226,12 +239,18 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     for (int it = 0; it < PN; ++it) {
       const int node = tid + it * C::NT;
       if (node < C::NODES) {
-        if (g[it] < 0) {
+        if constexpr (IO == 3) {   // layer 0: level 0 -> plane 0, levels >= 1 -> their rows of the buffer
+          const int uv = node / n, k = node % n;
+          const double* src = A.q + (int64_t)g[it] * A.ldq;
+#pragma unroll
+          for (int p = 0; p < F; ++p)
+            cp_async8(k == 0 ? s_q + C::QB_P + p * C::YFS + (uv / V) * C::YUS + uv % V
+                             : s_q + (s_pdst[uv] + k - 1) * 5 + qcol[p], src + qcol[p]);
+        } else if (g[it] < 0) {
 #pragma unroll
           for (int p = 0; p < F; ++p) s_q[p * C::QP + qnode(node)] = 0.0;
         } else {
           const double* src = A.q + (int64_t)g[it] * A.ldq;
-#pragma unroll
           const int qo = qnode(node);
 #pragma unroll
           for (int p = 0; p < F; ++p) cp_async8(s_q + p * C::QP + qo, src + qcol[p]);
@@ -278,6 +297,37 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       tma_copy(s_q + C::QB_S + r_pos * nlev * F, src, (uint32_t)(r_cnt * nlev * F * 8), bar + 1);
     }
   };
+  // IO 3: lane r of warp 0 holds run r of the tile's chunk table (gid at layer 1, gid stride per
+  // layer, rows, row-buffer position); a layer l >= 1 is one bulk copy per run (16-byte aligned ends:
+  // a run starting at an odd gid moves 8 bytes before its first row too; the table keeps one spare
+  // row between runs)
+  int c_g1 = 0, c_st = 0, c_rows = 0, c_dst = 0;
+  if constexpr (IO == 3) {
+    const int32_t* tc = A.tchunk + t * C::TCW;
+    if (tid < 32 && tid < tc[UV]) {
+      c_g1 = tc[UV + 1 + 4 * tid];
+      c_st = tc[UV + 2 + 4 * tid];
+      c_rows = tc[UV + 3 + 4 * tid];
+      c_dst = tc[UV + 4 + 4 * tid];
+    }
+  }
+  int64_t c_tail = -1;   // IO 3: gid of a run's last row that a bulk copy would overrun (the end of q)
+  auto issue_chunks = [&](int l) {
+    const int64_t g = (int64_t)c_g1 + (int64_t)c_st * (l - 1);
+    const uint32_t shift = (uint32_t)(g & 1) * 8u;
+    uint32_t bytes = c_rows ? ((c_rows * 40u + shift + 15u) & ~15u) : 0u;
+    if (c_rows && g * 40 - shift + bytes > A.ng * 40) {                  // the last rows of q: the
+      bytes = ((c_rows - 1) * 40u + shift + 15u) & ~15u;                  // final row loaded at step a
+      c_tail = g + c_rows - 1;
+    }
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, bytes);
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + 1)), "r"(tot)
+                   : "memory");
+    if (bytes)
+      tma_copy(reinterpret_cast<char*>(s_q) + c_dst * 40 - shift,
+               reinterpret_cast<const char*>(A.q) + g * 40 - shift, bytes, bar + 1);
+  };
   // IO 2: stage -> level buffers (layer l: levels 1..N; prologue: level 0 -> plane 0); an item =
   // (stage position j, level kk): its F fields in two 16-byte loads, stored at the column's offset
   auto patch = [&](int l, int nper) {
@@ -302,6 +352,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     if constexpr (IO == 2) {
       const int o = f * C::YFS + u * C::YUS + v;
       return (k == 0) ? lo[o] : (k == N ? hi[o] : s_q[(k - 1) * C::YLS + o]);
+    } else if constexpr (IO == 3) {
+      return (k == 0) ? lo[f * C::YFS + u * C::YUS + v] : s_q[(s_pdst[u * V + v] + k - 1) * 5 + myqc];
     } else {
       return s_q[tq(u, v, k)];
     }
@@ -388,17 +440,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   };
 
   int gcur[PN], gnext[PN];
-  if constexpr (IO != 2) load_gids(0, gcur);
+  if constexpr (IO != 2) load_gids(0, gcur);   // IO 3: layer 0 is gathered
   if (WV == 0 && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  if (IO == 2 && tid == 0) {
+  if ((IO == 2 || IO == 3) && tid == 0) {
     mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   if constexpr (IO == 2)
     for (int j = tid; j < C::NPER; j += C::NT) s_pdst[j] = tper[j];
+  if constexpr (IO == 3)   // s_pdst: the row of level 1 of each tile column in the row buffer
+    for (int j = tid; j < UV; j += C::NT) s_pdst[j] = A.tchunk[t * C::TCW + j];
   if (WV == 1 && tid == 0) l2_prefetch(Wt_t, C::WL * 8);
   for (int uv = tid; uv < UV; uv += C::NT) {
     const int u = uv / V, v = uv % V;
@@ -411,9 +465,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     s_ct[uv] = make_int4(o[0], o[1], o[2], o[3]);
     s_code[uv] = A.code[t * UV + uv];
   }
+  if constexpr (IO == 3) __syncthreads();   // s_pdst before the layer-0 gather uses it
   if constexpr (IO != 2) {
     issue_gather(gcur);
-    if (nlay > 1) load_gids(1, gnext);
+    if (GATHER && nlay > 1) load_gids(1, gnext);
   }
   if constexpr (H > 1)
     for (int x = tid; x < n * n; x += C::NT) sD[x] = Dt.D[x / n][x % n];
@@ -436,8 +491,18 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       issue_loads(0, nper);
     }
   }
+  // IO 3: the row-buffer address of level 0 of the thread's plane rows (u = px*N + r) and eta lines
+  // (v = py*N + a) minus one row: level k >= 1 of them is at + 5 k (layer-invariant)
+  int prow[IO == 3 ? n : 1], erow[IO == 3 ? n : 1];
+  if constexpr (IO == 3) {
+#pragma unroll
+    for (int r = 0; r < n; ++r) {
+      prow[r] = (s_pdst[(px * N + r) * V + py * N + jp] - 1) * 5 + myqc;
+      erow[r] = (s_pdst[(px * N + jp) * V + py * N + r] - 1) * 5 + myqc;
+    }
+  }
   int nown = 0;   // IO 1: tile-owned columns (s_perm lists them first)
-  if constexpr (IO == 1)
+  if constexpr (OUT_YT)
     for (int uv = 0; uv < UV; ++uv) nown += (s_code[uv] < 0) ? 1 : 0;
   double carry[NR];
 #pragma unroll
@@ -451,16 +516,27 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     if constexpr (IO == 2) {   // layer l's loads (levels 1..N-1, level 0 of block l+1, perimeter rows)
       mbar_wait(bar + 1, (uint32_t)((l + 1) & 1));
       patch(l, nper);
+    } else if constexpr (IO == 3) {   // layer 0 gathered, then one bulk-copy phase per layer
+      if (l == 0) {
+        cp_async_wait_all();
+      } else {
+        mbar_wait(bar + 1, (uint32_t)((l - 1) & 1));
+        if (c_tail >= 0) {   // the row at the end of q (after the bulk copy, which ends before it)
+#pragma unroll
+          for (int ff = 0; ff < 5; ++ff) s_q[(c_dst + c_rows - 1) * 5 + ff] = A.q[c_tail * 5 + ff];
+          c_tail = -1;
+        }
+      }
     } else {
       cp_async_wait_all();
     }
     __syncthreads();
-    const double* sq_lo = s_q + C::QB_L0 + (l & 1) * C::YLS;
-    const double* sq_hi = s_q + C::QB_L0 + ((l + 1) & 1) * C::YLS;
+    const double* sq_lo = s_q + (IO == 3 ? C::QB_P : C::QB_L0) + (l & 1) * C::YLS;
+    const double* sq_hi = s_q + (IO == 3 ? C::QB_P : C::QB_L0) + ((l + 1) & 1) * C::YLS;
     if (WV == 1 && tid == 0 && l + 1 < nlay) l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
     if (tid == C::NT - 1 && l + 1 < nlay) {   // output-item gid / Minv of the next layer -> L2
       l2_prefetch(Mt_t + (int64_t)(l + 1) * C::MTS, C::MTS * 8);
-      if (IO != 1) l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
+      if (!OUT_YT) l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
     }
     // ---- b: plane derivatives in registers, eta lines (i = jp) strong
     double p0[NR][n], p2[NR][n];   // [row][k]: dq_xi, dq_zeta -> f_xi, f_zeta -> accumulator
@@ -469,7 +545,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       for (int r = 0; r < NR; ++r) {
         double ql[n];
 #pragma unroll
-        for (int k = 0; k < n; ++k) ql[k] = qrd(sq_lo, sq_hi, px * N + I0 + r, py * N + jp, k);
+        for (int k = 0; k < n; ++k)
+          ql[k] = (IO == 3 && k > 0) ? s_q[prow[IO == 3 ? r : 0] + 5 * k] : qrd(sq_lo, sq_hi, px * N + I0 + r, py * N + jp, k);
         if constexpr (EO) {
           hv::eo_mv<n, 0>(Dt, ql, p2[r]);
         } else {
@@ -525,7 +602,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         const int li = (H == 1) ? jp : I0 + kk, k = (H == 1) ? K0 + kk : jp;
         double ql[n];
 #pragma unroll
-        for (int a = 0; a < n; ++a) ql[a] = qrd(sq_lo, sq_hi, px * N + li, py * N + a, k);
+        for (int a = 0; a < n; ++a)
+          ql[a] = (IO == 3 && k > 0) ? s_q[erow[IO == 3 ? a : 0] + 5 * k] : qrd(sq_lo, sq_hi, px * N + li, py * N + a, k);
         if constexpr (EO) {
           double yl[n];
           hv::eo_mv<n, 0>(Dt, ql, yl);
@@ -542,13 +620,30 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         }
       }
     }
+    if constexpr (IO == 3) {
+      // level N of layer l is level 0 of layer l + 1: row buffer -> plane (l+1)&1 before the buffer is
+      // refilled (a thread's items all have its own field: NT is a multiple of F)
+      static_assert(IO != 3 || C::NT % F == 0, "IO 3: plane copy items keep the thread's field");
+      if (l + 1 < nlay) {
+        double* pn = s_q + C::QB_P + ((l + 1) & 1) * C::YLS;
+        for (int x = tid; x < UV * F; x += C::NT) {
+          const int uv = x / F;
+          pn[f * C::YFS + (uv / V) * C::YUS + uv % V] = s_q[(s_pdst[uv] + N - 1) * 5 + myqc];
+        }
+      }
+    }
     __syncthreads();
     // s_q of layer l is dead: gather q(l+1) (IO 2: the loads of layer l + 1; plane l&1 takes level 0 of
-    // block l + 2, the level buffer and the stage the rest)
+    // block l + 2, the level buffer and the stage the rest; IO 3: the row buffer takes layer l + 1)
     if constexpr (IO == 2) {
       if (tid < 32 && l + 1 < nlay) {
         fence_proxy_async();
         issue_loads(l + 1, nper);
+      }
+    } else if constexpr (IO == 3) {
+      if (tid < 32 && l + 1 < nlay) {
+        fence_proxy_async();
+        issue_chunks(l + 1);
       }
     } else {
       if (l + 1 < nlay) issue_gather(gnext);
@@ -736,7 +831,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     double mf[PF];
     double my[C::PFY];   // IO 1: scale * Minv of tile-owned block items, 1 for perimeter (raw partial sums)
     constexpr int FI_ = C::FI;
-    if constexpr (IO == 1) {
+    if constexpr (OUT_YT) {
 #pragma unroll
       for (int it = 0; it < C::PFY; ++it) {
         const int qi = tid + it * C::NT;
@@ -776,7 +871,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     // ---- f: node owners (items (column, k < N); k = N only on the top layer) sum the
     // element copies of all F fields (predicated loads, fixed order (c0 + c1) + (c2 + c3)),
     // then one row store per item
-    if constexpr (IO == 1) {
+    if constexpr (OUT_YT) {
       // block items in (k, u, v) order: consecutive lanes store consecutive v.  Perimeter (slot) items:
       // raw partial sums into their partial rows (the fix-up sums them into the compact slot rows that
       // pass 2 stages); their block entries are never read, the raw sums keep the block's sectors whole
@@ -873,7 +968,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         }
       }
     }
-    if (IO != 2 && l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
+    if (GATHER && l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
     // the next step's barrier (a) orders these reads before the scratch is rewritten
   }
 }
@@ -982,8 +1077,19 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
     }
 #endif
     if constexpr (n == 5 && TX == 2 && TY == 2 && F == 4) {   // tile-ordered intermediate passes
+      if (A.io == 3) {
+        if (A.wform == 1) return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 3>(A, Dt, st);
+        if (A.wform == 2) return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 3>(A, Dt, st);
+        return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 3>(A, Dt, st);
+      }
       if (A.io == 1 || A.io == 2) {
         const bool w = A.io == 1;
+#ifdef HV_PLANE_ABLATE
+        {
+          const char* v = getenv("HV_PLANE_VARIANT");   // 42: pass 1 without the q gather (timing only)
+          if (w && A.wform == 1 && v && atoi(v) == 42) return run_plane_om<n, TX, TY, F, 0, 3, 2, 1, 1, 0, 1>(A, Dt, st);
+        }
+#endif
         if (A.wform == 1) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 1>(A, Dt, st)
                                    : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 2>(A, Dt, st);
         if (A.wform == 2) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 1>(A, Dt, st)
@@ -1038,6 +1144,11 @@ int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStr
   HV_PLANE_CASE(4)
 #undef HV_PLANE_CASE
   HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no instantiation for N=%d F=%d", N, F);
+}
+
+int plane_chunk_rows(int N, int TX, int TY) {
+  if (N != 4 || TX != 2 || TY != 2) return -1;
+  return PlaneCfg<5, 2, 2, 4, 0, 1, 1, 3>::CRR - 2;
 }
 
 bool plane_yt_layout(int N, int TX, int TY, int F, int64_t* lay) {

@@ -45,6 +45,8 @@ struct TileArgs {
   int io;
   const int32_t* tper;      // (ntiles, NPER + 96) per tile: [stage position] u*YUS + v of its slot columns
                             // (in slot order), then 32 runs of consecutive slots (first slot, count, position)
+  const int32_t* tchunk;    // (ntiles, U*V + 1 + 128) bulk-copy runs of a tile's q input (io 3, tiles.py)
+  int64_t ng;               // rows of q (io 3: no bulk copy reads past row ng - 1)
   double* sv;               // final values of the slot column nodes: [nslot][F] (z = 0), then per layer
                             // block lb: [nslot][N][F] (z = lb*N + 1 + kk)
 };
@@ -53,6 +55,7 @@ bool tile_supported(int N, int TX, int TY, int F);
 int slot_pack(const TileArgs& A, int F, cudaStream_t st);
 int slot_fixup(const TileArgs& A, int F, cudaStream_t st);
 bool plane_yt_layout(int N, int TX, int TY, int F, int64_t* lay);
+int plane_chunk_rows(int N, int TX, int TY);
 bool plane_supported(int N, int TX, int TY, int F);
 int laplacian_plane(const TileArgs& A, int N, int F, const double* Drow, cudaStream_t st);
 int plane_pack(int N, int TX, int TY, int64_t ntiles, int nlay, const int32_t* elem, const double* W, int64_t nloc,

@@ -16,6 +16,7 @@ import numpy as np
 from . import _lib
 from .assembly import GlobalMass, weights3
 from .device import to_dev, torch_mod
+from .tiles import build_chunk_table
 
 __all__ = ["EulerOps"]
 
@@ -201,6 +202,14 @@ class EulerOps:
                 if yt is not None:
                     p.d_tper, p.d_yt, p.d_sv = (x.data_ptr() for x in yt)
                     keep += list(yt)
+                    # pass 1's input by bulk copies of gid runs (lattice-numbered meshes; HV_CHUNK=0: gather)
+                    cap = _lib.lib().hv_plane_chunk_rows(tp.N, tp.TX, tp.TY)
+                    ct = (build_chunk_table(tp, cap) if cap > 0 and os.environ.get("HV_CHUNK", "1") != "0"
+                          else None)
+                    if ct is not None:
+                        ct = to_dev(ct)
+                        p.d_tchunk = ct.data_ptr()
+                        keep.append(ct)
                 if self.ext_cols:
                     face = self.ext_face
                     p.d_slot_ext, p.d_ext_slots = d["slot_ext"].data_ptr(), d["ext_slots"].data_ptr()

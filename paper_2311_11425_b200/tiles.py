@@ -161,3 +161,80 @@ def build_tile_plan(mesh, TX, TY, ext_cols=None, _order=None):
                     slot_col=shared_cols.astype(np.int32), slot_row0=slot_row0.astype(np.int32),
                     slot_nc=slot_nc.astype(np.int32), npart=npart, n_z=mesh.n_z,
                     tmeta=tiles[:, 3:5].astype(np.int32))
+
+
+def build_chunk_table(tp, rows_cap, row_ld=5):
+    """Bulk-copy description of a tile plan's q input (lap_plane.cu IO 3), or None.
+
+    On lattice-numbered meshes (first-appearance order over elements, local nodes (i, j, k), k
+    fastest: mesh.py:86-107) the new nodes of an element are one contiguous gid range and a tile
+    column's levels k = 1..N of a layer are consecutive gids.  For every tile this finds the runs
+    of consecutive gids that hold its levels 1..N (the same runs in every layer >= 1, each start
+    advancing by a fixed stride per layer), places them in the kernel's row buffer (AoS rows of
+    ``row_ld`` doubles; a start row with the parity of its gid so that both ends of a bulk copy are
+    16-byte aligned, one spare row between runs, the element chunks 68 rows apart so that the
+    lanes of the four elements hit different bank groups), and returns per tile
+    ``[colrow (U*V) | nruns | 32 x (gid at layer 1, stride, rows, dst row)]`` as int32.
+    Verified against ``tp.gt`` for every layer; None if any tile does not fit the model.
+    """
+    U, V, n, N, nlay = tp.U, tp.V, tp.n, tp.N, tp.nlay
+    if nlay < 2:
+        return None
+    UV = U * V
+    gt = tp.gt[:, :, :UV * n].reshape(tp.ntiles, nlay, UV, n).astype(np.int64)
+    if np.any(gt < 0):
+        return None
+    lev = gt[:, :, :, 1:]                                       # (t, l, uv, N) levels 1..N
+    # levels of a column consecutive in every layer
+    if not np.all(np.diff(lev, axis=3) == 1):
+        return None
+    width = UV + 1 + 4 * 32
+    out = np.zeros((tp.ntiles, width), dtype=np.int32)
+    col0 = lev[:, :, :, 0]                                      # (t, l, uv) gid of level 1
+    for t in range(tp.ntiles):
+        c1 = col0[t, 1]
+        order = np.argsort(c1, kind="stable")
+        s = c1[order]
+        # columns whose level-1 gids are N apart continue the same run
+        brk = np.nonzero(np.diff(s) != N)[0] + 1
+        starts = np.concatenate([[0], brk])
+        ends = np.concatenate([brk, [len(s)]])
+        if len(starts) > 32:
+            return None
+        # every layer: a run's columns keep their offsets (one stride per run)
+        runs = []
+        for a, b in zip(starts, ends):
+            cols = order[a:b]
+            ct = col0[t]                                          # (nlay, UV)
+            st = ct[1:][:, cols] - ct[1][cols][None, :]           # (nlay-1, ncols)
+            if not np.all(st == st[:, :1]):
+                return None
+            d = st[:, 0]
+            stride = int(d[1] - d[0]) if len(d) > 1 else 0
+            if not np.array_equal(d, stride * np.arange(nlay - 1)):
+                return None
+            runs.append((int(c1[cols[0]]), stride, (b - a) * N, cols))
+        # placement: big runs (element chunks) first, 68 rows apart; then the faces
+        runs.sort(key=lambda r: -r[2])
+        cur, big = 0, 0
+        colrow = np.zeros(UV, dtype=np.int64)
+        meta = []
+        for g1, stride, nrows, cols in runs:
+            if stride % 2:
+                return None                                      # parity must not change between layers
+            p = cur + (1 if cur else 0)
+            if nrows >= 4 * N * N:
+                p = max(p, 68 * big)
+                big += 1
+            if (p - g1) % 2:
+                p += 1
+            colrow[cols] = p + N * np.arange(len(cols))
+            meta.append((g1, stride, nrows, p))
+            cur = p + nrows
+        if cur + 1 > rows_cap:
+            return None
+        out[t, :UV] = colrow
+        out[t, UV] = len(meta)
+        for r, m in enumerate(meta):
+            out[t, UV + 1 + 4 * r:UV + 5 + 4 * r] = m
+    return out

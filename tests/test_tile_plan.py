@@ -96,3 +96,58 @@ def test_plan_rejects_unstructured():
     m = hm.build_box_lattice(2, 2, 2, 3, (200.0, 240.0, 100.0))
     m.hgrid = None
     assert build_tile_plan(m, 2, 2) is None
+
+
+def _chunk_model_ok(p, ct, ld=5):
+    """Every node (u, v, k >= 1) of every layer >= 1 sits where the chunk table's runs put its gid."""
+    UV, N = p.U * p.V, p.N
+    gt = p.gt[:, :, :UV * p.n].reshape(p.ntiles, p.nlay, UV, p.n)
+    for t in range(p.ntiles):
+        colrow, nr = ct[t, :UV], ct[t, UV]
+        runs = ct[t, UV + 1:UV + 1 + 4 * nr].reshape(-1, 4)
+        # runs: disjoint row ranges with a spare row between them, start row parity = gid parity
+        rr = sorted((int(p0), int(p0 + nrow)) for _, _, nrow, p0 in runs)
+        assert all(b[0] > a[1] for a, b in zip(rr, rr[1:]))
+        assert all((g1 - p0) % 2 == 0 and st % 2 == 0 for g1, st, _, p0 in runs)
+        for l in range(1, p.nlay):
+            row = np.full(rr[-1][1] + 1, -1, dtype=np.int64)
+            for g1, st, nrow, p0 in runs:
+                row[p0:p0 + nrow] = g1 + st * (l - 1) + np.arange(nrow)
+            got = row[colrow[:, None] + np.arange(N)[None, :]]
+            assert np.array_equal(got, gt[t, l, :, 1:])
+
+
+@pytest.mark.parametrize("perturb", [True, False])
+def test_chunk_table_lattice_box(perturb):
+    """Lattice-numbered boxes (configs 1, 2, 5): the bulk-copy runs of pass 1's input reproduce the
+    tile node gids of every layer >= 1 (lap_plane.cu IO 3)."""
+    from paper_2311_11425_b200.tiles import build_chunk_table
+
+    m = hm.build_box_lattice(6, 4, 3, 4, (6000.0, 4000.0, 1500.0), perturb=perturb)
+    p = build_tile_plan(m, 2, 2)
+    ct = build_chunk_table(p, 360)
+    assert ct is not None
+    _chunk_model_ok(p, ct)
+    assert ct[:, p.U * p.V].max() <= 32
+
+
+def test_chunk_table_rejects_what_it_cannot_model():
+    """Single-layer meshes and capacities below the runs: no table (the gather path runs)."""
+    from paper_2311_11425_b200.tiles import build_chunk_table
+
+    m1 = hm.build_box_lattice(4, 4, 1, 4, (4000.0, 4000.0, 500.0))
+    assert build_chunk_table(build_tile_plan(m1, 2, 2), 360) is None
+    m = hm.build_box_lattice(4, 4, 2, 4, (4000.0, 4000.0, 1000.0))
+    assert build_chunk_table(build_tile_plan(m, 2, 2), 200) is None
+
+
+def test_chunk_table_sphere_if_modelled():
+    """The cubed sphere's numbering: either modelled exactly or rejected (never a wrong table)."""
+    from paper_2311_11425_b200.tiles import build_chunk_table
+
+    m = hm.build_cubed_sphere(hm.MeshConfig("sphere", panels_per_edge=4, n_elem_vertical=3, degree=4,
+                                            radius=6.371e6, z_top=1e4))
+    p = build_tile_plan(m, 2, 2)
+    ct = build_chunk_table(p, 360)
+    if ct is not None:
+        _chunk_model_ok(p, ct)
