@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "hv_common.h"
 #include "lap_common.cuh"
@@ -339,10 +340,215 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::D
   }
 }
 
+// Column sweep of the 2C / 3C Euler RHS with line tasks (N = 7 single-column tiles; 2NC keeps
+// euler_tile_kernel).  Per layer:
+//   phase 1  thread = node: gather q, metric record, EOS, contravariant velocities -> the 15 fluxes
+//            (3 directions x [w3 F_rho, w3 F_thermo, 3 momentum]) into shared arrays; the geopotential
+//            (and Coriolis) terms of the node stay in registers
+//   phase 2  thread = (direction, flux, line): the whole line in registers, one even-odd product
+//            (-D^T for the weak rho / thermo fluxes, D for the strong momentum fluxes, DTabEO), the
+//            results back in place -- one shared load and store per node and flux instead of 8 x 7
+//            loads per node and direction in euler_tile_kernel's per-node line sums
+//   phase 3  thread = node: sum the directions, the element accumulator (euler.py:191-224), then the
+//            same on-chip DSS / carry / partial rows as euler_tile_kernel
+// Flux arrays: node (i, j, k) at i*PI + j*n + k with PI = n*n + 1, so the half-warps of phase 1 / 3 and
+// of the i- and k-direction lines hit 16 distinct banks (the j-direction lines: 2-way).
+template <int n>
+struct ElinesCfg {
+  static constexpr int nn = n * n * n, PI = n * n + 1, FS = ((n - 1) * PI + (n - 1) * n + n + 1) & ~1;
+  static constexpr int NL = n * n;                    // lines per direction and flux
+  static constexpr int OFF_C = 15 * FS;               // carry [2][n*n][5]
+  static constexpr int OFF_CF = OFF_C + 2 * n * n * 5;   // even-odd coefficients (hv::EOSmem)
+  static constexpr int OFF_CODE = OFF_CF + 2 * hv::EOSmem<n>::PER;
+  static constexpr size_t SMEM = sizeof(double) * (OFF_CODE + (n * n + 1) / 2);
+};
+
+template <int n>
+__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::DTabEO<n> Dt, EulerConsts K,
+                                                          int64_t nelem, const int32_t* __restrict__ gid,
+                                                          const double* __restrict__ w3,
+                                                          const double* __restrict__ Mt, const double* __restrict__ q,
+                                                          int64_t ldq, hv::TileArgs A,
+                                                          const int32_t* __restrict__ elem) {
+  using C = ElinesCfg<n>;
+  constexpr int nn = C::nn, N = n - 1, PI = C::PI, FS = C::FS;
+  extern __shared__ double sm[];
+  double* s_f = sm;                                      // [15][FS] fluxes, then line results
+  double* s_carry = sm + C::OFF_C;                       // [2][n*n][5]
+  int* s_code = reinterpret_cast<int*>(sm + C::OFF_CODE);
+  double* s_cf = sm + C::OFF_CF;
+  const int64_t tl = blockIdx.x;
+  const int t = threadIdx.x;
+  hv::eo_smem_fill<n>(Dt, s_cf, t, blockDim.x);   // visible after the first layer's phase-1 barrier
+  const bool act = t < nn;
+  const int i = t / (n * n), j = (t / n) % n, k = t % n;
+  const int na = i * PI + j * n + k;                     // this node's slot in a flux array
+  const int nlay = A.nlay;
+  const int64_t nloc = nelem * nn;
+  if (t < n * n) s_code[t] = A.code[tl * n * n + t];
+  const double* Mt_t = A.Mt + tl * (int64_t)nlay * (((nn + 1) & ~1));
+  const double w = act ? w3[t] : 0.0;
+  for (int l = 0; l < nlay; ++l) {
+    const int64_t e = elem[tl * nlay + l];
+    const int64_t p = e * nn + (act ? t : 0);
+    // ---- phase 1 (euler_node_acc's fluxes, reference expression order)
+    double extra[3] = {0.0, 0.0, 0.0};                   // geopotential + Coriolis terms of acc[1..3]
+    int g = 0;
+    if (act) {
+      g = gid[p];
+      double qv[5];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
+      const double Jg = Mt[9 * nloc + p];
+      const double mask = ((l == 0 && k == 0) || (l == nlay - 1 && k == n - 1)) ? 0.0 : 1.0;
+      const double rho = qv[0];
+      double P;
+      if (K.set == 1) {
+        P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+      } else {
+        const double phi = Mt[14 * nloc + p];
+        const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
+        P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);
+      }
+      const double tflux = (K.set == 1) ? qv[4] / qv[0] : (qv[4] + P) / qv[0];
+      double sg[3] = {0.0, 0.0, 0.0};
+      // one direction at a time: grad xi^m (3 doubles) live only inside its iteration
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        double gm[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gm[c] = Mt[(m * 3 + c) * nloc + p];
+        double un = (gm[0] * qv[1] + gm[1] * qv[2] + gm[2] * qv[3]) / rho;
+        if (m == 2) un = un * mask;
+        const double jun = Jg * un;
+        s_f[(m * 5 + 0) * FS + na] = w * (jun * qv[0]);
+        s_f[(m * 5 + 1) * FS + na] = w * (jun * qv[0] * tflux);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) s_f[(m * 5 + 2 + c) * FS + na] = Jg * (qv[1 + c] * un + P * gm[c]);
+        if ((K.dirs >> m) & 1) {
+          const double dphi = Mt[(10 + m) * nloc + p];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) sg[c] += dphi * gm[c];
+        }
+      }
+      const double wj = w * Jg;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) extra[c] = wj * qv[0] * sg[c];
+      if (K.omega > 0.0) {   // Coriolis 2 omega e x u (euler.py:183-188, 217-223)
+        double ev[3];
+        if (K.coriolis == 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ev[c] = Mt[(15 + c) * nloc + p];
+        } else {
+          double gz[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) gz[c] = Mt[(6 + c) * nloc + p];
+          const double zn = sqrt(gz[0] * gz[0] + gz[1] * gz[1] + gz[2] * gz[2]);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ev[c] = gz[c] / zn;
+        }
+        const double ux = qv[1], uy = qv[2], uz = qv[3];
+        const double cx = ev[1] * uz - ev[2] * uy, cy = ev[2] * ux - ev[0] * uz, cz = ev[0] * uy - ev[1] * ux;
+        extra[0] += wj * 2.0 * K.omega * cx;
+        extra[1] += wj * 2.0 * K.omega * cy;
+        extra[2] += wj * 2.0 * K.omega * cz;
+      }
+    }
+    __syncthreads();
+    // the next layer's element record (13 metric components, gids, Minv) -> L2, so that its phase-1
+    // loads wait for L2 rather than DRAM
+    if (l + 1 < nlay && t < 16) {
+      const int64_t en = elem[tl * nlay + l + 1];
+      const void* src = nullptr;
+      uint32_t bytes = nn * 8;
+      if (t < 13) src = Mt + t * nloc + en * nn;
+      else if (t == 13) { src = gid + en * nn; bytes = nn * 4; }
+      else if (t == 14) { src = Mt_t + (int64_t)(l + 1) * ((nn + 1) & ~1); bytes = ((nn + 1) & ~1) * 8; }
+      if (src && (bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
+    // ---- phase 2: line tasks (direction m, flux x, line); warp-uniform (m, x)
+#pragma unroll 1
+    for (int T = t; T < 15 * C::NL; T += blockDim.x) {
+      const int m = T / (5 * C::NL), x = (T / C::NL) % 5, lam = T % C::NL;
+      if (!((K.dirs >> m) & 1)) continue;
+      int base, stride;
+      if (m == 0) { base = (lam / n) * n + lam % n; stride = PI; }          // line (j, k)
+      else if (m == 1) { base = (lam / n) * PI + lam % n; stride = n; }     // line (i, k)
+      else { base = (lam % n) * PI + (lam / n) * n; stride = 1; }           // line (i, j)
+      double* fl = s_f + (m * 5 + x) * FS + base;
+      double xl[n];
+#pragma unroll
+      for (int a = 0; a < n; ++a) xl[a] = fl[a * stride];
+      if (x < 2) hv::eo_mv_st_s<n, 1>(s_cf, xl, fl, stride);   // -D^T (weak), in place
+      else hv::eo_mv_st_s<n, 0>(s_cf, xl, fl, stride);         // D (strong), in place
+    }
+    __syncthreads();
+    // ---- phase 3: element accumulator, then the column DSS
+    if (act) {
+      double acc[5];
+      double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int m = 0; m < 3; ++m)
+        if ((K.dirs >> m) & 1) {
+#pragma unroll
+          for (int x = 0; x < 5; ++x) r[x] += s_f[(m * 5 + x) * FS + na];
+        }
+      acc[0] = -r[0];                                   // acc -= weak = acc + sum_a D[a,i] (w3 F)_a
+      acc[4] = -r[1];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[1 + c] = -(w * r[2 + c]) - extra[c];
+      double* cw = s_carry + (l & 1) * n * n * 5 + (i * n + j) * 5;
+      const double* cr = s_carry + ((l + 1) & 1) * n * n * 5 + (i * n + j) * 5;
+      if (k == 0 && l > 0) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) acc[f] = cr[f] + acc[f];   // previous layer's top first
+      }
+      if (k == N && l < nlay - 1) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) cw[f] = acc[f];
+      } else {
+        const int cd = s_code[i * n + j];
+        const int z = l * N + k;
+        if (cd < 0) {
+          const double mi = A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t];
+          double* o = A.out + (int64_t)g * A.ldo;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) o[f] = A.accumulate ? o[f] + mi * acc[f] : mi * acc[f];
+        } else {
+          double* o = A.part + ((int64_t)cd * A.n_z + z) * 5;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) o[f] = acc[f];
+        }
+      }
+    }
+    __syncthreads();   // the flux arrays and the carry slot are rewritten by the next layer
+  }
+}
+
+template <int n>
+int run_lines(const double* Drow, const EulerConsts& K, int64_t nelem, const int32_t* gid, const double* w3,
+              const double* Mt, const double* q, int64_t ldq, const hv::TileArgs& A, const int32_t* elem,
+              cudaStream_t st) {
+  hv::DTabEO<n> Dt;
+  hv::fill_dtab_eo(Dt, Drow);
+  using C = ElinesCfg<n>;
+  auto kern = euler_lines_kernel<n>;
+  HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  kern<<<(unsigned)A.ntiles, ((C::nn + 31) / 32) * 32, C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
+
 template <int n>
 int run_tile(const double* Drow, const EulerConsts& K, int64_t nelem, const int32_t* gid, const double* w3,
              const double* Mt, const double* q, int64_t ldq, const hv::TileArgs& A, const int32_t* elem,
              cudaStream_t st) {
+  // 2C / 3C at N >= 4: the line-task kernel (HV_EULER_LINES=0 keeps the per-node line sums)
+  if constexpr (n >= 5) {
+    const char* ev = getenv("HV_EULER_LINES");
+    if (K.set != 0 && !(ev && atoi(ev) == 0)) return run_lines<n>(Drow, K, nelem, gid, w3, Mt, q, ldq, A, elem, st);
+  }
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
   constexpr int nn = n * n * n;

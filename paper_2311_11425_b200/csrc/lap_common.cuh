@@ -83,6 +83,92 @@ __device__ __forceinline__ void eo_mv(const DTabEO<n>& Dt, const double (&x)[n],
   }
 }
 
+// eo_mv with the outputs stored as they are formed (out[i * stride]): fewer live registers
+template <int n, int W>
+__device__ __forceinline__ void eo_mv_st(const DTabEO<n>& Dt, const double (&x)[n], double* out, int stride) {
+  constexpr int N = n - 1, M = n / 2;
+  double xd[M], xs[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) {
+    xd[a] = x[a] - x[N - a];
+    xs[a] = x[a] + x[N - a];
+  }
+  double xm = 0.0;
+  if constexpr (n % 2 == 1) xm = x[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double e = Dt.ce[W][i][0] * xd[0], o = Dt.co[W][i][0] * xs[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) {
+      e = fma(Dt.ce[W][i][a], xd[a], e);
+      o = fma(Dt.co[W][i][a], xs[a], o);
+    }
+    if constexpr (n % 2 == 1) o = fma(Dt.cm[W][i], xm, o);
+    out[i * stride] = e + o;
+    out[(N - i) * stride] = e - o;
+  }
+  if constexpr (n % 2 == 1) {
+    double e = Dt.ce[W][M][0] * xd[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) e = fma(Dt.ce[W][M][a], xd[a], e);
+    out[M * stride] = e;
+  }
+}
+
+// eo_mv_st with the coefficients read from shared memory (a copy of DTabEO's ce[W], co[W], cm[W] in
+// that order, eo_smem_fill): kernels whose loops would otherwise hoist the constant-bank coefficients
+// into registers and spill them
+template <int n>
+struct EOSmem {
+  static constexpr int M = n / 2 > 0 ? n / 2 : 1, CE = ((n + 1) / 2) * M, CO = M * M, PER = CE + CO + M;
+};
+template <int n>
+__device__ __forceinline__ void eo_smem_fill(const DTabEO<n>& Dt, double* cf, int tid, int nthr) {
+  using E = EOSmem<n>;
+  for (int x = tid; x < 2 * E::PER; x += nthr) {
+    const int w = x / E::PER, r = x % E::PER;
+    double v;
+    if (r < E::CE) v = Dt.ce[w][r / E::M][r % E::M];
+    else if (r < E::CE + E::CO) v = Dt.co[w][(r - E::CE) / E::M][(r - E::CE) % E::M];
+    else v = Dt.cm[w][r - E::CE - E::CO];
+    cf[x] = v;
+  }
+}
+template <int n, int W>
+__device__ __forceinline__ void eo_mv_st_s(const double* cf0, const double (&x)[n], double* out, int stride) {
+  using E = EOSmem<n>;
+  constexpr int N = n - 1, M = n / 2;
+  const double* ce = cf0 + W * E::PER;
+  const double* co = ce + E::CE;
+  const double* cm = co + E::CO;
+  double xd[M], xs[M];
+#pragma unroll
+  for (int a = 0; a < M; ++a) {
+    xd[a] = x[a] - x[N - a];
+    xs[a] = x[a] + x[N - a];
+  }
+  double xm = 0.0;
+  if constexpr (n % 2 == 1) xm = x[M];
+#pragma unroll
+  for (int i = 0; i < M; ++i) {
+    double e = ce[i * M] * xd[0], o = co[i * M] * xs[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) {
+      e = fma(ce[i * M + a], xd[a], e);
+      o = fma(co[i * M + a], xs[a], o);
+    }
+    if constexpr (n % 2 == 1) o = fma(cm[i], xm, o);
+    out[i * stride] = e + o;
+    out[(N - i) * stride] = e - o;
+  }
+  if constexpr (n % 2 == 1) {
+    double e = ce[M * M] * xd[0];
+#pragma unroll
+    for (int a = 1; a < M; ++a) e = fma(ce[M * M + a], xd[a], e);
+    out[M * stride] = e;
+  }
+}
+
 // Up to five (state column) indices.
 struct FieldMap {
   int f[5];

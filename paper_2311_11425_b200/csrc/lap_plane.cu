@@ -94,7 +94,7 @@ struct PlaneCfg {
   static constexpr int MTS = (NODES + 1) & ~1;
   // field-major (SoA) shared arrays with padded strides.  For the production shape (n = 5,
   // 2x2 tiles, thread order (jp, e, f)) the strides come from an exhaustive bank-conflict
-  // search (ablate/bank_search.py): every plane / eta-line access of a half-warp then hits
+  // search (tools/bank_search.py): every plane / eta-line access of a half-warp then hits
   // 16 distinct 8-byte banks.  Other shapes use the plain padded layout.
   static constexpr bool TUNED = (n == 5 && TX == 2 && TY == 2 && H == 1);
   // N = 7 single-column tiles, H = 4 (tools/bank_search_n7.py, half-warp model: ~2x fewer wavefronts than plain)
