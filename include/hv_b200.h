@@ -181,6 +181,12 @@ typedef struct hv_lap_plan {
                                 * (nglobal, 5) rows (lattice-numbered meshes, tiles.build_chunk_table) */
   double* d_sv;                /* (nslot * n_z * 4) final values of the slot column nodes: [nslot][4]
                                 * for z = 0, then per layer lb [nslot][N][4] for z = lb*N + 1 + kk   */
+  /* vertical segments (plane kernel, N <= 4, one GPU): seg > 0 sweeps each tile as segments of seg
+   * layers, one CTA each (more CTAs for meshes with few tiles); the levels between segments leave raw
+   * sums in d_bnd that the slot fix-up completes.  seg = 0: whole columns. */
+  int seg;
+  double* d_bnd;               /* (ntiles, nseg - 1, 2, U*V, 5) boundary-level sums                      */
+  const int32_t* d_prow;       /* (rows) partial row -> tile * U*V + u*V + v                             */
 } hv_lap_plan;
 
 /* Split Laplacian pass for the multi-GPU slab decomposition (the host runs the

@@ -73,6 +73,9 @@ class LapPlan(C.Structure):
         ("d_yt", _P),
         ("d_tchunk", _P),
         ("d_sv", _P),
+        ("seg", C.c_int),
+        ("d_bnd", _P),
+        ("d_prow", _P),
     ]
 
 

@@ -38,6 +38,7 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
   A.wform = P->wform; A.kh = P->kh; A.kd = P->kd; A.Ms = P->d_Ms;
   A.io = 0; A.tper = P->d_tper; A.sv = P->d_sv; A.tchunk = P->d_tchunk; A.ng = P->nglobal;
+  A.seg = P->seg; A.bnd = P->d_bnd; A.prow = P->d_prow;
   return A;
 }
 
@@ -55,7 +56,7 @@ bool use_tiles(const hv_lap_plan* P, int nf) {
 // alpha = 2 through the tile-ordered intermediate (plane kernel, N = 4, 2x2 tiles, 4 fields, one GPU)
 bool use_yt(const hv_lap_plan* P, int nf, const double* out) {
   int64_t lay[5];
-  return P->d_yt && P->d_tper && P->d_sv && use_plane(P, nf) && hv::plane_yt_layout(P->N, P->TX, P->TY, nf, lay) &&
+  return P->d_yt && P->d_tper && P->d_sv && P->seg <= 0 && use_plane(P, nf) && hv::plane_yt_layout(P->N, P->TX, P->TY, nf, lay) &&
          !(P->d_slot_ext && P->next > 0) && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
 }
 

@@ -75,44 +75,92 @@ __global__ void slot_pack_kernel(TileArgs A) {
   for (int ff = 0; ff < F; ++ff) o[ff] = acc[ff];
 }
 
+// vertical segments (lap_plane.cu, TileArgs::seg): the partial of a slot column node on a segment
+// boundary is the sum of the two segments' raw sums (from below, then from above) of its owning tile
+template <int F>
+__device__ __forceinline__ void bnd_partial(const TileArgs& A, int64_t r, int b, int nseg, int UV, double (&v)[F]) {
+  const int64_t tu = A.prow[r], t = tu / UV, uv = tu - t * UV;
+  const double* lo = A.bnd + (((t * (nseg - 1) + b) * 2 + 0) * UV + uv) * F;
+  const double* hi = lo + (int64_t)UV * F;
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) v[ff] = lo[ff] + hi[ff];
+}
+
 template <int F>
 __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (id >= A.nslot * A.n_z) return;
+  const int64_t nsi = A.nslot * A.n_z;
+  const int N = (A.n_z - 1) / A.nlay, n = N + 1;
+  const int nseg = A.seg > 0 ? (A.nlay + A.seg - 1) / A.seg : 1;
+  const int UV = (A.TX * N + 1) * (A.TY * N + 1);
   const unsigned nz = (unsigned)A.n_z;
-  int64_t s;     // slot
-  int z;         // level
+  int64_t s = -1;  // slot (-1: a tile-owned node on a segment boundary)
+  int z;           // level
+  int g;           // output row
+  double acc[F];
+  double mi;
   double* o;
-  if (row_mode == 3) {
-    // the slot rows of the tile-ordered intermediate, in their own order (lap_tile.cuh: [nslot][F] for
-    // z = 0, then per layer block [nslot][N][F]): thread id writes row id
-    const int N = (A.n_z - 1) / A.nlay;
-    if (id < A.nslot) {
-      s = id;
-      z = 0;
+  if (id < nsi) {
+    if (row_mode == 3) {
+      // the slot rows of the tile-ordered intermediate, in their own order (lap_tile.cuh: [nslot][F] for
+      // z = 0, then per layer block [nslot][N][F]): thread id writes row id
+      if (id < A.nslot) {
+        s = id;
+        z = 0;
+      } else {
+        const int64_t r = id - A.nslot, lb = r / (A.nslot * N), w = r - lb * (A.nslot * N);
+        s = w / N;
+        z = (int)(lb * N + 1 + (w - s * N));
+      }
     } else {
-      const int64_t r = id - A.nslot, lb = r / (A.nslot * N), w = r - lb * (A.nslot * N);
-      s = w / N;
-      z = (int)(lb * N + 1 + (w - s * N));
+      s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
+      z = (int)((unsigned)id - (unsigned)s * nz);
     }
+    g = A.col_gid[(int64_t)A.slot_col[s] * A.n_z + z];
+    mi = A.Ms ? __ldg(A.Ms + s * A.n_z + z) : __ldg(A.Minv + g);
+    const int zb = (nseg > 1) ? A.seg * N : 0;
+    if (zb && z % zb == 0 && z > 0 && z < A.n_z - 1) {   // segment boundary: the owners' two halves
+      const int b = z / zb - 1, r0 = A.slot_row0[s], nc = A.slot_nc[s];
+#pragma unroll
+      for (int ff = 0; ff < F; ++ff) acc[ff] = 0.0;
+      for (int r = 0; r < nc; ++r) {
+        double v[F];
+        bnd_partial<F>(A, r0 + r, b, nseg, UV, v);
+#pragma unroll
+        for (int ff = 0; ff < F; ++ff) acc[ff] += v[ff];
+      }
+    } else {
+      local_sum<F>(A, s, z, acc);
+    }
+  } else {
+    // tile-owned column nodes on segment boundaries: (tile, boundary, column)
+    if (nseg == 1) return;
+    const int64_t x = id - nsi, per = (int64_t)(nseg - 1) * UV;
+    const int64_t t = x / per;
+    if (t >= A.ntiles) return;
+    const int b = (int)((x - t * per) / UV), uv = (int)(x % UV);
+    if (A.code[t * UV + uv] >= 0) return;                 // slot columns: the slot items above
+    const int lb = (b + 1) * A.seg, gts = (UV * n + 3) & ~3;
+    g = A.gt[(t * A.nlay + lb) * gts + uv * n];
+    if (g < 0) return;
+    z = lb * N;
+    mi = __ldg(A.Minv + g);
+    const double* lo = A.bnd + (((t * (nseg - 1) + b) * 2 + 0) * UV + uv) * F;
+    const double* hi = lo + (int64_t)UV * F;
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) acc[ff] = lo[ff] + hi[ff];
+  }
+  if (row_mode == 3) {
     o = A.sv + id * F;
   } else {
-    s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
-    z = (int)((unsigned)id - (unsigned)s * nz);
-    o = nullptr;
+    o = A.out + (int64_t)g * A.ldo;
   }
-  const int c = A.slot_col[s];
-  const int g = A.col_gid[(int64_t)c * A.n_z + z];
-  if (row_mode != 3) o = A.out + (int64_t)g * A.ldo;
-  const double mi = A.Ms ? __ldg(A.Ms + s * A.n_z + z) : __ldg(A.Minv + g);
   double prev[F];
   if (A.accumulate) {
 #pragma unroll
     for (int ff = 0; ff < F; ++ff) prev[ff] = o[A.of.f[ff]];
   }
-  double acc[F];
-  local_sum<F>(A, s, z, acc);
-  if (A.slot_ext && A.slot_ext[s] >= 0) {
+  if (s >= 0 && A.slot_ext && A.slot_ext[s] >= 0) {
     const int ext = A.slot_ext[s];
     const double* rm = A.recv + ((int64_t)ext * A.n_z + z) * F;
     const bool lower_side = ext < A.face;   // side 0: the neighbour has the lower rank
@@ -159,8 +207,12 @@ int pack_f(const TileArgs& A, cudaStream_t st) {
 
 template <int F>
 int fixup_f(const TileArgs& A, cudaStream_t st) {
-  if (A.nslot <= 0) return HV_OK;
-  const int64_t tot = A.nslot * A.n_z;
+  const int nseg = A.seg > 0 ? (A.nlay + A.seg - 1) / A.seg : 1;
+  const int N = (A.n_z - 1) / A.nlay;
+  const int64_t nbi = (nseg > 1) ? A.ntiles * (nseg - 1) * (int64_t)((A.TX * N + 1) * (A.TY * N + 1)) : 0;
+  if (nseg > 1 && (!A.bnd || !A.prow || A.io != 0 || A.slot_ext)) HV_FAIL(HV_ERR_INVALID, "slot_fixup: bad segment plan");
+  if (A.nslot <= 0 && nbi == 0) return HV_OK;
+  const int64_t tot = A.nslot * A.n_z + nbi;
   if (tot >= (int64_t)1 << 31) HV_FAIL(HV_ERR_UNSUPPORTED, "slot_fixup: %lld slot rows", (long long)tot);
   int row_mode = 0;
   if (A.io == 1 || A.io == 3) {   // pass 1 into the tile-ordered intermediate

@@ -140,7 +140,7 @@ struct PlaneCfg {
   // IO 3 (pass 1 with bulk-copied input, tiles.build_chunk_table): the state's (nglobal, 5) rows of
   // levels 1..N in a row buffer (whole rows, runs of consecutive gids), level 0 in two planes laid
   // out like a Yt level [f][u][v]
-  static constexpr int CRR = 362;                        // row-buffer rows (the table places <= 360)
+  static constexpr int CRR = 392;                        // row-buffer rows (the table places <= 390)
   static constexpr int QB_P = CRR * 5;                   // IO 3: the two level-0 planes
   static constexpr int TCW = UV + 1 + 4 * 32;            // IO 3: ints per tile of TileArgs::tchunk
   static constexpr int SQB = IO == 2 ? QB_S + NPER * N * F : (IO == 3 ? QB_P + 2 * YLS : SQ);
@@ -201,11 +201,15 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   const int jp = min(tid / (F * H * NE), n - 1);
   const int I0 = ih * NR, K0 = ih * NK;
   const int px = e / TY, py = e % TY;
-  const int64_t t = A.tile0 + blockIdx.x;
+  const int nlay = A.nlay;
+  // vertical segments (IO 0): CTA = (tile, segment of A.seg layers) sweeping layers [l0, l1)
+  const int nseg = (IO == 0 && A.seg > 0) ? (nlay + A.seg - 1) / A.seg : 1;
+  const int64_t t = A.tile0 + blockIdx.x / nseg;
+  const int sg = blockIdx.x % nseg;
+  const int l0 = (nseg > 1) ? sg * A.seg : 0, l1 = (nseg > 1) ? min(nlay, l0 + A.seg) : nlay;
   const int tx = A.tmeta[2 * t], ty = A.tmeta[2 * t + 1];
   const bool pth = tid < C::NP;       // plane thread (the rest: helper lanes for the node-granular steps)
   const bool act = pth && (px < tx) && (py < ty);
-  const int nlay = A.nlay;
   const int32_t* gt_t = A.gt + t * (int64_t)nlay * C::GTS;
   const double* Wt_t = A.Wt + t * (int64_t)nlay * C::WL;
   const double* Mt_t = A.Mt + t * (int64_t)nlay * C::MTS;
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   };
 
   int gcur[PN], gnext[PN];
-  if constexpr (IO != 2) load_gids(0, gcur);   // IO 3: layer 0 is gathered
+  if constexpr (IO != 2) load_gids(l0, gcur);   // IO 3: layer 0 is gathered
   if (WV == 0 && tid == 0) {
     mbar_init(bar, 1);
     fence_mbar_init();
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   if constexpr (IO == 3) __syncthreads();   // s_pdst before the layer-0 gather uses it
   if constexpr (IO != 2) {
     issue_gather(gcur);
-    if (GATHER && nlay > 1) load_gids(1, gnext);
+    if (GATHER && l0 + 1 < l1) load_gids(l0 + 1, gnext);
   }
   if constexpr (H > 1)
     for (int x = tid; x < n * n; x += C::NT) sD[x] = Dt.D[x / n][x % n];
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         if ((s_code[uv] < 0) == (pass == 0)) s_perm[c++] = uv;
   }
   __syncthreads();
-  if (WV == 0 && tid == 0) issue_metric(0);
+  if (WV == 0 && tid == 0) issue_metric(l0);
   if constexpr (IO == 2) {   // prologue: level 0 of block 0 (+ its perimeter rows); then layer 0's loads
     if (tid < 32) issue_loads(-1, nper);
     mbar_wait(bar + 1, 0);
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   // partners stay converged (their scratch is zeroed in step e)
   const bool run = (H == 1) ? act : pth;
 
-  for (int l = 0; l < nlay; ++l) {
+  for (int l = l0; l < l1; ++l) {
     // ---- a: q(l) has landed
     if constexpr (IO == 2) {   // layer l's loads (levels 1..N-1, level 0 of block l+1, perimeter rows)
       mbar_wait(bar + 1, (uint32_t)((l + 1) & 1));
@@ -533,8 +537,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     __syncthreads();
     const double* sq_lo = s_q + (IO == 3 ? C::QB_P : C::QB_L0) + (l & 1) * C::YLS;
     const double* sq_hi = s_q + (IO == 3 ? C::QB_P : C::QB_L0) + ((l + 1) & 1) * C::YLS;
-    if (WV == 1 && tid == 0 && l + 1 < nlay) l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
-    if (tid == C::NT - 1 && l + 1 < nlay) {   // output-item gid / Minv of the next layer -> L2
+    if (WV == 1 && tid == 0 && l + 1 < l1) l2_prefetch(Wt_t + (int64_t)(l + 1) * C::WL, C::WL * 8);
+    if (tid == C::NT - 1 && l + 1 < l1) {   // output-item gid / Minv of the next layer -> L2
       l2_prefetch(Mt_t + (int64_t)(l + 1) * C::MTS, C::MTS * 8);
       if (!OUT_YT) l2_prefetch(gt_t + (int64_t)(l + 1) * C::GTS, C::GTS * 4);
     }
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         issue_chunks(l + 1);
       }
     } else {
-      if (l + 1 < nlay) issue_gather(gnext);
+      if (l + 1 < l1) issue_gather(gnext);
     }
     if (AB & 8) {
 #pragma unroll
@@ -655,7 +659,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         for (int k = 0; k < n; ++k) p0[r][k] = p2[r][k] = s_q[tq(r, jp, k)];
     }
     // ---- c: flux at the plane nodes, weak xi / zeta in registers
-    if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)(l & 1));
+    if (WV == 0 && !(AB & 4)) mbar_wait(bar, (uint32_t)((l - l0) & 1));
     if (run && WF == 2) {
       // isotropic form: [i][k][e][j]; the F field lanes of a plane read the same s (broadcast)
       const double* Sw = s_w + e * n + jp;
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       }
     }
     __syncthreads();
-    if (WV == 0 && tid == 0 && l + 1 < nlay) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
+    if (WV == 0 && tid == 0 && l + 1 < l1) {      // metric buffer free: W(l+1) lands during d, e, f, a, b
       fence_proxy_async();
       issue_metric(l + 1);
     }
@@ -946,7 +950,21 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
           const double c3 = (ct.z >= 0) ? sp[ct.w] : 0.0;
           val.v[p] = (c0 + c1) + (c2 + c3);
         }
-        emit(gf[it], mf[it], val, s_code[uv], l * N + k);
+        if (IO == 0 && k == 0 && l == l0 && l0 > 0) {   // segment bottom: raw sum, from above
+          double* o = A.bnd + (((t * (nseg - 1) + sg - 1) * 2 + 1) * UV + uv) * F;
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[p] = val.v[p];
+        } else {
+          emit(gf[it], mf[it], val, s_code[uv], l * N + k);
+        }
+      }
+      if (IO == 0 && l == l1 - 1 && l1 < nlay) {   // segment top: raw sums, from below
+        for (int uv = tid; uv < UV; uv += C::NT) {
+          const int4 ct = s_ct[uv];
+          double* o = A.bnd + (((t * (nseg - 1) + sg) * 2 + 0) * UV + uv) * F;
+#pragma unroll
+          for (int p = 0; p < F; ++p) o[p] = csum(ct, s_s + p * C::SP + N);
+        }
       }
       if (l == nlay - 1) {        // top nodes of the columns
         for (int uv = tid; uv < UV; uv += C::NT) {
@@ -968,7 +986,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         }
       }
     }
-    if (GATHER && l + 2 < nlay) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
+    if (GATHER && l + 2 < l1) load_gids(l + 2, gnext);   // consumed by the gather issued in step b of l + 1
     // the next step's barrier (a) orders these reads before the scratch is rewritten
   }
 }
@@ -1019,7 +1037,9 @@ int run_plane_om(const TileArgs& A, const hv::DTabEO<n>& Dt, cudaStream_t st) {
   auto kern = lap_plane_kernel<n, TX, TY, F, WV, MB, AB, H, WF, OM, IO>;
   HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
   if (A.tile1 <= A.tile0) return HV_OK;
-  kern<<<(unsigned)(A.tile1 - A.tile0), C::NT, C::SMEM, st>>>(Dt, A);
+  const int nseg = (IO == 0 && A.seg > 0) ? (A.nlay + A.seg - 1) / A.seg : 1;
+  if (IO != 0 && A.seg > 0) HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: vertical segments need io 0");
+  kern<<<(unsigned)((A.tile1 - A.tile0) * nseg), C::NT, C::SMEM, st>>>(Dt, A);
   HV_LAUNCH_CHECK();
   return HV_OK;
 }

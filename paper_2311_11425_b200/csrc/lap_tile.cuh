@@ -47,6 +47,12 @@ struct TileArgs {
                             // (in slot order), then 32 runs of consecutive slots (first slot, count, position)
   const int32_t* tchunk;    // (ntiles, U*V + 1 + 128) bulk-copy runs of a tile's q input (io 3, tiles.py)
   int64_t ng;               // rows of q (io 3: no bulk copy reads past row ng - 1)
+  // vertical segments (plane kernel, io 0): seg > 0 sweeps each tile's columns as segments of seg layers
+  // (one CTA each); the levels between segments leave raw partial sums in bnd, [tile][boundary][side
+  // 0: from below, 1: from above][U*V][F], which slot_fixup completes (prow: partial row -> tile*U*V + uv)
+  int seg;
+  double* bnd;
+  const int32_t* prow;
   double* sv;               // final values of the slot column nodes: [nslot][F] (z = 0), then per layer
                             // block lb: [nslot][N][F] (z = lb*N + 1 + kk)
 };

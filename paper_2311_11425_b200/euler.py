@@ -88,6 +88,22 @@ class EulerOps:
         cols = d["col_gid"][d["slot_col"].long()].long()
         return self.mass.d_Minv[cols].contiguous()
 
+    @staticmethod
+    def _segments(tp):
+        """Layers per vertical segment of the N <= 4 plane sweep (hv_lap_plan.seg), 0 = whole columns.
+        A mesh with fewer tiles than one wave of CTA slots (148 SMs x 4) is swept as two half columns
+        (config 2: 256 tiles x 8 layers -> 512 CTAs of 4 layers: 0.114 -> 0.102 ms per H_nu op; 8 or 4
+        segments measured 0.132 / 0.114 ms, and config 3's 1350 tiles lose with 2, 0.46 -> 0.52 ms).
+        HV_SEG (layers per segment) overrides."""
+        env = os.environ.get("HV_SEG", "")
+        if env:
+            seg = int(env)
+        else:
+            if tp.ntiles >= 148 * 4 or tp.nlay < 2:
+                return 0
+            seg = -(-tp.nlay // 2)
+        return seg if 0 < seg < tp.nlay else 0
+
     def _yt_chain(self, tp, d):
         """(tper, yt, sv) for H_nu's tile-ordered intermediate (hv_lap_plan.d_yt), or
         None when the plane kernel has no tile-ordered mode for this plan (or HV_YT=0)."""
@@ -198,7 +214,8 @@ class EulerOps:
                 Ms = self._slot_minv(d)
                 p.d_Ms = _lib.ptr(Ms)
                 keep += [Wt, Mt, Ms]
-                yt = self._yt_chain(tp, d) if layout == 1 and not self.ext_cols else None
+                seg = self._segments(tp) if layout == 1 and dev.N <= 4 and not self.ext_cols else 0
+                yt = self._yt_chain(tp, d) if layout == 1 and not self.ext_cols and not seg else None
                 if yt is not None:
                     p.d_tper, p.d_yt, p.d_sv = (x.data_ptr() for x in yt)
                     keep += list(yt)
@@ -210,6 +227,16 @@ class EulerOps:
                         ct = to_dev(ct)
                         p.d_tchunk = ct.data_ptr()
                         keep.append(ct)
+                if seg:
+                    nseg = -(-tp.nlay // seg)
+                    t, u, v = np.nonzero(tp.code >= 0)
+                    prow = np.zeros(max(1, tp.npart), dtype=np.int32)
+                    prow[tp.code[t, u, v]] = (t * tp.U * tp.V + u * tp.V + v).astype(np.int32)
+                    bnd = torch.zeros(tp.ntiles * (nseg - 1) * 2 * tp.U * tp.V * 5, dtype=torch.float64,
+                                      device="cuda")
+                    prow = to_dev(prow)
+                    p.seg, p.d_bnd, p.d_prow = seg, bnd.data_ptr(), prow.data_ptr()
+                    keep += [bnd, prow]
                 if self.ext_cols:
                     face = self.ext_face
                     p.d_slot_ext, p.d_ext_slots = d["slot_ext"].data_ptr(), d["ext_slots"].data_ptr()

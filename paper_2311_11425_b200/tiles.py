@@ -214,24 +214,28 @@ def build_chunk_table(tp, rows_cap, row_ld=5):
             if not np.array_equal(d, stride * np.arange(nlay - 1)):
                 return None
             runs.append((int(c1[cols[0]]), stride, (b - a) * N, cols))
-        # placement: big runs (element chunks) first, 68 rows apart; then the faces
+        # placement: big runs (element chunks) first, 68 rows apart; then the faces.  When that does not
+        # fit the row buffer (e.g. cubed-sphere tiles at panel edges), packed with one spare row only.
         runs.sort(key=lambda r: -r[2])
-        cur, big = 0, 0
-        colrow = np.zeros(UV, dtype=np.int64)
-        meta = []
-        for g1, stride, nrows, cols in runs:
-            if stride % 2:
-                return None                                      # parity must not change between layers
-            p = cur + (1 if cur else 0)
-            if nrows >= 4 * N * N:
-                p = max(p, 68 * big)
-                big += 1
-            if (p - g1) % 2:
-                p += 1
-            colrow[cols] = p + N * np.arange(len(cols))
-            meta.append((g1, stride, nrows, p))
-            cur = p + nrows
-        if cur + 1 > rows_cap:
+        if any(st % 2 for _, st, _, _ in runs):
+            return None                                          # parity must not change between layers
+        for aligned in (True, False):
+            cur, big = 0, 0
+            colrow = np.zeros(UV, dtype=np.int64)
+            meta = []
+            for g1, stride, nrows, cols in runs:
+                p = cur + (1 if cur else 0)
+                if aligned and nrows >= 4 * N * N:
+                    p = max(p, 68 * big)
+                    big += 1
+                if (p - g1) % 2:
+                    p += 1
+                colrow[cols] = p + N * np.arange(len(cols))
+                meta.append((g1, stride, nrows, p))
+                cur = p + nrows
+            if cur + 1 <= rows_cap:
+                break
+        else:
             return None
         out[t, :UV] = colrow
         out[t, UV] = len(meta)

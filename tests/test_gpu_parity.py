@@ -220,7 +220,9 @@ def test_tile_ordered_intermediate_bitwise(pair, monkeypatch):
     name, p, o = pair
     from paper_2311_11425_b200 import euler, hyperdiff, state
 
-    plan = p.ops.lap_plan(p.vm)
+    monkeypatch.setenv("HV_SEG", "0")          # whole columns (small meshes are otherwise segmented)
+    yops = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+    plan = yops.lap_plan(p.vm)
     if not plan.d_yt:
         pytest.skip("no tile-ordered mode for this plan (N != 4 or not the plane kernel)")
     monkeypatch.setenv("HV_YT", "0")
@@ -228,7 +230,7 @@ def test_tile_ordered_intermediate_bitwise(pair, monkeypatch):
     assert not ops0.lap_plan(p.vm).d_yt
     cfg2 = hyperdiff.HyperDiffConfig(**{**p.c["hd"], "alpha": 2})
     st = state.StateField("2C", o.state)
-    a = hyperdiff.hyperdiffusion_apply(st, cfg2, p.vm, p.ops)
+    a = hyperdiff.hyperdiffusion_apply(st, cfg2, p.vm, yops)
     b = hyperdiff.hyperdiffusion_apply(st, cfg2, p.vm, ops0)
     assert np.array_equal(a, b)
     if p.cfg.alpha == 2:
@@ -239,9 +241,38 @@ def test_tile_ordered_intermediate_bitwise(pair, monkeypatch):
     qd = torch.from_numpy(o.state).cuda()
     base = torch.randn_like(qd)
     oa, ob = base.clone(), base.clone()
-    hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg2, p.vm, p.ops, out=oa, accumulate=True)
+    hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg2, p.vm, yops, out=oa, accumulate=True)
     hyperdiff.hyperdiffusion_apply(state.StateField("2C", qd), cfg2, p.vm, ops0, out=ob, accumulate=True)
     assert torch.equal(oa, ob)
+
+
+@pytest.mark.parametrize("seg", ["1", "2"])
+def test_vertical_segments_match_whole_columns(pair, monkeypatch, seg):
+    """The plane sweep cut into vertical segments (HV_SEG layers per CTA; the levels between segments
+    completed by the slot fix-up) gives the whole-column result to rounding, for H_nu and for the
+    Laplacian on 1, 4 and 5 fields."""
+    name, p, o = pair
+    from paper_2311_11425_b200 import euler, hyperdiff, state
+
+    if p.m.degree > 4 or p.c.get("nv", 2) < 2 or not p.ops._tile_arrays():
+        pytest.skip("segments: N <= 4 plane kernel, >= 2 layers")
+    monkeypatch.setenv("HV_SEG", "0")
+    ops0 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+    ops0.lap_plan(p.vm)                        # plans are built lazily: before HV_SEG changes
+    monkeypatch.setenv("HV_SEG", seg)
+    ops1 = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
+    plan = ops1.lap_plan(p.vm)
+    if plan.seg == 0:
+        pytest.skip("mesh has fewer layers than the segment")
+    assert ops0.lap_plan(p.vm).seg == 0 and not plan.d_yt
+    st = state.StateField("2C", o.state)
+    a = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops0)
+    b = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, ops1)
+    assert rel_l2(b, a) <= 1e-14 and rel_l2(b, o.hyper()) <= TOL
+    for fields in ((3,), (1, 2, 3, 4), (0, 1, 2, 3, 4)):
+        la = hyperdiff.laplacian_apply_fields(o.state, p.vm, ops0, fields)
+        lb = hyperdiff.laplacian_apply_fields(o.state, p.vm, ops1, fields)
+        assert rel_l2(lb, la) <= 1e-14
 
 
 def test_all_five_fields_one_pass(pair):
