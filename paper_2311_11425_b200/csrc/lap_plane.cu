@@ -176,8 +176,8 @@ struct PlaneCfg {
 template <int n, int TX, int TY, int F, int WV, int MB, int AB = 0, int H = 1, int WF = 0, int OM = 0, int IO = 0>
 __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB) lap_plane_kernel(hv::DTabEO<n> Dt, TileArgs A) {
   using C = PlaneCfg<n, TX, TY, F, WV, H, WF, IO>;
-  static_assert(IO == 0 || (H == 1 && F == 4 && (AB == 0 || (IO == 1 && AB == 2))),
-                "tile-ordered intermediate: H = 1, 4 fields");
+  static_assert(IO == 0 || (F == 4 && (H == 1 || IO != 3) && (AB == 0 || (IO == 1 && AB == 2))),
+                "tile-ordered intermediate: 4 fields (split planes: no bulk-copied pass-1 input)");
   constexpr bool OUT_YT = (IO == 1 || IO == 3);   // results into the tile-ordered intermediate
   constexpr bool GATHER = (IO == 0 || IO == 1);   // q gathered by gid every layer (IO 3: layer 0 only)
   // line contractions held whole in a thread's registers (zeta, eta; xi too for whole planes, H = 1)
@@ -1066,6 +1066,19 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
   hv::fill_dtab_eo(Dt, Drow);
   if constexpr (n == 8) {
     const char* hs = getenv("HV_N7_SPLIT");
+    if constexpr (TX == 1 && TY == 1 && F == 4) {   // tile-ordered intermediate passes (split planes, H = 4)
+      if (A.io == 1 || A.io == 2) {
+        if (hs && atoi(hs) == 2) HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: tile-ordered passes need H = 4 at N = 7");
+        const bool w = A.io == 1;
+        if (A.wform == 1) return w ? run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 1, 0, 1>(A, Dt, st)
+                                   : run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 1, 0, 2>(A, Dt, st);
+        if (A.wform == 2) return w ? run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 2, 0, 1>(A, Dt, st)
+                                   : run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 2, 0, 2>(A, Dt, st);
+        return w ? run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 0, 0, 1>(A, Dt, st)
+                 : run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 0, 0, 2>(A, Dt, st);
+      }
+    }
+    if (A.io) HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no tile-ordered mode for this shape");
     if (A.wform == 1) {
       if (hs && atoi(hs) == 2) return run_plane_v<n, TX, TY, F, 0, 1, 0, 2, 1>(A, Dt, st);
       return run_plane_v<n, TX, TY, F, 0, 1, 0, 4, 1>(A, Dt, st);
@@ -1172,7 +1185,17 @@ int plane_chunk_rows(int N, int TX, int TY) {
 }
 
 bool plane_yt_layout(int N, int TX, int TY, int F, int64_t* lay) {
-  if (N != 4 || TX != 2 || TY != 2 || F != 4) return false;
+  if (F != 4) return false;
+  if (N == 7 && TX == 1 && TY == 1) {   // split-plane kernel: lanes (f, ih) hit f + 4 ih (mod 16) as well
+    using C = PlaneCfg<8, 1, 1, 4, 0, 4, 2, 1>;
+    lay[0] = C::YLS;
+    lay[1] = C::YUS;
+    lay[2] = C::YFS;
+    lay[3] = C::YBLK;
+    lay[4] = C::NPER;
+    return true;
+  }
+  if (N != 4 || TX != 2 || TY != 2) return false;
   using C = PlaneCfg<5, 2, 2, 4, 0, 1, 1, 1>;
   lay[0] = C::YLS;
   lay[1] = C::YUS;

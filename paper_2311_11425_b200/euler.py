@@ -109,6 +109,9 @@ class EulerOps:
         None when the plane kernel has no tile-ordered mode for this plan (or HV_YT=0)."""
         if os.environ.get("HV_YT", "1") == "0":
             return None
+        # N = 7: the split-plane kernel with H = 4 only (HV_YT7=0 keeps the rows intermediate there)
+        if tp.N == 7 and (os.environ.get("HV_YT7", "1") != "1" or os.environ.get("HV_N7_SPLIT", "") == "2"):
+            return None
         lay = np.zeros(5, dtype=np.int64)
         if _lib.lib().hv_plane_yt_layout(tp.N, tp.TX, tp.TY, 4, lay.ctypes.data) != 0:
             return None

@@ -221,6 +221,7 @@ def test_tile_ordered_intermediate_bitwise(pair, monkeypatch):
     from paper_2311_11425_b200 import euler, hyperdiff, state
 
     monkeypatch.setenv("HV_SEG", "0")          # whole columns (small meshes are otherwise segmented)
+    monkeypatch.setenv("HV_YT7", "1")          # the N = 7 split-plane variant too
     yops = euler.EulerOps(p.m, p.mets, p.consts, "2C", hyper=(p.cfg, p.vm))
     plan = yops.lap_plan(p.vm)
     if not plan.d_yt:
