@@ -505,9 +505,6 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       erow[r] = (s_pdst[(px * N + jp) * V + py * N + r] - 1) * 5 + myqc;
     }
   }
-  int nown = 0;   // IO 1: tile-owned columns (s_perm lists them first)
-  if constexpr (OUT_YT)
-    for (int uv = 0; uv < UV; ++uv) nown += (s_code[uv] < 0) ? 1 : 0;
   double carry[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) carry[r] = 0.0;
@@ -834,14 +831,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     int gf[PF];
     double mf[PF];
     double my[C::PFY];   // IO 1: scale * Minv of tile-owned block items, 1 for perimeter (raw partial sums)
-    constexpr int FI_ = C::FI;
     if constexpr (OUT_YT) {
 #pragma unroll
       for (int it = 0; it < C::PFY; ++it) {
         const int qi = tid + it * C::NT;
         my[it] = 1.0;
         if (qi < C::FIY) {
-          const int k = qi / UV, uv = qi - k * UV;
+          const int uv = s_perm[qi / N], k = qi % N;
           if (s_code[uv] < 0) my[it] = A.scale * __ldg(Mt_t + (int64_t)l * C::MTS + uv * n + k);
         }
       }
@@ -876,18 +872,30 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     // element copies of all F fields (predicated loads, fixed order (c0 + c1) + (c2 + c3)),
     // then one row store per item
     if constexpr (OUT_YT) {
-      // block items in (k, u, v) order: consecutive lanes store consecutive v.  Perimeter (slot) items:
-      // raw partial sums into their partial rows (the fix-up sums them into the compact slot rows that
-      // pass 2 stages); their block entries are never read, the raw sums keep the block's sectors whole
+      // block items in s_perm order (tile-owned columns first, the N levels of a column in consecutive
+      // lanes: the element-copy reads then have fewer bank conflicts than in (k, u, v) order, and a warp
+      // still stores runs of a level).  Perimeter (slot) items: raw partial sums (my = 1) also into their
+      // partial rows, 4 lanes one 128-byte run (the fix-up sums them into the compact slot rows that pass
+      // 2 stages); their block entries are never read, the raw sums keep the block's sectors whole
       double* yb = A.out + t * chain + (int64_t)l * C::YBLK;
 #pragma unroll
       for (int it = 0; it < C::PFY; ++it) {
         const int qi = tid + it * C::NT;
         if (qi >= C::FIY) continue;
-        const int k = qi / UV, uv = qi - k * UV, u = uv / V, v = uv - u * V;
+        const int uv = s_perm[qi / N], k = qi % N, u = uv / V, v = uv - u * V;
         const int4 ct = s_ct[uv];
+        hv::Vec<F> val;
 #pragma unroll
-        for (int p = 0; p < F; ++p) yb[k * C::YLS + p * C::YFS + u * C::YUS + v] = my[it] * csum(ct, s_s + p * C::SP + k);
+        for (int p = 0; p < F; ++p) {
+          val.v[p] = my[it] * csum(ct, s_s + p * C::SP + k);
+          yb[k * C::YLS + p * C::YFS + u * C::YUS + v] = val.v[p];
+        }
+        const int cd = s_code[uv];
+        if (cd >= 0) {
+          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * F;
+          st_v2(o, val.v[0], val.v[1]);
+          st_v2(o + 2, val.v[2], val.v[3]);
+        }
       }
       // the layout's padding (v = V..YUS-1 of every u row, u*YUS >= U*YUS up to YFS): zeros, so that
       // every sector of the block is written whole (no partial-sector read-modify-write in L2)
@@ -897,15 +905,6 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
           const int kf = x / PP, j = x - kf * PP;
           yb[(kf / F) * C::YLS + (kf % F) * C::YFS + ((j < U * PV) ? (j / PV) * C::YUS + V + j % PV : U * C::YUS + j - U * PV)] = 0.0;
         }
-      }
-      // the perimeter items again, column by column (s_perm: slot columns after the tile-owned ones), so
-      // that 4 lanes write one 128-byte run of partial rows
-      for (int qi = nown * N + tid; qi < FI_; qi += C::NT) {
-        const int uv = s_perm[qi / N], k = qi % N;
-        const int4 ct = s_ct[uv];
-        double* o = A.part + ((int64_t)s_code[uv] * A.n_z + l * N + k) * F;
-        st_v2(o, csum(ct, s_s + 0 * C::SP + k), csum(ct, s_s + 1 * C::SP + k));
-        st_v2(o + 2, csum(ct, s_s + 2 * C::SP + k), csum(ct, s_s + 3 * C::SP + k));
       }
       if (l == nlay - 1) {        // top level of the columns -> level 0 of block nlay
         double* yt = yb + C::YBLK;

@@ -71,3 +71,32 @@ if __name__ == "__main__":
     res.sort()
     for r in res[:12]:
         print(r)
+
+
+def items_perm_colfast(owned=lambda u, v: 0 < u < U - 1 and 0 < v < V - 1):
+    cols = [(u, v) for u in range(U) for v in range(V) if owned(u, v)]
+    cols += [(u, v) for u in range(U) for v in range(V) if not owned(u, v)]
+    return [(u, v, k) for k in range(N) for (u, v) in cols]
+
+
+def cost_items(items, SP=588, ES=147, AS=28, BS=5, wf=wf_half):
+    sa = lambda f, e, a, b, c: f * SP + e * ES + a * AS + b * BS + c
+    NTH, tot = 96, 0
+    nit = len(items)
+    for warp in range(NTH // 32):
+        for it in range((nit + NTH - 1) // NTH):
+            idx = [warp * 32 + ln + it * NTH for ln in range(32)]
+            sel = [items[x] if x < nit else None for x in idx]
+            for f in range(F):
+                for c in range(4):
+                    addrs = []
+                    for x in sel:
+                        if x is None:
+                            addrs.append(None)
+                            continue
+                        u, v, k = x
+                        cp = elem_copies(u, v)
+                        addrs.append(sa(f, cp[c][0], cp[c][1], cp[c][2], k) if c < len(cp) else None)
+                    if any(a is not None for a in addrs):
+                        tot += wf(addrs)
+    return tot
