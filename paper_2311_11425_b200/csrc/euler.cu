@@ -363,39 +363,50 @@ struct ElinesCfg {
   static constexpr size_t SMEM = sizeof(double) * (OFF_CODE + (n * n + 1) / 2);
 };
 
-template <int n>
-__global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::DTabEO<n> Dt, EulerConsts K,
+// NPT nodes per thread (blockDim = n^3 / NPT): NPT = 2 gives each thread twice the registers (2 x 256
+// threads x 128 at N = 7) so that both nodes' phase-1 loads are in flight together
+template <int n, int NPT>
+__global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::DTabEO<n> Dt, EulerConsts K,
                                                           int64_t nelem, const int32_t* __restrict__ gid,
                                                           const double* __restrict__ w3,
                                                           const double* __restrict__ Mt, const double* __restrict__ q,
                                                           int64_t ldq, hv::TileArgs A,
                                                           const int32_t* __restrict__ elem) {
   using C = ElinesCfg<n>;
-  constexpr int nn = C::nn, N = n - 1, PI = C::PI, FS = C::FS;
+  constexpr int nn = C::nn, N = n - 1, PI = C::PI, FS = C::FS, NB = nn / NPT;
+  static_assert(nn % NPT == 0, "nodes per thread");
   extern __shared__ double sm[];
   double* s_f = sm;                                      // [15][FS] fluxes, then line results
   double* s_carry = sm + C::OFF_C;                       // [2][n*n][5]
   int* s_code = reinterpret_cast<int*>(sm + C::OFF_CODE);
   double* s_cf = sm + C::OFF_CF;
   const int64_t tl = blockIdx.x;
-  const int t = threadIdx.x;
-  hv::eo_smem_fill<n>(Dt, s_cf, t, blockDim.x);   // visible after the first layer's phase-1 barrier
-  const bool act = t < nn;
-  const int i = t / (n * n), j = (t / n) % n, k = t % n;
-  const int na = i * PI + j * n + k;                     // this node's slot in a flux array
+  const int t0 = threadIdx.x;
+  hv::eo_smem_fill<n>(Dt, s_cf, t0, blockDim.x);   // visible after the first layer's phase-1 barrier
   const int nlay = A.nlay;
   const int64_t nloc = nelem * nn;
-  if (t < n * n) s_code[t] = A.code[tl * n * n + t];
+  for (int x = t0; x < n * n; x += blockDim.x) s_code[x] = A.code[tl * n * n + x];
   const double* Mt_t = A.Mt + tl * (int64_t)nlay * (((nn + 1) & ~1));
-  const double w = act ? w3[t] : 0.0;
+  double w[NPT];
+#pragma unroll
+  for (int jn = 0; jn < NPT; ++jn) w[jn] = (t0 + jn * NB < nn) ? w3[t0 + jn * NB] : 0.0;
   for (int l = 0; l < nlay; ++l) {
     const int64_t e = elem[tl * nlay + l];
-    const int64_t p = e * nn + (act ? t : 0);
-    // ---- phase 1 (euler_node_acc's fluxes, reference expression order)
-    double extra[3] = {0.0, 0.0, 0.0};                   // geopotential + Coriolis terms of acc[1..3]
-    int g = 0;
-    if (act) {
-      g = gid[p];
+    double extra[NPT][3];                                // geopotential + Coriolis terms of acc[1..3]
+    int gn[NPT];
+    // ---- phase 1 (euler_node_acc's fluxes, reference expression order), node t = t0 + jn * NB
+#pragma unroll
+    for (int jn = 0; jn < NPT; ++jn) {
+      const int t = t0 + jn * NB;
+      const bool act = t < nn;
+      const int k = t % n;
+      const int na = (t / (n * n)) * PI + ((t / n) % n) * n + k;
+      const int64_t p = e * nn + (act ? t : 0);
+      extra[jn][0] = extra[jn][1] = extra[jn][2] = 0.0;
+      gn[jn] = 0;
+      if (!act) continue;
+      const int g = gid[p];
+      gn[jn] = g;
       double qv[5];
 #pragma unroll
       for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
@@ -421,8 +432,8 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
         double un = (gm[0] * qv[1] + gm[1] * qv[2] + gm[2] * qv[3]) / rho;
         if (m == 2) un = un * mask;
         const double jun = Jg * un;
-        s_f[(m * 5 + 0) * FS + na] = w * (jun * qv[0]);
-        s_f[(m * 5 + 1) * FS + na] = w * (jun * qv[0] * tflux);
+        s_f[(m * 5 + 0) * FS + na] = w[jn] * (jun * qv[0]);
+        s_f[(m * 5 + 1) * FS + na] = w[jn] * (jun * qv[0] * tflux);
 #pragma unroll
         for (int c = 0; c < 3; ++c) s_f[(m * 5 + 2 + c) * FS + na] = Jg * (qv[1 + c] * un + P * gm[c]);
         if ((K.dirs >> m) & 1) {
@@ -431,9 +442,9 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
           for (int c = 0; c < 3; ++c) sg[c] += dphi * gm[c];
         }
       }
-      const double wj = w * Jg;
+      const double wj = w[jn] * Jg;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) extra[c] = wj * qv[0] * sg[c];
+      for (int c = 0; c < 3; ++c) extra[jn][c] = wj * qv[0] * sg[c];
       if (K.omega > 0.0) {   // Coriolis 2 omega e x u (euler.py:183-188, 217-223)
         double ev[3];
         if (K.coriolis == 0) {
@@ -449,27 +460,27 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
         }
         const double ux = qv[1], uy = qv[2], uz = qv[3];
         const double cx = ev[1] * uz - ev[2] * uy, cy = ev[2] * ux - ev[0] * uz, cz = ev[0] * uy - ev[1] * ux;
-        extra[0] += wj * 2.0 * K.omega * cx;
-        extra[1] += wj * 2.0 * K.omega * cy;
-        extra[2] += wj * 2.0 * K.omega * cz;
+        extra[jn][0] += wj * 2.0 * K.omega * cx;
+        extra[jn][1] += wj * 2.0 * K.omega * cy;
+        extra[jn][2] += wj * 2.0 * K.omega * cz;
       }
     }
     __syncthreads();
     // the next layer's element record (13 metric components, gids, Minv) -> L2, so that its phase-1
     // loads wait for L2 rather than DRAM
-    if (l + 1 < nlay && t < 16) {
+    if (l + 1 < nlay && t0 < 16) {
       const int64_t en = elem[tl * nlay + l + 1];
       const void* src = nullptr;
       uint32_t bytes = nn * 8;
-      if (t < 13) src = Mt + t * nloc + en * nn;
-      else if (t == 13) { src = gid + en * nn; bytes = nn * 4; }
-      else if (t == 14) { src = Mt_t + (int64_t)(l + 1) * ((nn + 1) & ~1); bytes = ((nn + 1) & ~1) * 8; }
+      if (t0 < 13) src = Mt + t0 * nloc + en * nn;
+      else if (t0 == 13) { src = gid + en * nn; bytes = nn * 4; }
+      else if (t0 == 14) { src = Mt_t + (int64_t)(l + 1) * ((nn + 1) & ~1); bytes = ((nn + 1) & ~1) * 8; }
       if (src && (bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
     }
     // ---- phase 2: line tasks (direction m, flux x, line); warp-uniform (m, x)
 #pragma unroll 1
-    for (int T = t; T < 15 * C::NL; T += blockDim.x) {
+    for (int T = t0; T < 15 * C::NL; T += blockDim.x) {
       const int m = T / (5 * C::NL), x = (T / C::NL) % 5, lam = T % C::NL;
       if (!((K.dirs >> m) & 1)) continue;
       int base, stride;
@@ -485,7 +496,12 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
     }
     __syncthreads();
     // ---- phase 3: element accumulator, then the column DSS
-    if (act) {
+#pragma unroll
+    for (int jn = 0; jn < NPT; ++jn) {
+      const int t = t0 + jn * NB;
+      if (t >= nn) continue;
+      const int i = t / (n * n), j = (t / n) % n, k = t % n;
+      const int na = i * PI + j * n + k;
       double acc[5];
       double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -497,7 +513,7 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
       acc[0] = -r[0];                                   // acc -= weak = acc + sum_a D[a,i] (w3 F)_a
       acc[4] = -r[1];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) acc[1 + c] = -(w * r[2 + c]) - extra[c];
+      for (int c = 0; c < 3; ++c) acc[1 + c] = -(w[jn] * r[2 + c]) - extra[jn][c];
       double* cw = s_carry + (l & 1) * n * n * 5 + (i * n + j) * 5;
       const double* cr = s_carry + ((l + 1) & 1) * n * n * 5 + (i * n + j) * 5;
       if (k == 0 && l > 0) {
@@ -512,7 +528,7 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::
         const int z = l * N + k;
         if (cd < 0) {
           const double mi = A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t];
-          double* o = A.out + (int64_t)g * A.ldo;
+          double* o = A.out + (int64_t)gn[jn] * A.ldo;
 #pragma unroll
           for (int f = 0; f < 5; ++f) o[f] = A.accumulate ? o[f] + mi * acc[f] : mi * acc[f];
         } else {
@@ -533,9 +549,18 @@ int run_lines(const double* Drow, const EulerConsts& K, int64_t nelem, const int
   hv::DTabEO<n> Dt;
   hv::fill_dtab_eo(Dt, Drow);
   using C = ElinesCfg<n>;
-  auto kern = euler_lines_kernel<n>;
-  HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-  kern<<<(unsigned)A.ntiles, ((C::nn + 31) / 32) * 32, C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
+  // one node per thread; HV_EULER_NPT=2 at N = 7: two (2 x 256 threads x 120 registers: both nodes' loads in
+  // flight together, but half the warps -- c4 Euler sweep 2.26 -> 2.87 ms, not taken)
+  const char* ev = getenv("HV_EULER_NPT");
+  if (n == 8 && ev && atoi(ev) == 2) {
+    auto kern = euler_lines_kernel<n, (n == 8 ? 2 : 1)>;
+    HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    kern<<<(unsigned)A.ntiles, C::nn / (n == 8 ? 2 : 1), C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
+  } else {
+    auto kern = euler_lines_kernel<n, 1>;
+    HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    kern<<<(unsigned)A.ntiles, ((C::nn + 31) / 32) * 32, C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
+  }
   HV_LAUNCH_CHECK();
   return HV_OK;
 }
