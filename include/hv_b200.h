@@ -116,7 +116,9 @@ int hv_viscous_metric(int N, int mode, const double* h_a, double b, const double
  * then G_nu = sum_m k_m e_m e_m^T (hyperdiff.py:80, k_m = nu_m vals_m = a_m / b) collapses to
  * k_h I + (k_v - k_h) e_3 e_3^T, e_3 the eigenvector of the largest eigenvalue of G (the same
  * Jacobi eigensolve as hv_viscous_metric), so W = w3 Jg G_nu = kh |u|^2 I + kd u u^T with
- * u = sqrt(w3 Jg[gid]) e_3: d_U (3, nelem*n^3) component-major, half the bytes of d_W (ncomp = 3).
+ * u = sqrt(w3 Jg[gid]) e_3.  ncomp = 3 writes d_U (3, nelem*n^3) component-major, half the bytes of
+ * d_W, as u' = sqrt(scale w3 Jg[gid]) e_3 with scale = |kd| (what a wform-1 plan expects: the sweep
+ * then forms (kh / kd) |u'|^2 d + u' (u' . d) and the sign of kd goes into the output scale).
  * Isotropic form (c_1 == c_2 == c_3, so k_v == k_h and G_nu = k_h I): ncomp = 1 writes
  * d_U[p] = scale * w3 Jg[gid] with scale = k_h, one double per node (no eigensolve).
  * Returns HV_ERR_DEGENERATE like hv_viscous_metric (ncomp = 3). */
@@ -162,7 +164,8 @@ typedef struct hv_lap_plan {
   double* d_recv;              /* (2*face, n_z, F) neighbour sums (NCCL receive buffer)        */
   /* form of d_Wt for the plane kernel (kernel == 1): 0 = the 6 components of W;
    * 1 = axis form (scaled mode with c_1 == c_2, hyperdiff.py:71-80: G_nu = k_h I + (k_v - k_h) e_3 e_3^T):
-   * u = sqrt(w3 Jg[gid]) e_3 (3 components, hv_viscous_axis) and W = kh |u|^2 I + kd u u^T;
+   * d_Wt holds u' = sqrt(|kd| w3 Jg[gid]) e_3 (3 components, hv_viscous_axis with scale = |kd|) and
+   * W = kh |u|^2 I + kd u u^T = sgn(kd) [(kh / kd) |u'|^2 I + u' u'^T]; kd != 0;
    * 2 = isotropic form (c_1 == c_2 == c_3): s = kh w3 Jg[gid] (1 component), W = s I */
   int wform;
   double kh, kd;

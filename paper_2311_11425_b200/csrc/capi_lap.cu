@@ -22,6 +22,7 @@ int check_plan(const hv_lap_plan* P) {
   if (P->nelem <= 0 || P->nglobal <= 0 || !P->d_gid || !P->d_off || !P->d_idx || !P->d_W || !P->d_Minv ||
       !P->d_work || !P->d_y)
     HV_FAIL(HV_ERR_INVALID, "incomplete laplacian plan");
+  if (P->wform == 1 && !(P->kd != 0.0)) HV_FAIL(HV_ERR_INVALID, "axis-form plan with kd == 0 (use the isotropic form)");
   return HV_OK;
 }
 
@@ -37,6 +38,13 @@ hv::TileArgs tile_args(const hv_lap_plan* P, const double* q, int64_t ldq, const
   A.slot_ext = P->d_slot_ext; A.ext_slots = P->d_ext_slots; A.next = P->d_slot_ext ? P->next : 0;
   A.face = P->face; A.send = P->d_send; A.recv = P->d_recv;
   A.wform = P->wform; A.kh = P->kh; A.kd = P->kd; A.Ms = P->d_Ms;
+  if (P->wform == 1) {
+    // axis form: d_Wt holds u' = sqrt(|kd| w3 Jg) e_3, so W = sgn(kd) [(kh / kd) |u'|^2 I + u' u'^T]:
+    // the sweep forms the bracket (one FP64 multiply less per node and field), the sign goes into
+    // the output scale
+    A.kh = P->kh / P->kd;
+    A.scale = (P->kd < 0.0) ? -scale : scale;
+  }
   A.io = 0; A.tper = P->d_tper; A.sv = P->d_sv; A.tchunk = P->d_tchunk; A.ng = P->nglobal;
   A.seg = P->seg; A.bnd = P->d_bnd; A.prow = P->d_prow;
   return A;

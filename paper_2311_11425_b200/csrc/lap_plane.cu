@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     if (run && WF == 1) {
       // axis form: [c][i][k][e][j]; the F field lanes of a plane read the same u (broadcast)
       const double* Uw = s_w + e * n + jp;
-      const double kh = A.kh, kd = A.kd;
+      const double kh = A.kh;   // kh / kd: u is scaled by sqrt(|kd|), the sign of kd is in A.scale (capi_lap.cu)
       constexpr int CS = n * n * NE * n;
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
             const int k = k0 + kk;
             const double d0 = p0[r][k], d2 = p2[r][k];
             const double hs = kh * (u0[kk] * u0[kk] + u1[kk] * u1[kk] + u2[kk] * u2[kk]);
-            const double tv = kd * (u0[kk] * d0 + u1[kk] * d1[kk] + u2[kk] * d2);
+            const double tv = u0[kk] * d0 + u1[kk] * d1[kk] + u2[kk] * d2;
             p0[r][k] = hs * d0 + tv * u0[kk];
             s_s[sidx(e, i, jp, k)] = hs * d1[kk] + tv * u1[kk];
             p2[r][k] = hs * d2 + tv * u2[kk];

@@ -206,6 +206,7 @@ struct ViscParams {
   double a[3];
   double b;
   double nu[3];
+  double uscale;   // axis form: u = sqrt(uscale w3 Jg) e_3
 };
 
 // Per element node: G = grad grad^T -> eigh -> nu (hyperdiff.py:54-79) ->
@@ -261,8 +262,8 @@ __global__ void viscous_kernel(int nn, ViscParams P, const double* __restrict__ 
 #pragma unroll
       for (int m = 0; m < 3; ++m) evec_out[p * 9 + c * 3 + m] = V[c][m];
   }
-  if (U_out) {   // axis form (hv_viscous_axis): u = sqrt(w3 Jg) e_3, e_3 = eigenvector of the largest eigenvalue
-    const double su = sqrt(w3[r] * Jg[gid[p]]);
+  if (U_out) {   // axis form (hv_viscous_axis): u = sqrt(uscale w3 Jg) e_3, e_3 = eigenvector of the largest eigenvalue
+    const double su = sqrt(P.uscale * (w3[r] * Jg[gid[p]]));
 #pragma unroll
     for (int c = 0; c < 3; ++c) U_out[c * nloc + p] = su * V[c][2];
   }
@@ -420,6 +421,7 @@ extern "C" int hv_viscous_axis(int N, const double* d_grad, int64_t nelem, const
   }
   ViscParams P{};
   P.mode = 1;   // the eigenvectors only; nu unused
+  P.uscale = scale > 0.0 ? scale : 1.0;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = reset_flags(st);
   if (rc) return rc;

@@ -189,13 +189,14 @@ class EulerOps:
                 wform = 0
                 if ax is not None and ax[1] == 0.0 and wf != "1":
                     wform = 2
-                elif ax is not None and (dev.N <= 4 or wf == "1"):
+                elif ax is not None and ax[1] != 0.0 and (dev.N <= 4 or wf == "1"):
                     wform = 1
                 ncomp = {0: 6, 1: 3, 2: 1}[wform]
                 wl = (_lib.lib().hv_plane_metric_doubles(dev.N, tp.TX, tp.TY, wform) if layout == 1
                       else 6 * n * tp.NE * n * n)
                 Wt = torch.empty(tp.ntiles * tp.nlay * wl, dtype=torch.float64, device="cuda")
-                src = viscous.packed_axis(self.metrics.d_Jg, ncomp, ax[0]) if wform else W
+                # isotropic: s = kh w3 Jg; axis: u = sqrt(|kd| w3 Jg) e_3 (the sweep then needs no kd multiply)
+                src = viscous.packed_axis(self.metrics.d_Jg, ncomp, ax[0] if wform == 2 else abs(ax[1])) if wform else W
                 _lib.check(_lib.lib().hv_tile_pack_metric(dev.N, tp.TX, tp.TY, tp.ntiles, tp.nlay,
                                                           d["elem"].data_ptr(), src.data_ptr(), dev.nloc,
                                                           wform + 1 if wform else layout, Wt.data_ptr(),

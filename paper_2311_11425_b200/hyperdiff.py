@@ -120,7 +120,7 @@ class ViscousMetric:
         return kh, float(a[2]) / float(b) - kh
 
     def packed_axis(self, d_Jg, ncomp=3, scale=1.0):
-        """Axis form u = sqrt(w3 Jg[gid]) e_3 (3, nloc), or (ncomp=1, isotropic case) s = scale w3 Jg[gid]
+        """Axis form u = sqrt(scale w3 Jg[gid]) e_3 (3, nloc), or (ncomp=1, isotropic case) s = scale w3 Jg[gid]
         (1, nloc), for the plane kernel (hv_viscous_axis); not cached (the plan keeps only its
         tile-ordered copy)."""
         torch = torch_mod()
