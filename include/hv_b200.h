@@ -49,6 +49,10 @@ int64_t hv_launch_count(void);
  * chains of `iters` dependent FP64 FMAs (2 * 8 * iters * blocks * threads FLOPs); bench.py times it
  * with CUDA events for the measured FP64 peak.  d_out: >= blocks * threads doubles. */
 int hv_probe_dfma(double* d_out, int64_t iters, int blocks, int threads, void* stream);
+/* Test probe, not on the operator path: d_out[i] = x_i^y with the power function the Euler kernels use
+ * for the equation of state (state.py:84-101 calls numpy's power; csrc/hv_pow.cuh: <= 1 ulp for positive
+ * normal x, the library pow otherwise). */
+int hv_probe_pow(int64_t n, const double* d_x, double y, double* d_out, void* stream);
 
 /* ---------------------------------------------------------------- host mesh
  * Replaces Mesh._number_gridpoints (mesh.py:86-107): bit-exact gid

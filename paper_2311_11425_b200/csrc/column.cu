@@ -24,6 +24,7 @@
 #include <cmath>
 
 #include "hv_common.h"
+#include "hv_pow.cuh"
 #include "lap_common.cuh"
 
 namespace {
@@ -104,8 +105,8 @@ __global__ void __launch_bounds__(256) column_jacobian_kernel(hv::DTab<n> Dt, hv
     cmass[z] = m;
     const double rho = qv[0];
     double P;
-    if (K.set == 0) P = K.P_A * pow(rho * K.R * qv[4] / K.P_A, K.gamma);
-    else if (K.set == 1) P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+    if (K.set == 0) P = K.P_A * hv::pow_pos(rho * K.R * qv[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * hv::pow_pos(K.R * qv[4] / K.P_A, K.gamma);
     else {
       const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
       P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "hv_common.h"
+#include "hv_pow.cuh"
 #include "lap_common.cuh"
 #include "lap_tile.cuh"
 
@@ -132,8 +133,8 @@ __device__ __forceinline__ void euler_node_acc(const hv::DTab<n>& Dt, const Eule
     if (K.set == 2) phi = Mt[M_PHI * nloc + p];   // the geopotential enters the 3C pressure only
     const double rho = qv[0];
     // EOS (state.py:84-101), reference expression order
-    if (K.set == 0) P = K.P_A * pow(qv[0] * K.R * qv[4] / K.P_A, K.gamma);
-    else if (K.set == 1) P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+    if (K.set == 0) P = K.P_A * hv::pow_pos(qv[0] * K.R * qv[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * hv::pow_pos(K.R * qv[4] / K.P_A, K.gamma);
     else {
       const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
       P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);
@@ -353,6 +354,25 @@ __global__ void __launch_bounds__(512, (n >= 8 ? 2 : 1)) euler_tile_kernel(hv::D
 //            same on-chip DSS / carry / partial rows as euler_tile_kernel
 // Flux arrays: node (i, j, k) at i*PI + j*n + k with PI = n*n + 1, so the half-warps of phase 1 / 3 and
 // of the i- and k-direction lines hit 16 distinct banks (the j-direction lines: 2-way).
+// A row of 5 doubles at element offset 5 r of a 16-byte aligned array (state / output rows, 5-wide
+// partial rows): 40 bytes, 16-byte aligned when r is even, 8 bytes past that when r is odd -- one
+// 8-byte and two 16-byte accesses instead of five 8-byte ones, the same instructions for both parities
+__device__ __forceinline__ void ld_row5(const double* row, bool odd, double (&v)[5]) {
+  const double a = row[odd ? 0 : 4];
+  const double2 b = *reinterpret_cast<const double2*>(row + (odd ? 1 : 0));
+  const double2 c = *reinterpret_cast<const double2*>(row + (odd ? 3 : 2));
+  v[0] = odd ? a : b.x;
+  v[1] = odd ? b.x : b.y;
+  v[2] = odd ? b.y : c.x;
+  v[3] = odd ? c.x : c.y;
+  v[4] = odd ? c.y : a;
+}
+__device__ __forceinline__ void st_row5(double* row, bool odd, const double (&v)[5]) {
+  row[odd ? 0 : 4] = odd ? v[0] : v[4];
+  *reinterpret_cast<double2*>(row + (odd ? 1 : 0)) = odd ? make_double2(v[1], v[2]) : make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(row + (odd ? 3 : 2)) = odd ? make_double2(v[3], v[4]) : make_double2(v[2], v[3]);
+}
+
 template <int n>
 struct ElinesCfg {
   static constexpr int nn = n * n * n, PI = n * n + 1, FS = ((n - 1) * PI + (n - 1) * n + n + 1) & ~1;
@@ -360,7 +380,15 @@ struct ElinesCfg {
   static constexpr int OFF_C = 15 * FS;               // carry [2][n*n][5]
   static constexpr int OFF_CF = OFF_C + 2 * n * n * 5;   // even-odd coefficients (hv::EOSmem)
   static constexpr int OFF_CODE = OFF_CF + 2 * hv::EOSmem<n>::PER;
-  static constexpr size_t SMEM = sizeof(double) * (OFF_CODE + (n * n + 1) / 2);
+  static constexpr int OFF_EL = OFF_CODE + (n * n + 1) / 2;   // element of every layer of the column (int, <= 256 layers)
+  // staged variant (bulk copies need 16-byte multiples: even n): the next layer's grad xi / eta / zeta
+  // and Jg rows (10 x n^3 doubles) and its gids, one mbarrier
+  static constexpr bool STG = (n % 2 == 0) && (n * n * n * 4) % 16 == 0;
+  static constexpr int NST = 10;
+  static constexpr int OFF_ST = (OFF_EL + 128 + 1) & ~1;
+  static constexpr int OFF_G = OFF_ST + (STG ? NST * nn : 0);
+  static constexpr int OFF_BAR = OFF_G + (STG ? (nn + 1) / 2 : 0);
+  static constexpr size_t SMEM = sizeof(double) * (OFF_BAR + (STG ? 2 : 0));
 };
 
 // NPT nodes per thread (blockDim = n^3 / NPT): NPT = 2 gives each thread twice the registers (2 x 256
@@ -386,12 +414,64 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
   const int nlay = A.nlay;
   const int64_t nloc = nelem * nn;
   for (int x = t0; x < n * n; x += blockDim.x) s_code[x] = A.code[tl * n * n + x];
+  // the column's elements in shared memory and the next layer's gids in registers: a layer's phase 1
+  // then starts with the q-row loads instead of the chain elem -> gid -> q row
+  int* s_el = reinterpret_cast<int*>(sm + C::OFF_EL);
+  for (int x = t0; x < nlay; x += blockDim.x) s_el[x] = elem[tl * nlay + x];
   const double* Mt_t = A.Mt + tl * (int64_t)nlay * (((nn + 1) & ~1));
+  constexpr bool STG = C::STG;
+  // 16-byte row accesses (ld_row5 / st_row5) when the rows are 5 wide and the arrays 16-byte aligned
+  const bool vq = ldq == 5 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  const bool vo = A.ldo == 5 && (reinterpret_cast<uintptr_t>(A.out) & 15) == 0 && (reinterpret_cast<uintptr_t>(A.part) & 15) == 0;
+  const double* s_m = sm + C::OFF_ST;                    // [NST][nn] staged record rows of the current layer
+  const int* s_g = reinterpret_cast<const int*>(sm + C::OFF_G);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  // layer le's rows 0..9 of the record (grad xi, eta, zeta; Jg) and gids -> the stage: 11 bulk copies on
+  // one mbarrier phase, ~43 KB in flight per CTA while the previous layer's phases 2 and 3 run (the
+  // per-thread loads they replace kept ~4 loads in flight per thread: latency-bound at 2.9 TB/s)
+  auto issue_stage = [&](int64_t en) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"((uint32_t)(C::NST * nn * 8 + nn * 4))
+                 : "memory");
+#pragma unroll 1
+    for (int c = 0; c < C::NST; ++c)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(s_m + c * nn)),
+                   "l"(Mt + c * nloc + en * nn), "r"((uint32_t)(nn * 8)), "r"(b)
+                   : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(s_g)),
+                 "l"(gid + en * nn), "r"((uint32_t)(nn * 4)), "r"(b)
+                 : "memory");
+  };
+  if constexpr (STG) {
+    if (t0 == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   double w[NPT];
+  int gnx[NPT];                                          // gids of the next layer's nodes (unstaged variant)
 #pragma unroll
-  for (int jn = 0; jn < NPT; ++jn) w[jn] = (t0 + jn * NB < nn) ? w3[t0 + jn * NB] : 0.0;
+  for (int jn = 0; jn < NPT; ++jn) {
+    w[jn] = (t0 + jn * NB < nn) ? w3[t0 + jn * NB] : 0.0;
+    gnx[jn] = (!STG && t0 + jn * NB < nn) ? gid[(int64_t)elem[tl * nlay] * nn + t0 + jn * NB] : 0;
+  }
+  __syncthreads();
+  if constexpr (STG) {
+    if (t0 == 0) issue_stage(s_el[0]);
+  }
   for (int l = 0; l < nlay; ++l) {
-    const int64_t e = elem[tl * nlay + l];
+    const int64_t e = s_el[l];
+    if constexpr (STG) {   // this layer's stage has landed
+      const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar), par = (uint32_t)(l & 1);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(b), "r"(par)
+                     : "memory");
+    }
     double extra[NPT][3];                                // geopotential + Coriolis terms of acc[1..3]
     int gn[NPT];
     // ---- phase 1 (euler_node_acc's fluxes, reference expression order), node t = t0 + jn * NB
@@ -405,17 +485,22 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       extra[jn][0] = extra[jn][1] = extra[jn][2] = 0.0;
       gn[jn] = 0;
       if (!act) continue;
-      const int g = gid[p];
+      const int g = STG ? s_g[t] : gnx[jn];
       gn[jn] = g;
+      if (!STG && l + 1 < nlay) gnx[jn] = gid[(int64_t)s_el[l + 1] * nn + t];
       double qv[5];
+      if (vq) {
+        ld_row5(q + (int64_t)g * 5, g & 1, qv);
+      } else {
 #pragma unroll
-      for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
-      const double Jg = Mt[9 * nloc + p];
+        for (int f = 0; f < 5; ++f) qv[f] = q[(int64_t)g * ldq + f];
+      }
+      const double Jg = STG ? s_m[9 * nn + t] : Mt[9 * nloc + p];
       const double mask = ((l == 0 && k == 0) || (l == nlay - 1 && k == n - 1)) ? 0.0 : 1.0;
       const double rho = qv[0];
       double P;
       if (K.set == 1) {
-        P = K.P_A * pow(K.R * qv[4] / K.P_A, K.gamma);
+        P = K.P_A * hv::pow_pos(K.R * qv[4] / K.P_A, K.gamma);
       } else {
         const double phi = Mt[14 * nloc + p];
         const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
@@ -428,7 +513,7 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       for (int m = 0; m < 3; ++m) {
         double gm[3];
 #pragma unroll
-        for (int c = 0; c < 3; ++c) gm[c] = Mt[(m * 3 + c) * nloc + p];
+        for (int c = 0; c < 3; ++c) gm[c] = STG ? s_m[(m * 3 + c) * nn + t] : Mt[(m * 3 + c) * nloc + p];
         double un = (gm[0] * qv[1] + gm[1] * qv[2] + gm[2] * qv[3]) / rho;
         if (m == 2) un = un * mask;
         const double jun = Jg * un;
@@ -453,7 +538,7 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
         } else {
           double gz[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) gz[c] = Mt[(6 + c) * nloc + p];
+          for (int c = 0; c < 3; ++c) gz[c] = STG ? s_m[(6 + c) * nn + t] : Mt[(6 + c) * nloc + p];
           const double zn = sqrt(gz[0] * gz[0] + gz[1] * gz[1] + gz[2] * gz[2]);
 #pragma unroll
           for (int c = 0; c < 3; ++c) ev[c] = gz[c] / zn;
@@ -468,12 +553,18 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
     __syncthreads();
     // the next layer's element record (13 metric components, gids, Minv) -> L2, so that its phase-1
     // loads wait for L2 rather than DRAM
+    if constexpr (STG) {
+      if (t0 == 32 && l + 1 < nlay) {   // the stage is free: every thread is past its phase-1 reads
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_stage(s_el[l + 1]);
+      }
+    }
     if (l + 1 < nlay && t0 < 16) {
-      const int64_t en = elem[tl * nlay + l + 1];
+      const int64_t en = s_el[l + 1];
       const void* src = nullptr;
       uint32_t bytes = nn * 8;
-      if (t0 < 13) src = Mt + t0 * nloc + en * nn;
-      else if (t0 == 13) { src = gid + en * nn; bytes = nn * 4; }
+      if (t0 < 13) { if (!STG || t0 >= C::NST) src = Mt + t0 * nloc + en * nn; }
+      else if (t0 == 13) { if (!STG) { src = gid + en * nn; bytes = nn * 4; } }
       else if (t0 == 14) { src = Mt_t + (int64_t)(l + 1) * ((nn + 1) & ~1); bytes = ((nn + 1) & ~1) * 8; }
       if (src && (bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -526,15 +617,26 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       } else {
         const int cd = s_code[i * n + j];
         const int z = l * N + k;
-        if (cd < 0) {
-          const double mi = A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t];
-          double* o = A.out + (int64_t)gn[jn] * A.ldo;
+        // one store path for both kinds of node: the final row M^-1 acc of a node the column owns, or
+        // the raw sums into its 5-wide partial row (perimeter nodes; slot_fixup sums them)
+        const bool fin = cd < 0;
+        const int64_t r = fin ? (int64_t)gn[jn] : (int64_t)cd * A.n_z + z;
+        double* o = fin ? A.out + r * A.ldo : A.part + r * 5;
+        const double mi = fin ? A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t] : 1.0;
+        double v[5];
 #pragma unroll
-          for (int f = 0; f < 5; ++f) o[f] = A.accumulate ? o[f] + mi * acc[f] : mi * acc[f];
+        for (int f = 0; f < 5; ++f) v[f] = fin ? mi * acc[f] : acc[f];
+        if (vo) {
+          if (A.accumulate && fin) {
+            double pv[5];
+            ld_row5(o, r & 1, pv);
+#pragma unroll
+            for (int f = 0; f < 5; ++f) v[f] = pv[f] + v[f];
+          }
+          st_row5(o, r & 1, v);
         } else {
-          double* o = A.part + ((int64_t)cd * A.n_z + z) * 5;
 #pragma unroll
-          for (int f = 0; f < 5; ++f) o[f] = acc[f];
+          for (int f = 0; f < 5; ++f) o[f] = (A.accumulate && fin) ? o[f] + v[f] : v[f];
         }
       }
     }
@@ -572,7 +674,7 @@ int run_tile(const double* Drow, const EulerConsts& K, int64_t nelem, const int3
   // 2C / 3C at N >= 4: the line-task kernel (HV_EULER_LINES=0 keeps the per-node line sums)
   if constexpr (n >= 5) {
     const char* ev = getenv("HV_EULER_LINES");
-    if (K.set != 0 && !(ev && atoi(ev) == 0)) return run_lines<n>(Drow, K, nelem, gid, w3, Mt, q, ldq, A, elem, st);
+    if (K.set != 0 && A.nlay <= 256 && !(ev && atoi(ev) == 0)) return run_lines<n>(Drow, K, nelem, gid, w3, Mt, q, ldq, A, elem, st);
   }
   hv::DTab<n> Dt;
   hv::fill_dtab(Dt, Drow);
@@ -700,12 +802,12 @@ __global__ void euler_vertical_kernel(hv::DTab<n> Dt, EulerConsts K, hv::DTab<n>
       phi[i] = Phi_g[g[i]];
       const double rho = qv[i][0];
       if (K.set == 0) {
-        P[i] = K.P_A * pow(qv[i][0] * K.R * qv[i][4] / K.P_A, K.gamma);
+        P[i] = K.P_A * hv::pow_pos(qv[i][0] * K.R * qv[i][4] / K.P_A, K.gamma);
         uz[i] = msk[i] * (qv[i][1] * z[i][0] + qv[i][2] * z[i][1] + qv[i][3] * z[i][2]);
         tf[i] = 0.0;
       } else {
         if (K.set == 1) {
-          P[i] = K.P_A * pow(K.R * qv[i][4] / K.P_A, K.gamma);
+          P[i] = K.P_A * hv::pow_pos(K.R * qv[i][4] / K.P_A, K.gamma);
         } else {
           const double ke = 0.5 * (qv[i][1] * qv[i][1] + qv[i][2] * qv[i][2] + qv[i][3] * qv[i][3]) / rho;
           P[i] = (K.gamma - 1.0) * (qv[i][4] - ke - rho * phi[i]);
@@ -846,8 +948,8 @@ __global__ void __launch_bounds__(DIAG_T) diag_partial_kernel(EulerConsts K, dou
     const double* r = q + g * 5;
     const double rho = r[0], m = Mm[g], phi = Phi[g];
     double P;
-    if (K.set == 0) P = K.P_A * pow(rho * K.R * r[4] / K.P_A, K.gamma);
-    else if (K.set == 1) P = K.P_A * pow(K.R * r[4] / K.P_A, K.gamma);
+    if (K.set == 0) P = K.P_A * hv::pow_pos(rho * K.R * r[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * hv::pow_pos(K.R * r[4] / K.P_A, K.gamma);
     else {
       const double kk = 0.5 * (r[1] * r[1] + r[2] * r[2] + r[3] * r[3]) / rho;
       P = (K.gamma - 1.0) * (r[4] - kk - rho * phi);
@@ -875,8 +977,8 @@ __global__ void __launch_bounds__(DIAG_T) diag_partial_kernel(EulerConsts K, dou
     const int64_t g = col_gid[c * n_z];
     const double* r = q + g * 5;
     double P;
-    if (K.set == 0) P = K.P_A * pow(r[0] * K.R * r[4] / K.P_A, K.gamma);
-    else if (K.set == 1) P = K.P_A * pow(K.R * r[4] / K.P_A, K.gamma);
+    if (K.set == 0) P = K.P_A * hv::pow_pos(r[0] * K.R * r[4] / K.P_A, K.gamma);
+    else if (K.set == 1) P = K.P_A * hv::pow_pos(K.R * r[4] / K.P_A, K.gamma);
     else {
       const double kk = 0.5 * (r[1] * r[1] + r[2] * r[2] + r[3] * r[3]) / r[0];
       P = (K.gamma - 1.0) * (r[4] - kk - r[0] * Phi[g]);

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "hv_common.h"
+#include "hv_pow.cuh"
 
 namespace {
 
@@ -26,7 +27,19 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* out, int64_t it
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = s;
 }
 
+__global__ void pow_probe_kernel(int64_t n, const double* __restrict__ x, double y, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = hv::pow_pos(x[i], y);
+}
+
 }  // namespace
+
+extern "C" int hv_probe_pow(int64_t n, const double* d_x, double y, double* d_out, void* stream) {
+  if (n <= 0 || !d_x || !d_out) HV_FAIL(HV_ERR_INVALID, "hv_probe_pow: bad arguments");
+  pow_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, d_x, y, d_out);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
 
 extern "C" int hv_probe_dfma(double* d_out, int64_t iters, int blocks, int threads, void* stream) {
   if (!d_out || iters <= 0 || blocks <= 0 || threads <= 0 || threads > 256)

@@ -576,3 +576,27 @@ def test_laplacian_leaves_unlisted_columns(case):
     assert np.all(got[:, 0] == 7.0)
     ref = hyperdiff.laplacian_apply_fields(q, p.vm, p.ops, (1, 2, 3, 4)).cpu().numpy()
     assert np.array_equal(got[:, 1:], ref[:, 1:])
+
+
+def test_eos_power_device():
+    """The power function of the Euler kernels' equation of state (csrc/hv_pow.cuh; state.py:84-101 uses
+    numpy's power, i.e. glibc pow): within 1 ulp of numpy over the EOS range and far outside it, and
+    the library pow for arguments outside the fast path (zero, subnormal, huge exponents)."""
+    import torch
+
+    from paper_2311_11425_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    x = np.concatenate([0.5 + 1.5 * rng.random(200000), np.exp((rng.random(200000) * 2 - 1) * 200.0),
+                        [0.0, 1e-320, 1e-200, 1e200, np.inf, 1.0]])
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    for y in (1.4, 1004.5 / 717.5, -1.4, 0.5):
+        _lib.check(_lib.lib().hv_probe_pow(x.size, xd.data_ptr(), y, out.data_ptr(), _lib.stream_handle()))
+        got = out.cpu().numpy()
+        with np.errstate(divide="ignore", over="ignore"):
+            ref = np.power(x, y)
+        fin = np.isfinite(ref) & (ref != 0)
+        assert np.array_equal(got[~fin], ref[~fin])
+        ulp = np.abs(got[fin] - ref[fin]) / np.spacing(np.abs(ref[fin]))
+        assert ulp.max() <= 1.0, (y, ulp.max())
