@@ -11,6 +11,9 @@ resident, result returned as a CUDA tensor).
 from __future__ import annotations
 
 import ctypes as C
+import os
+import weakref
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -180,6 +183,41 @@ def _as_device(x):
     return x.contiguous(), False
 
 
+# Small meshes (configs 1 and 2) are launch-bound: an op is 2-4 kernels of 10-40 us each, about the
+# cost of the Python / ctypes call that enqueues them.  The second time an op is asked for with the same
+# plan and the same buffers it is captured into a CUDA graph, and replayed from then on.  A graph
+# depends only on pointers (the caller's arrays and the plan's own buffers, kept alive by ``ops``), so
+# a key hit is always valid while ``ops`` lives; HV_GRAPH=0 disables, HV_GRAPH_MAX is the node bound.
+_GRAPHS = OrderedDict()
+_GRAPH_CAP = 16
+
+
+def _run_graphed(ops, key, launch):
+    torch = torch_mod()
+    if (ops.mesh.nglobal > int(os.environ.get("HV_GRAPH_MAX", 1 << 20)) or os.environ.get("HV_GRAPH", "1") == "0"
+            or torch.cuda.is_current_stream_capturing()):
+        launch()
+        return
+    key = (id(ops),) + key
+    ent = _GRAPHS.get(key)
+    if ent is not None and ent[0]() is not ops:      # a dead EulerOps whose id was reused
+        ent = None
+    if ent is None:
+        launch()
+        _GRAPHS[key] = (weakref.ref(ops), None)
+        while len(_GRAPHS) > _GRAPH_CAP:
+            _GRAPHS.popitem(last=False)
+        return
+    _GRAPHS.move_to_end(key)
+    g = ent[1]
+    if g is None:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            launch()
+        _GRAPHS[key] = (ent[0], g)
+    g.replay()
+
+
 def laplacian_apply(field_g, viscous, ops):
     """M^-1 DSS(-L_nu q), one field (hyperdiff.py:84-94)."""
     torch = torch_mod()
@@ -189,8 +227,9 @@ def laplacian_apply(field_g, viscous, ops):
     plan = ops.lap_plan(viscous)
     out = torch.empty_like(q)
     qf = (C.c_int32 * 1)(0)
-    _lib.check(_lib.lib().hv_laplacian(C.byref(plan), q.data_ptr(), 1, 1, qf, out.data_ptr(), 1, qf, 1.0,
-                                       _lib.stream_handle()))
+    _run_graphed(ops, ("lap1", id(plan), q.data_ptr(), out.data_ptr()), lambda: _lib.check(
+        _lib.lib().hv_laplacian(C.byref(plan), q.data_ptr(), 1, 1, qf, out.data_ptr(), 1, qf, 1.0,
+                                _lib.stream_handle())))
     return out.cpu().numpy() if host else out
 
 
@@ -203,8 +242,10 @@ def laplacian_apply_fields(q, viscous, ops, fields):
     full = qd.dim() == 2 and sorted(fields) == list(range(qd.shape[1]))
     out = torch.empty_like(qd) if full else torch.zeros_like(qd)
     fl = (C.c_int32 * len(fields))(*fields)
-    _lib.check(_lib.lib().hv_laplacian(C.byref(plan), qd.data_ptr(), qd.shape[1], len(fields), fl, out.data_ptr(),
-                                       qd.shape[1], fl, 1.0, _lib.stream_handle()))
+    _run_graphed(ops, ("lapf", id(plan), qd.data_ptr(), out.data_ptr(), qd.shape[1], tuple(fields), full),
+                 lambda: _lib.check(_lib.lib().hv_laplacian(
+                     C.byref(plan), qd.data_ptr(), qd.shape[1], len(fields), fl, out.data_ptr(), qd.shape[1], fl,
+                     1.0, _lib.stream_handle())))
     return out.cpu().numpy() if host else out
 
 
@@ -222,7 +263,9 @@ def hyperdiffusion_apply(state, cfg, viscous, ops, out=None, accumulate=False):
     if out is None:
         out = torch.empty_like(q)
     vars_ = (C.c_int32 * len(cfg.variables))(*cfg.variables)
-    _lib.check(_lib.lib().hv_hyperdiffusion(C.byref(plan), q.data_ptr(), q.shape[1], len(cfg.variables), vars_,
-                                            cfg.alpha, out.data_ptr(), out.shape[1], int(bool(accumulate)),
-                                            _lib.stream_handle()))
+    _run_graphed(ops, ("hnu", id(plan), q.data_ptr(), q.shape[1], out.data_ptr(), out.shape[1], tuple(cfg.variables),
+                       cfg.alpha, bool(accumulate)),
+                 lambda: _lib.check(_lib.lib().hv_hyperdiffusion(
+                     C.byref(plan), q.data_ptr(), q.shape[1], len(cfg.variables), vars_, cfg.alpha, out.data_ptr(),
+                     out.shape[1], int(bool(accumulate)), _lib.stream_handle())))
     return out.cpu().numpy() if host else out

@@ -600,3 +600,33 @@ def test_eos_power_device():
         assert np.array_equal(got[~fin], ref[~fin])
         ulp = np.abs(got[fin] - ref[fin]) / np.spacing(np.abs(ref[fin]))
         assert ulp.max() <= 1.0, (y, ulp.max())
+
+
+def test_small_mesh_graph_replay():
+    """Small meshes replay a captured CUDA graph from the third call with the same plan and buffers
+    (hyperdiff._run_graphed): the replays read the buffers' current contents and give the first
+    call's bits; HV_GRAPH=0 (no capture) gives the same."""
+    import torch
+
+    from oracle_cases import OracleProblem
+    from product_cases import ProductProblem
+    from paper_2311_11425_b200 import hyperdiff, state
+
+    p = ProductProblem("box_p_n4")
+    o = OracleProblem("box_p_n4")
+    q = torch.from_numpy(o.state).cuda()
+    out = torch.empty_like(q)
+    st = state.StateField("2C", q)
+    hyperdiff._GRAPHS.clear()
+    first = hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops, out=out).clone()
+    assert rel_l2(first.cpu().numpy(), o.hyper()) <= TOL
+    for _ in range(3):
+        out.fill_(float("nan"))
+        hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops, out=out)
+        assert torch.equal(out, first)
+    assert any(g is not None for _, g in hyperdiff._GRAPHS.values())
+    q.mul_(2.0)                                   # a replay reads the new contents
+    hyperdiff.hyperdiffusion_apply(st, p.cfg, p.vm, p.ops, out=out)
+    assert torch.equal(out, 2.0 * first)
+    lap = [hyperdiff.laplacian_apply_fields(q, p.vm, p.ops, (0, 1, 2, 3, 4)) for _ in range(4)]
+    assert all(torch.equal(x, lap[0]) for x in lap[1:])
