@@ -101,21 +101,8 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
   double mi;
   double* o;
   if (id < nsi) {
-    if (row_mode == 3) {
-      // the slot rows of the tile-ordered intermediate, in their own order (lap_tile.cuh: [nslot][F] for
-      // z = 0, then per layer block [nslot][N][F]): thread id writes row id
-      if (id < A.nslot) {
-        s = id;
-        z = 0;
-      } else {
-        const int64_t r = id - A.nslot, lb = r / (A.nslot * N), w = r - lb * (A.nslot * N);
-        s = w / N;
-        z = (int)(lb * N + 1 + (w - s * N));
-      }
-    } else {
-      s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
-      z = (int)((unsigned)id - (unsigned)s * nz);
-    }
+    s = (unsigned)id / nz;       // nslot * n_z < 2^31 (checked by the launcher)
+    z = (int)((unsigned)id - (unsigned)s * nz);
     g = A.col_gid[(int64_t)A.slot_col[s] * A.n_z + z];
     mi = A.Ms ? __ldg(A.Ms + s * A.n_z + z) : __ldg(A.Minv + g);
     const int zb = (nseg > 1) ? A.seg * N : 0;
@@ -151,7 +138,11 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
     for (int ff = 0; ff < F; ++ff) acc[ff] = lo[ff] + hi[ff];
   }
   if (row_mode == 3) {
-    o = A.sv + id * F;
+    // the slot rows of the tile-ordered intermediate (lap_tile.cuh: [nslot][F] for z = 0, then per layer
+    // block [nslot][N][F]); threads walk a column's levels (its partial rows are read as contiguous runs,
+    // the slot rows written as 128-byte pieces)
+    const int64_t row = (z == 0) ? s : A.nslot + (((int64_t)((z - 1) / N) * A.nslot + s) * N + (z - 1) % N);
+    o = A.sv + row * F;
   } else {
     o = A.out + (int64_t)g * A.ldo;
   }
