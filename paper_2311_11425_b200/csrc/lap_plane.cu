@@ -831,6 +831,10 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     int gf[PF];
     double mf[PF];
     double my[C::PFY];   // IO 1: scale * Minv of tile-owned block items, 1 for perimeter (raw partial sums)
+    // IO 1 / 3: the items' columns (7 bits each, bit 7 = tile-owned) stay packed in one register from here
+    // to step f, which then starts at the element-copy offsets instead of the chain s_perm -> s_ct
+    static_assert(!OUT_YT || (UV < 128 && C::PFY <= 4), "packed item columns");
+    unsigned uvp = 0;
     if constexpr (OUT_YT) {
 #pragma unroll
       for (int it = 0; it < C::PFY; ++it) {
@@ -838,7 +842,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         my[it] = 1.0;
         if (qi < C::FIY) {
           const int uv = s_perm[qi / N], k = qi % N;
-          if (s_code[uv] < 0) my[it] = A.scale * __ldg(Mt_t + (int64_t)l * C::MTS + uv * n + k);
+          const bool own = s_code[uv] < 0;
+          uvp |= (unsigned)(uv | (own ? 0x80 : 0)) << (8 * it);
+          if (own) my[it] = __ldg(Mt_t + (int64_t)l * C::MTS + uv * n + k);   // scaled at its use in step f
         }
       }
     } else {
@@ -882,17 +888,19 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       for (int it = 0; it < C::PFY; ++it) {
         const int qi = tid + it * C::NT;
         if (qi >= C::FIY) continue;
-        const int uv = s_perm[qi / N], k = qi % N, u = uv / V, v = uv - u * V;
+        const unsigned ub = (uvp >> (8 * it)) & 0xffu;
+        const int uv = (int)(ub & 0x7fu), k = qi % N, u = uv / V, v = uv - u * V;
         const int4 ct = s_ct[uv];
+        const bool own = (ub & 0x80u) != 0;
+        const double ms = own ? A.scale * my[it] : 1.0;
         hv::Vec<F> val;
 #pragma unroll
         for (int p = 0; p < F; ++p) {
-          val.v[p] = my[it] * csum(ct, s_s + p * C::SP + k);
+          val.v[p] = ms * csum(ct, s_s + p * C::SP + k);
           yb[k * C::YLS + p * C::YFS + u * C::YUS + v] = val.v[p];
         }
-        const int cd = s_code[uv];
-        if (cd >= 0) {
-          double* o = A.part + ((int64_t)cd * A.n_z + l * N + k) * F;
+        if (!own) {
+          double* o = A.part + ((int64_t)s_code[uv] * A.n_z + l * N + k) * F;
           st_v2(o, val.v[0], val.v[1]);
           st_v2(o + 2, val.v[2], val.v[3]);
         }
