@@ -561,6 +561,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         }
 #pragma unroll
         for (int k = 0; k < n; ++k) p0[r][k] = ql[k];   // q plane, xi-differentiated below
+        if constexpr (IO == 3) {
+          // level N of layer l is level 0 of layer l + 1: the plane owners hold it, so they fill plane
+          // (l+1)&1 (unused during layer l) before the row buffer is refilled -- the tile's 81 columns
+          // are the union of the elements' plane rows (shared edges written twice, same value)
+          if (l + 1 < nlay)
+            s_q[C::QB_P + ((l + 1) & 1) * C::YLS + f * C::YFS + (px * N + I0 + r) * C::YUS + py * N + jp] = ql[N];
+        }
       }
 #pragma unroll
       for (int k = 0; k < n; ++k) {
@@ -618,18 +625,6 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
             for (int a = 0; a < n; ++a) s = fma(Dt.D[a2][a], ql[a], s);
             s_s[sidx(e, li, a2, k)] = s;
           }
-        }
-      }
-    }
-    if constexpr (IO == 3) {
-      // level N of layer l is level 0 of layer l + 1: row buffer -> plane (l+1)&1 before the buffer is
-      // refilled (a thread's items all have its own field: NT is a multiple of F)
-      static_assert(IO != 3 || C::NT % F == 0, "IO 3: plane copy items keep the thread's field");
-      if (l + 1 < nlay) {
-        double* pn = s_q + C::QB_P + ((l + 1) & 1) * C::YLS;
-        for (int x = tid; x < UV * F; x += C::NT) {
-          const int uv = x / F;
-          pn[f * C::YFS + (uv / V) * C::YUS + uv % V] = s_q[(s_pdst[uv] + N - 1) * 5 + myqc];
         }
       }
     }
@@ -834,6 +829,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     // IO 1 / 3: the items' columns (7 bits each, bit 7 = tile-owned) stay packed in one register from here
     // to step f, which then starts at the element-copy offsets instead of the chain s_perm -> s_ct
     static_assert(!OUT_YT || (UV < 128 && C::PFY <= 4), "packed item columns");
+    constexpr bool PK = !OUT_YT && UV < 128 && PF <= 4;   // the same for the row-output items
     unsigned uvp = 0;
     if constexpr (OUT_YT) {
 #pragma unroll
@@ -851,7 +847,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
-        const int node = (qi < C::FI) ? s_perm[qi / N] * n + qi % N : 0;
+        const int uv = (qi < C::FI) ? s_perm[qi / N] : 0;
+        const int node = (qi < C::FI) ? uv * n + qi % N : 0;
+        if constexpr (PK) uvp |= (unsigned)(uv | (s_code[uv] < 0 ? 0x80 : 0)) << (8 * it);
         gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
         mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
       }
@@ -945,7 +943,8 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
         if (gf[it] < 0) continue;
-        const int uv = s_perm[qi / N], k = qi % N;
+        const unsigned ub = (uvp >> (8 * it)) & 0xffu;
+        const int uv = PK ? (int)(ub & 0x7fu) : s_perm[qi / N], k = qi % N;
         const int4 ct = s_ct[uv];
         hv::Vec<F> val;
 #pragma unroll
@@ -962,7 +961,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
           for (int p = 0; p < F; ++p) o[p] = val.v[p];
         } else {
-          emit(gf[it], mf[it], val, s_code[uv], l * N + k);
+          emit(gf[it], mf[it], val, (PK && (ub & 0x80u)) ? -1 : s_code[uv], l * N + k);
         }
       }
       if (IO == 0 && l == l1 - 1 && l1 < nlay) {   // segment top: raw sums, from below
