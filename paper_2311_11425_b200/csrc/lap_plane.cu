@@ -829,7 +829,6 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
     // IO 1 / 3: the items' columns (7 bits each, bit 7 = tile-owned) stay packed in one register from here
     // to step f, which then starts at the element-copy offsets instead of the chain s_perm -> s_ct
     static_assert(!OUT_YT || (UV < 128 && C::PFY <= 4), "packed item columns");
-    constexpr bool PK = !OUT_YT && UV < 128 && PF <= 4;   // the same for the row-output items
     unsigned uvp = 0;
     if constexpr (OUT_YT) {
 #pragma unroll
@@ -847,9 +846,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
-        const int uv = (qi < C::FI) ? s_perm[qi / N] : 0;
-        const int node = (qi < C::FI) ? uv * n + qi % N : 0;
-        if constexpr (PK) uvp |= (unsigned)(uv | (s_code[uv] < 0 ? 0x80 : 0)) << (8 * it);
+        const int node = (qi < C::FI) ? s_perm[qi / N] * n + qi % N : 0;
         gf[it] = (qi < C::FI) ? __ldg(gt_t + (int64_t)l * C::GTS + node) : -1;
         mf[it] = (qi < C::FI) ? __ldg(Mt_t + (int64_t)l * C::MTS + node) : 0.0;
       }
@@ -943,8 +940,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       for (int it = 0; it < PF; ++it) {
         const int qi = tid + it * C::NT;
         if (gf[it] < 0) continue;
-        const unsigned ub = (uvp >> (8 * it)) & 0xffu;
-        const int uv = PK ? (int)(ub & 0x7fu) : s_perm[qi / N], k = qi % N;
+        const int uv = s_perm[qi / N], k = qi % N;
         const int4 ct = s_ct[uv];
         hv::Vec<F> val;
 #pragma unroll
@@ -961,7 +957,7 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
 #pragma unroll
           for (int p = 0; p < F; ++p) o[p] = val.v[p];
         } else {
-          emit(gf[it], mf[it], val, (PK && (ub & 0x80u)) ? -1 : s_code[uv], l * N + k);
+          emit(gf[it], mf[it], val, s_code[uv], l * N + k);
         }
       }
       if (IO == 0 && l == l1 - 1 && l1 < nlay) {   // segment top: raw sums, from below
