@@ -408,15 +408,13 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
           return;
         }
         if (row5 && !A.accumulate) {
-          if ((g & 1) == 0) {
-            st_v2(o, 0.0, m * val.v[0]);
-            st_v2(o + 2, m * val.v[1], m * val.v[2]);
-            o[4] = m * val.v[3];
-          } else {
-            o[0] = 0.0;
-            st_v2(o + 1, m * val.v[0], m * val.v[1]);
-            st_v2(o + 3, m * val.v[2], m * val.v[3]);
-          }
+          // row (0, v0, v1, v2, v3) of 40 bytes: 16-byte aligned when g is even, 8 bytes past that when odd --
+          // one 8-byte and two 16-byte stores with parity-selected offsets (no divergent branch)
+          const bool odd = (g & 1) != 0;
+          const double v0 = m * val.v[0], v1 = m * val.v[1], v2 = m * val.v[2], v3 = m * val.v[3];
+          o[odd ? 0 : 4] = odd ? 0.0 : v3;
+          st_v2(o + (odd ? 1 : 0), odd ? v0 : 0.0, odd ? v1 : v0);
+          st_v2(o + (odd ? 3 : 2), odd ? v2 : v1, odd ? v3 : v2);
           return;
         }
       }
