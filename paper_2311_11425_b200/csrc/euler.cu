@@ -593,6 +593,17 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       if (t >= nn) continue;
       const int i = t / (n * n), j = (t / n) % n, k = t % n;
       const int na = i * PI + j * n + k;
+      // where this node's result goes -- the final row M^-1 acc of a node the column owns, or the raw sums
+      // into its 5-wide partial row (perimeter nodes; slot_fixup sums them) -- and the global loads of the
+      // store (M^-1, the row's previous value when accumulating) first: they fly during the sums below
+      const bool carry_up = (k == N && l < nlay - 1);       // top level: carried into the next layer
+      const int cd = s_code[i * n + j];
+      const bool fin = cd < 0;
+      const int64_t ro = fin ? (int64_t)gn[jn] : (int64_t)cd * A.n_z + l * N + k;
+      double* o = fin ? A.out + ro * A.ldo : A.part + ro * 5;
+      const double mraw = (fin && !carry_up) ? Mt_t[(int64_t)l * ((nn + 1) & ~1) + t] : 1.0;
+      double pv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      if (vo && A.accumulate && fin && !carry_up) ld_row5(o, ro & 1, pv);
       double acc[5];
       double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -611,29 +622,20 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
 #pragma unroll
         for (int f = 0; f < 5; ++f) acc[f] = cr[f] + acc[f];   // previous layer's top first
       }
-      if (k == N && l < nlay - 1) {
+      if (carry_up) {
 #pragma unroll
         for (int f = 0; f < 5; ++f) cw[f] = acc[f];
       } else {
-        const int cd = s_code[i * n + j];
-        const int z = l * N + k;
-        // one store path for both kinds of node: the final row M^-1 acc of a node the column owns, or
-        // the raw sums into its 5-wide partial row (perimeter nodes; slot_fixup sums them)
-        const bool fin = cd < 0;
-        const int64_t r = fin ? (int64_t)gn[jn] : (int64_t)cd * A.n_z + z;
-        double* o = fin ? A.out + r * A.ldo : A.part + r * 5;
-        const double mi = fin ? A.scale * Mt_t[(int64_t)l * ((nn + 1) & ~1) + t] : 1.0;
+        const double mi = fin ? A.scale * mraw : 1.0;
         double v[5];
 #pragma unroll
         for (int f = 0; f < 5; ++f) v[f] = fin ? mi * acc[f] : acc[f];
         if (vo) {
           if (A.accumulate && fin) {
-            double pv[5];
-            ld_row5(o, r & 1, pv);
 #pragma unroll
             for (int f = 0; f < 5; ++f) v[f] = pv[f] + v[f];
           }
-          st_row5(o, r & 1, v);
+          st_row5(o, ro & 1, v);
         } else {
 #pragma unroll
           for (int f = 0; f < 5; ++f) o[f] = (A.accumulate && fin) ? o[f] + v[f] : v[f];
