@@ -461,17 +461,43 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
   if constexpr (STG) {
     if (t0 == 0) issue_stage(s_el[0]);
   }
+  auto wait_stage = [&](int le) {   // layer le's stage has landed
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar), par = (uint32_t)(le & 1);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done)
+                   : "r"(b), "r"(par)
+                   : "memory");
+  };
+  // staged variant: a layer's gids and q rows are read at the END of the previous layer's phase 3 (the stage
+  // has landed by then), so the q-row loads fly across the layer barrier instead of heading phase 1
+  int gq[NPT];
+  double qn[NPT][5];
+  auto load_q = [&]() {
+#pragma unroll
+    for (int jn = 0; jn < NPT; ++jn) {
+      const int t = t0 + jn * NB;
+      gq[jn] = 0;
+#pragma unroll
+      for (int f = 0; f < 5; ++f) qn[jn][f] = 0.0;
+      if (t >= nn) continue;
+      const int g = s_g[t];
+      gq[jn] = g;
+      if (vq) {
+        ld_row5(q + (int64_t)g * 5, g & 1, qn[jn]);
+      } else {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) qn[jn][f] = q[(int64_t)g * ldq + f];
+      }
+    }
+  };
+  if constexpr (STG) {
+    wait_stage(0);
+    load_q();
+  }
   for (int l = 0; l < nlay; ++l) {
     const int64_t e = s_el[l];
-    if constexpr (STG) {   // this layer's stage has landed
-      const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar), par = (uint32_t)(l & 1);
-      uint32_t done = 0;
-      while (!done)
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(done)
-                     : "r"(b), "r"(par)
-                     : "memory");
-    }
     double extra[NPT][3];                                // geopotential + Coriolis terms of acc[1..3]
     int gn[NPT];
     // ---- phase 1 (euler_node_acc's fluxes, reference expression order), node t = t0 + jn * NB
@@ -485,11 +511,14 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       extra[jn][0] = extra[jn][1] = extra[jn][2] = 0.0;
       gn[jn] = 0;
       if (!act) continue;
-      const int g = STG ? s_g[t] : gnx[jn];
+      const int g = STG ? gq[jn] : gnx[jn];
       gn[jn] = g;
       if (!STG && l + 1 < nlay) gnx[jn] = gid[(int64_t)s_el[l + 1] * nn + t];
       double qv[5];
-      if (vq) {
+      if constexpr (STG) {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) qv[f] = qn[jn][f];
+      } else if (vq) {
         ld_row5(q + (int64_t)g * 5, g & 1, qv);
       } else {
 #pragma unroll
@@ -640,6 +669,12 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
 #pragma unroll
           for (int f = 0; f < 5; ++f) o[f] = (A.accumulate && fin) ? o[f] + v[f] : v[f];
         }
+      }
+    }
+    if constexpr (STG) {
+      if (l + 1 < nlay) {
+        wait_stage(l + 1);
+        load_q();
       }
     }
     __syncthreads();   // the flux arrays and the carry slot are rewritten by the next layer
