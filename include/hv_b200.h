@@ -53,6 +53,10 @@ int hv_probe_dfma(double* d_out, int64_t iters, int blocks, int threads, void* s
  * for the equation of state (state.py:84-101 calls numpy's power; csrc/hv_pow.cuh: <= 1 ulp for positive
  * normal x, the library pow otherwise). */
 int hv_probe_pow(int64_t n, const double* d_x, double y, double* d_out, void* stream);
+/* Test probe: counts in *d_bad (zeroed by the caller) the pairs (a_j, b_i), j = 0, 97, 194, ..., whose
+ * quotient by the Euler kernels' reciprocal-and-correction division (csrc/hv_pow.cuh div_rcp) differs
+ * bitwise from IEEE a_j / b_i. */
+int hv_probe_div(int64_t n, const double* d_a, const double* d_b, unsigned long long* d_bad, void* stream);
 
 /* ---------------------------------------------------------------- host mesh
  * Replaces Mesh._number_gridpoints (mesh.py:86-107): bit-exact gid

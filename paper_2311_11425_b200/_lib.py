@@ -86,6 +86,7 @@ _SIGS = {
     "hv_launch_count": (C.c_int64, []),
     "hv_probe_dfma": (C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p]),
     "hv_probe_pow": (C.c_int, [C.c_int64, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]),
+    "hv_probe_div": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hv_rows_minv": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_int,
                                C.c_void_p]),
     "hv_number_gridpoints": (C.c_int, [_P, _I64, C.c_int, C.c_int, C.c_int, _D, _P, _P]),

@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
   }
+  const double rPA = __drcp_rn(K.P_A);                   // quotients by P_A and rho: hv::div_rcp (hv_pow.cuh)
   double w[NPT];
   int gnx[NPT];                                          // gids of the next layer's nodes (unstaged variant)
 #pragma unroll
@@ -529,13 +530,14 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       const double rho = qv[0];
       double P;
       if (K.set == 1) {
-        P = K.P_A * hv::pow_pos(K.R * qv[4] / K.P_A, K.gamma);
+        P = K.P_A * hv::pow_pos(hv::div_rcp(K.R * qv[4], K.P_A, rPA), K.gamma);
       } else {
         const double phi = Mt[14 * nloc + p];
         const double ke = 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / rho;
         P = (K.gamma - 1.0) * (qv[4] - ke - rho * phi);
       }
-      const double tflux = (K.set == 1) ? qv[4] / qv[0] : (qv[4] + P) / qv[0];
+      const double rrho = __drcp_rn(rho);   // the node's four quotients by rho: div_rcp
+      const double tflux = (K.set == 1) ? hv::div_rcp(qv[4], rho, rrho) : hv::div_rcp(qv[4] + P, rho, rrho);
       double sg[3] = {0.0, 0.0, 0.0};
       // one direction at a time: grad xi^m (3 doubles) live only inside its iteration
 #pragma unroll
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
         double gm[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) gm[c] = STG ? s_m[(m * 3 + c) * nn + t] : Mt[(m * 3 + c) * nloc + p];
-        double un = (gm[0] * qv[1] + gm[1] * qv[2] + gm[2] * qv[3]) / rho;
+        double un = hv::div_rcp(gm[0] * qv[1] + gm[1] * qv[2] + gm[2] * qv[3], rho, rrho);
         if (m == 2) un = un * mask;
         const double jun = Jg * un;
         s_f[(m * 5 + 0) * FS + na] = w[jn] * (jun * qv[0]);

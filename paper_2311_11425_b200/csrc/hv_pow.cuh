@@ -74,6 +74,18 @@ HV_POW_HD double pw_double(int64_t b) {
 #endif
 }
 
+// a / b with rb = the correctly rounded reciprocal of b (__drcp_rn; 1.0 / b on the host): a rb, then one
+// exact-residual correction (Markstein's theorem: the result is the correctly rounded quotient barring
+// over/underflow, i.e. what IEEE division gives; hv_probe_div counts the differences from a / b on the
+// device).  The compiler's out-of-line division routine cost ~40 instructions per quotient in the Euler
+// column sweep (16 % of its instructions for five quotients per node); this is 3 per quotient after one
+// reciprocal per divisor.
+HV_POW_HD double div_rcp(double a, double b, double rb) {
+  const double q = pw_mul(a, rb);
+  const double e = pw_fma(-q, b, a);
+  return pw_fma(e, rb, q);
+}
+
 // fast path: x a positive normal in [2^-500, 2^500], |y log x| <= 600 (checked by pow_pos)
 HV_POW_HD double pow_pos_core(double x, double y, bool* ok) {
   const double LN2_HI = 6.93147180369123816490e-01;   // 0x3fe62e42fee00000: 21 trailing zero bits x ... exact e * LN2_HI

@@ -32,7 +32,28 @@ __global__ void pow_probe_kernel(int64_t n, const double* __restrict__ x, double
   if (i < n) out[i] = hv::pow_pos(x[i], y);
 }
 
+// mismatches of hv::div_rcp against IEEE division over all (a_i, b_j) pairs of two arrays
+__global__ void div_probe_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
+                                 unsigned long long* __restrict__ bad) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double bi = b[i], rb = __drcp_rn(bi);
+  unsigned long long c = 0;
+  for (int64_t j = 0; j < n; j += 97) {
+    const double q0 = a[j] / bi, q1 = hv::div_rcp(a[j], bi, rb);
+    if (__double_as_longlong(q0) != __double_as_longlong(q1)) ++c;
+  }
+  if (c) atomicAdd(bad, c);
+}
+
 }  // namespace
+
+extern "C" int hv_probe_div(int64_t n, const double* d_a, const double* d_b, unsigned long long* d_bad, void* stream) {
+  if (n <= 0 || !d_a || !d_b || !d_bad) HV_FAIL(HV_ERR_INVALID, "hv_probe_div: bad arguments");
+  div_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, d_a, d_b, d_bad);
+  HV_LAUNCH_CHECK();
+  return HV_OK;
+}
 
 extern "C" int hv_probe_pow(int64_t n, const double* d_x, double y, double* d_out, void* stream) {
   if (n <= 0 || !d_x || !d_out) HV_FAIL(HV_ERR_INVALID, "hv_probe_pow: bad arguments");
