@@ -74,6 +74,26 @@ HV_POW_HD double pw_double(int64_t b) {
 #endif
 }
 
+// polynomial coefficients: on the device in constant memory, so that the FMAs take them as constant-bank
+// operands (as immediates every 64-bit coefficient costs two uniform-register moves: ~45 extra issue slots
+// per call)
+#if defined(__CUDACC__)
+#define HV_POW_TAB static __constant__ double
+#else
+#define HV_POW_TAB static const double
+#endif
+HV_POW_TAB pw_log_c[11] = {2.0 / 23.0, 2.0 / 21.0, 2.0 / 19.0, 2.0 / 17.0, 2.0 / 15.0, 2.0 / 13.0,
+                           2.0 / 11.0, 2.0 / 9.0,  2.0 / 7.0,  2.0 / 5.0,  2.0 / 3.0};
+HV_POW_TAB pw_exp_c[12] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+                           1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
+                           1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5};
+#if defined(__CUDACC__) && !defined(__CUDA_ARCH__)
+// host pass of a .cu file: the tables are device symbols; the host functions below are never called there
+#define HV_POW_C(tab, i) 0.0
+#else
+#define HV_POW_C(tab, i) tab[i]
+#endif
+
 // a / b with rb = the correctly rounded reciprocal of b (__drcp_rn; 1.0 / b on the host): a rb, then one
 // exact-residual correction (Markstein's theorem: the result is the correctly rounded quotient barring
 // over/underflow, i.e. what IEEE division gives; hv_probe_div counts the differences from a / b on the
@@ -110,17 +130,9 @@ HV_POW_HD double pow_pos_core(double x, double y, bool* ok) {
   const double s_lo = pw_mul(res, r);
   // log m = 2 s + s^3 (2/3 + 2/5 s^2 + ... + 2/23 s^20)
   const double s2 = pw_mul(s_hi, s_hi);
-  double p = 2.0 / 23.0;
-  p = pw_fma(p, s2, 2.0 / 21.0);
-  p = pw_fma(p, s2, 2.0 / 19.0);
-  p = pw_fma(p, s2, 2.0 / 17.0);
-  p = pw_fma(p, s2, 2.0 / 15.0);
-  p = pw_fma(p, s2, 2.0 / 13.0);
-  p = pw_fma(p, s2, 2.0 / 11.0);
-  p = pw_fma(p, s2, 2.0 / 9.0);
-  p = pw_fma(p, s2, 2.0 / 7.0);
-  p = pw_fma(p, s2, 2.0 / 5.0);
-  p = pw_fma(p, s2, 2.0 / 3.0);
+  double p = HV_POW_C(pw_log_c, 0);
+#pragma unroll
+  for (int i = 1; i < 11; ++i) p = pw_fma(p, s2, HV_POW_C(pw_log_c, i));
   const double s3 = pw_mul(s2, s_hi);
   const double lm_hi = pw_add(s_hi, s_hi);
   // d(2 atanh s)/ds = 2 / (1 - s^2): the low part of s enters as 2 s_lo (1 + s^2)
@@ -140,18 +152,9 @@ HV_POW_HD double pow_pos_core(double x, double y, bool* ok) {
   const double rr_hi = pw_fma(-kd, LN2_HI, t_hi);            // exact
   const double rr_lo = pw_fma(-kd, LN2_LO, t_lo);
   const double rr = pw_add(rr_hi, rr_lo);
-  double q = 1.0 / 6227020800.0;                            // 1/13!
-  q = pw_fma(q, rr, 1.0 / 479001600.0);
-  q = pw_fma(q, rr, 1.0 / 39916800.0);
-  q = pw_fma(q, rr, 1.0 / 3628800.0);
-  q = pw_fma(q, rr, 1.0 / 362880.0);
-  q = pw_fma(q, rr, 1.0 / 40320.0);
-  q = pw_fma(q, rr, 1.0 / 5040.0);
-  q = pw_fma(q, rr, 1.0 / 720.0);
-  q = pw_fma(q, rr, 1.0 / 120.0);
-  q = pw_fma(q, rr, 1.0 / 24.0);
-  q = pw_fma(q, rr, 1.0 / 6.0);
-  q = pw_fma(q, rr, 0.5);
+  double q = HV_POW_C(pw_exp_c, 0);                         // 1/13!, ..., 1/2
+#pragma unroll
+  for (int i = 1; i < 12; ++i) q = pw_fma(q, rr, HV_POW_C(pw_exp_c, i));
   // exp(rr) = (1 + rr_hi) + (rr_lo + rr^2 q), the first sum with its rounding error carried
   const double w = pw_fma(pw_mul(rr, rr), q, rr_lo);
   const double hi = pw_add(1.0, rr_hi);
