@@ -485,8 +485,16 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       if (t >= nn) continue;
       const int g = s_g[t];
       gq[jn] = g;
-      if (vq) {
-        ld_row5(q + (int64_t)g * 5, g & 1, qn[jn]);
+      if (vq) {   // raw pieces (ld_row5's loads); the parity selects wait for the data, so they happen in phase 1
+        const double* row = q + (int64_t)g * 5;
+        const bool odd = g & 1;
+        qn[jn][0] = row[odd ? 0 : 4];
+        const double2 b = *reinterpret_cast<const double2*>(row + (odd ? 1 : 0));
+        const double2 c = *reinterpret_cast<const double2*>(row + (odd ? 3 : 2));
+        qn[jn][1] = b.x;
+        qn[jn][2] = b.y;
+        qn[jn][3] = c.x;
+        qn[jn][4] = c.y;
       } else {
 #pragma unroll
         for (int f = 0; f < 5; ++f) qn[jn][f] = q[(int64_t)g * ldq + f];
@@ -517,8 +525,12 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       if (!STG && l + 1 < nlay) gnx[jn] = gid[(int64_t)s_el[l + 1] * nn + t];
       double qv[5];
       if constexpr (STG) {
-#pragma unroll
-        for (int f = 0; f < 5; ++f) qv[f] = qn[jn][f];
+        const bool odd = vq && (g & 1);                  // ld_row5's selects on load_q's raw pieces
+        qv[0] = (!vq || odd) ? qn[jn][0] : qn[jn][1];
+        qv[1] = !vq ? qn[jn][1] : (odd ? qn[jn][1] : qn[jn][2]);
+        qv[2] = !vq ? qn[jn][2] : (odd ? qn[jn][2] : qn[jn][3]);
+        qv[3] = !vq ? qn[jn][3] : (odd ? qn[jn][3] : qn[jn][4]);
+        qv[4] = !vq ? qn[jn][4] : (odd ? qn[jn][4] : qn[jn][0]);
       } else if (vq) {
         ld_row5(q + (int64_t)g * 5, g & 1, qv);
       } else {
