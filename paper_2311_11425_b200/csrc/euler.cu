@@ -645,8 +645,15 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       const int64_t ro = fin ? (int64_t)gn[jn] : (int64_t)cd * A.n_z + l * N + k;
       double* o = fin ? A.out + ro * A.ldo : A.part + ro * 5;
       const double mraw = (fin && !carry_up) ? Mt_t[(int64_t)l * ((nn + 1) & ~1) + t] : 1.0;
-      double pv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      if (vo && A.accumulate && fin && !carry_up) ld_row5(o, ro & 1, pv);
+      // the row's previous value as ld_row5's raw pieces (the parity selects, which wait for the data, at the use)
+      const bool oodd = ro & 1;
+      double pa = 0.0;
+      double2 pb = make_double2(0.0, 0.0), pc = make_double2(0.0, 0.0);
+      if (vo && A.accumulate && fin && !carry_up) {
+        pa = o[oodd ? 0 : 4];
+        pb = *reinterpret_cast<const double2*>(o + (oodd ? 1 : 0));
+        pc = *reinterpret_cast<const double2*>(o + (oodd ? 3 : 2));
+      }
       double acc[5];
       double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -675,10 +682,13 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
         for (int f = 0; f < 5; ++f) v[f] = fin ? mi * acc[f] : acc[f];
         if (vo) {
           if (A.accumulate && fin) {
-#pragma unroll
-            for (int f = 0; f < 5; ++f) v[f] = pv[f] + v[f];
+            v[0] = (oodd ? pa : pb.x) + v[0];
+            v[1] = (oodd ? pb.x : pb.y) + v[1];
+            v[2] = (oodd ? pb.y : pc.x) + v[2];
+            v[3] = (oodd ? pc.x : pc.y) + v[3];
+            v[4] = (oodd ? pc.y : pa) + v[4];
           }
-          st_row5(o, ro & 1, v);
+          st_row5(o, oodd, v);
         } else {
 #pragma unroll
           for (int f = 0; f < 5; ++f) o[f] = (A.accumulate && fin) ? o[f] + v[f] : v[f];
