@@ -155,7 +155,12 @@ struct PlaneCfg {
   // split planes (H > 1): D in shared memory for the xi exchange, whose row / column offsets vary
   // across the lanes of a warp (constant-bank loads would serialise)
   static constexpr int OFF_D = OFF_BAR + 4;
-  static constexpr size_t SMEM = sizeof(double) * (OFF_D + (H > 1 ? n * n : 0));
+  // split planes writing the tile-ordered intermediate (N = 7: shared memory is not what bounds the CTAs per
+  // SM): the block's padding positions as a table, so that the per-layer zeroing is a load and a store per item
+  static constexpr int PADN = N * F * (U * (YUS - V) + YFS - U * YUS);
+  static constexpr bool PADTAB = H > 1 && (IO == 1 || IO == 3);
+  static constexpr int OFF_PT = OFF_D + (H > 1 ? n * n : 0);
+  static constexpr size_t SMEM = sizeof(double) * (OFF_PT + (PADTAB ? (PADN + 1) / 2 : 0));
 };
 
 // Wp layout (per tile-layer): [cp 3][i n][k n][e NE][j n][2] (component pairs (w00,w01)
@@ -474,6 +479,14 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
   }
   if constexpr (H > 1)
     for (int x = tid; x < n * n; x += C::NT) sD[x] = Dt.D[x / n][x % n];
+  int* s_pad = reinterpret_cast<int*>(sm + C::OFF_PT);   // PADTAB: offsets of the block's padding doubles
+  if constexpr (C::PADTAB) {
+    constexpr int PV = C::YUS - V, PT = C::YFS - U * C::YUS, PP = U * PV + PT;
+    for (int x = tid; x < C::PADN; x += C::NT) {
+      const int kf = x / PP, j = x - kf * PP;
+      s_pad[x] = (kf / F) * C::YLS + (kf % F) * C::YFS + ((j < U * PV) ? (j / PV) * C::YUS + V + j % PV : U * C::YUS + j - U * PV);
+    }
+  }
   __syncthreads();
   if (tid == 0) {   // output items walk the tile-owned columns first (uniform warps in step f)
     int c = 0;
@@ -900,7 +913,9 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
       }
       // the layout's padding (v = V..YUS-1 of every u row, u*YUS >= U*YUS up to YFS): zeros, so that
       // every sector of the block is written whole (no partial-sector read-modify-write in L2)
-      {
+      if constexpr (C::PADTAB) {
+        for (int x = tid; x < C::PADN; x += C::NT) yb[s_pad[x]] = 0.0;
+      } else {
         constexpr int PV = C::YUS - V, PT = C::YFS - U * C::YUS, PP = U * PV + PT;
         for (int x = tid; x < N * F * PP; x += C::NT) {
           const int kf = x / PP, j = x - kf * PP;
