@@ -701,7 +701,8 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
         load_q();
       }
     }
-    __syncthreads();   // the flux arrays and the carry slot are rewritten by the next layer
+    // no barrier here: phase 3 reads and the next layer's phase 1 writes only the thread's OWN node's
+    // entries of the flux arrays, and a carry slot is rewritten two barriers after its last read
   }
 }
 
