@@ -187,6 +187,56 @@ __global__ void slot_fixup_kernel(TileArgs A, int row_mode) {
       if ((A.zero_mask >> zc) & 1u) o[zc] = 0.0;
 }
 
+// The two hot modes of slot_fixup_kernel<4> (H_nu's alpha = 2 on one GPU: slot rows of the tile-ordered
+// intermediate, MODE 3; the (ng, 5) result rows of fields 1..4 with column 0 zeroed, MODE 2) without the
+// generic kernel's segment / interface / accumulate paths: ~40 registers instead of 64, so 48 instead of 32
+// warps per SM keep loads in flight.  Same sums in the same order (rows r ascending from 0.0).
+template <int MODE>
+__global__ void __launch_bounds__(256, MODE == 3 ? 6 : 5) slot_fixup_lean_kernel(TileArgs A) {
+  constexpr int F = 4;
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= A.nslot * A.n_z) return;
+  const unsigned nz = (unsigned)A.n_z;
+  const int64_t s = (unsigned)id / nz;
+  const int z = (int)((unsigned)id - (unsigned)s * nz);
+  const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
+  int g = 0;
+  if (MODE == 2) g = A.col_gid[(int64_t)A.slot_col[s] * A.n_z + z];
+  const double mi = __ldg(A.Ms + id);
+  const double* p0 = A.part + ((int64_t)r0 * A.n_z + z) * F;
+  const int64_t rs = (int64_t)A.n_z * F;                  // doubles between a slot's consecutive partial rows
+  double v0[F], v1[F], acc[F];
+  load_row<F>(p0, v0);
+  if (nc > 1) load_row<F>(p0 + rs, v1);
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) {
+    acc[ff] = 0.0 + v0[ff];
+    if (nc > 1) acc[ff] += v1[ff];
+  }
+  for (int r = 2; r < nc; ++r) {
+    double w[F];
+    load_row<F>(p0 + r * rs, w);
+#pragma unroll
+    for (int ff = 0; ff < F; ++ff) acc[ff] += w[ff];
+  }
+  double r[F];
+#pragma unroll
+  for (int ff = 0; ff < F; ++ff) r[ff] = A.scale * (mi * acc[ff]);
+  if (MODE == 3) {
+    const int N = (A.n_z - 1) / A.nlay;
+    const int64_t row = (z == 0) ? s : A.nslot + (((int64_t)((z - 1) / N) * A.nslot + s) * N + (z - 1) % N);
+    double* o = A.sv + row * F;
+    st2(o, r[0], r[1]);
+    st2(o + 2, r[2], r[3]);
+  } else {   // row (0, r0, r1, r2, r3): parity-selected offsets, no divergent branch
+    double* o = A.out + (int64_t)g * 5;
+    const bool odd = (g & 1) != 0;
+    o[odd ? 0 : 4] = odd ? 0.0 : r[3];
+    st2(o + (odd ? 1 : 0), odd ? r[0] : 0.0, odd ? r[1] : r[0]);
+    st2(o + (odd ? 3 : 2), odd ? r[2] : r[1], odd ? r[3] : r[2]);
+  }
+}
+
 template <int F>
 int pack_f(const TileArgs& A, cudaStream_t st) {
   if (A.next <= 0) return HV_OK;
@@ -215,6 +265,14 @@ int fixup_f(const TileArgs& A, cudaStream_t st) {
     else if (A.ldo == 5 && A.zero_mask == 1u && A.of.f[0] == 1 && A.of.f[1] == 2 && A.of.f[2] == 3 &&
              A.of.f[3] == 4)
       row_mode = 2;
+  }
+  if constexpr (F == 4) {
+    if (nseg == 1 && !A.slot_ext && A.Ms && (row_mode == 2 || row_mode == 3)) {
+      if (row_mode == 3) slot_fixup_lean_kernel<3><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+      else slot_fixup_lean_kernel<2><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+      HV_LAUNCH_CHECK();
+      return HV_OK;
+    }
   }
   slot_fixup_kernel<F><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, row_mode);
   HV_LAUNCH_CHECK();
