@@ -237,6 +237,72 @@ __global__ void __launch_bounds__(256, MODE == 3 ? 6 : 5) slot_fixup_lean_kernel
   }
 }
 
+// 40-byte rows (5 doubles at element offset 5 r of a 16-byte aligned array) as one 8-byte and two 16-byte
+// accesses with parity-selected offsets; Row5 keeps the raw pieces so that the selects, which wait for the
+// data, happen where the values are used
+struct Row5 {
+  double a;
+  double2 b, c;
+};
+__device__ __forceinline__ Row5 ld_row5_raw(const double* row, bool odd) {
+  Row5 x;
+  x.a = row[odd ? 0 : 4];
+  x.b = *reinterpret_cast<const double2*>(row + (odd ? 1 : 0));
+  x.c = *reinterpret_cast<const double2*>(row + (odd ? 3 : 2));
+  return x;
+}
+__device__ __forceinline__ void row5_add(const Row5& x, bool odd, double (&v)[5]) {
+  v[0] += odd ? x.a : x.b.x;
+  v[1] += odd ? x.b.x : x.b.y;
+  v[2] += odd ? x.b.y : x.c.x;
+  v[3] += odd ? x.c.x : x.c.y;
+  v[4] += odd ? x.c.y : x.a;
+}
+
+// The Euler column sweep's fix-up (5 fields into (ng, 5) rows, optionally accumulating; one GPU, no
+// segments) without the generic kernel's other paths, rows moved in 16-byte pieces.  Same sums in the
+// same order as slot_fixup_kernel<5>.
+template <int ACC>
+__global__ void __launch_bounds__(256, 5) slot_fixup_lean5_kernel(TileArgs A) {
+  const int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (id >= A.nslot * A.n_z) return;
+  const unsigned nz = (unsigned)A.n_z;
+  const int64_t s = (unsigned)id / nz;
+  const int z = (int)((unsigned)id - (unsigned)s * nz);
+  const int r0 = A.slot_row0[s], nc = A.slot_nc[s];
+  const int g = A.col_gid[(int64_t)A.slot_col[s] * A.n_z + z];
+  const double mi = __ldg(A.Ms + id);
+  const int64_t pr = (int64_t)r0 * A.n_z + z;             // first partial row; the next ones n_z rows apart
+  const bool nzodd = A.n_z & 1;
+  const bool odd0 = pr & 1, odd1 = odd0 != nzodd;
+  double* o = A.out + (int64_t)g * 5;
+  const bool oodd = g & 1;
+  const Row5 x0 = ld_row5_raw(A.part + pr * 5, odd0);
+  Row5 x1 = x0, xo = x0;
+  if (nc > 1) x1 = ld_row5_raw(A.part + (pr + A.n_z) * 5, odd1);
+  if (ACC) xo = ld_row5_raw(o, oodd);
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  row5_add(x0, odd0, acc);
+  if (nc > 1) row5_add(x1, odd1, acc);
+  for (int r = 2; r < nc; ++r) {
+    const int64_t q = pr + (int64_t)r * A.n_z;
+    const Row5 x = ld_row5_raw(A.part + q * 5, q & 1);
+    row5_add(x, q & 1, acc);
+  }
+  double v[5];
+#pragma unroll
+  for (int ff = 0; ff < 5; ++ff) v[ff] = A.scale * (mi * acc[ff]);
+  if (ACC) {
+    double pv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    row5_add(xo, oodd, pv);
+#pragma unroll
+    for (int ff = 0; ff < 5; ++ff) v[ff] = pv[ff] + v[ff];
+  }
+  o[oodd ? 0 : 4] = oodd ? v[0] : v[4];
+  st2(o + (oodd ? 1 : 0), oodd ? v[1] : v[0], oodd ? v[2] : v[1]);
+  st2(o + (oodd ? 3 : 2), oodd ? v[3] : v[2], oodd ? v[4] : v[3]);
+}
+
 template <int F>
 int pack_f(const TileArgs& A, cudaStream_t st) {
   if (A.next <= 0) return HV_OK;
@@ -270,6 +336,16 @@ int fixup_f(const TileArgs& A, cudaStream_t st) {
     if (nseg == 1 && !A.slot_ext && A.Ms && (row_mode == 2 || row_mode == 3)) {
       if (row_mode == 3) slot_fixup_lean_kernel<3><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
       else slot_fixup_lean_kernel<2><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+      HV_LAUNCH_CHECK();
+      return HV_OK;
+    }
+  }
+  if constexpr (F == 5) {
+    const bool ident = A.of.f[0] == 0 && A.of.f[1] == 1 && A.of.f[2] == 2 && A.of.f[3] == 3 && A.of.f[4] == 4;
+    if (nseg == 1 && !A.slot_ext && A.Ms && A.ldo == 5 && ident && !A.zero_mask && A.io == 0 && A.out &&
+        ((uintptr_t)A.out & 15) == 0 && ((uintptr_t)A.part & 15) == 0) {
+      if (A.accumulate) slot_fixup_lean5_kernel<1><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
+      else slot_fixup_lean5_kernel<0><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A);
       HV_LAUNCH_CHECK();
       return HV_OK;
     }
