@@ -394,16 +394,12 @@ __global__ void __launch_bounds__(PlaneCfg<n, TX, TY, F, WV, H, WF, IO>::NT, MB)
         st_v2(o, m * val.v[0], m * val.v[1]);
         st_v2(o + 2, m * val.v[2], m * val.v[3]);
         return;
-      } else if constexpr (F == 4 && OM == 2) {
-        if ((g & 1) == 0) {
-          st_v2(o, 0.0, m * val.v[0]);
-          st_v2(o + 2, m * val.v[1], m * val.v[2]);
-          o[4] = m * val.v[3];
-        } else {
-          o[0] = 0.0;
-          st_v2(o + 1, m * val.v[0], m * val.v[1]);
-          st_v2(o + 3, m * val.v[2], m * val.v[3]);
-        }
+      } else if constexpr (F == 4 && OM == 2) {   // parity-selected offsets (see the row5 path below)
+        const bool odd = (g & 1) != 0;
+        const double v0 = m * val.v[0], v1 = m * val.v[1], v2 = m * val.v[2], v3 = m * val.v[3];
+        o[odd ? 0 : 4] = odd ? 0.0 : v3;
+        st_v2(o + (odd ? 1 : 0), odd ? v0 : 0.0, odd ? v1 : v0);
+        st_v2(o + (odd ? 3 : 2), odd ? v2 : v1, odd ? v3 : v2);
         return;
       }
       if constexpr (F == 4) {
@@ -1091,7 +1087,8 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
         // (c4 5.06 -> 4.76 ms per op; four CTAs at 128 registers spill: 4.94 ms; the rows-path variants
         // spill at 168: no gain)
         if (A.wform == 2) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 4, 2, 0, 1>(A, Dt, st)
-                                   : run_plane_om<n, TX, TY, F, 0, 3, 0, 4, 2, 0, 2>(A, Dt, st);
+                                   : (output_mode(A, F) == 2 ? run_plane_om<n, TX, TY, F, 0, 3, 0, 4, 2, 2, 2>(A, Dt, st)
+                                                             : run_plane_om<n, TX, TY, F, 0, 3, 0, 4, 2, 0, 2>(A, Dt, st));
         return w ? run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 0, 0, 1>(A, Dt, st)
                  : run_plane_om<n, TX, TY, F, 0, 1, 0, 4, 0, 0, 2>(A, Dt, st);
       }
@@ -1141,12 +1138,18 @@ int run_plane(const TileArgs& A, const double* Drow, cudaStream_t st) {
           if (w && A.wform == 1 && v && atoi(v) == 42) return run_plane_om<n, TX, TY, F, 0, 3, 2, 1, 1, 0, 1>(A, Dt, st);
         }
 #endif
-        if (A.wform == 1) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 1>(A, Dt, st)
-                                   : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 2>(A, Dt, st);
+        if (A.wform == 1) {
+          if (w) return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 1>(A, Dt, st);
+          if (output_mode(A, F) == 2) return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 2, 2>(A, Dt, st);
+          return run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 1, 0, 2>(A, Dt, st);
+        }
+        const bool o2 = !w && output_mode(A, F) == 2;   // H_nu's (ng, 5) result rows: compile-time row stores
         if (A.wform == 2) return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 1>(A, Dt, st)
-                                   : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 2>(A, Dt, st);
+                                   : (o2 ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 2, 2>(A, Dt, st)
+                                         : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 2, 0, 2>(A, Dt, st));
         return w ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 1>(A, Dt, st)
-                 : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 2>(A, Dt, st);
+                 : (o2 ? run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 2, 2>(A, Dt, st)
+                       : run_plane_om<n, TX, TY, F, 0, 3, 0, 1, 0, 0, 2>(A, Dt, st));
       }
     }
     if (A.io) HV_FAIL(HV_ERR_UNSUPPORTED, "plane kernel: no tile-ordered mode for this shape");
