@@ -630,6 +630,15 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
     }
     __syncthreads();
     // ---- phase 3: element accumulator, then the column DSS
+    if constexpr (STG) {   // the next layer's q rows towards L1 / L2 now (its gids have landed); loaded at the end of the phase
+      if (l + 1 < nlay) {
+        wait_stage(l + 1);
+#pragma unroll
+        for (int jn = 0; jn < NPT; ++jn)
+          if (t0 + jn * NB < nn)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(q + (int64_t)s_g[t0 + jn * NB] * ldq + 2));
+      }
+    }
 #pragma unroll
     for (int jn = 0; jn < NPT; ++jn) {
       const int t = t0 + jn * NB;
