@@ -169,6 +169,9 @@ static __device__ __noinline__ double pow_slow(double x, double y) { return pow(
 
 // x^y, x > 0 expected (the EOS argument); anything the fast path does not cover goes to pow()
 HV_POW_HD double pow_pos(double x, double y) {
+#if defined(__CUDACC__) && !defined(__CUDA_ARCH__)
+  return std::pow(x, y);   // host pass of a .cu file: the coefficient tables are device symbols
+#else
   bool ok = false;
   const int ex = (int)(pw_bits(x) >> 52);   // sign and exponent: 523 .. 1523 <=> positive, 2^-500 <= x < 2^501
   const double v = pow_pos_core(x, y, &ok);
@@ -177,6 +180,7 @@ HV_POW_HD double pow_pos(double x, double y) {
   return pow_slow(x, y);
 #else
   return std::pow(x, y);
+#endif
 #endif
 }
 
