@@ -393,8 +393,10 @@ struct ElinesCfg {
 
 // NPT nodes per thread (blockDim = n^3 / NPT): NPT = 2 gives each thread twice the registers (2 x 256
 // threads x 128 at N = 7) so that both nodes' phase-1 loads are in flight together
-template <int n, int NPT>
-__global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::DTabEO<n> Dt, EulerConsts K,
+// FAST: the configuration of config 4 fixed at compile time (set 2C, all three directions, no Coriolis):
+// no runtime branches on K.set / K.dirs / K.omega in the phases
+template <int n, int NPT, bool FAST = false>
+__global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines_kernel(hv::DTabEO<n> Dt, EulerConsts Kin,
                                                           int64_t nelem, const int32_t* __restrict__ gid,
                                                           const double* __restrict__ w3,
                                                           const double* __restrict__ Mt, const double* __restrict__ q,
@@ -403,6 +405,12 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
   using C = ElinesCfg<n>;
   constexpr int nn = C::nn, N = n - 1, PI = C::PI, FS = C::FS, NB = nn / NPT;
   static_assert(nn % NPT == 0, "nodes per thread");
+  struct KC {   // the constants the phases branch on: compile-time in the FAST variant
+    double P_A, R, gamma, omega;
+    int set, dirs, coriolis;
+  };
+  const KC K = FAST ? KC{Kin.P_A, Kin.R, Kin.gamma, 0.0, 1, 7, 0}
+                    : KC{Kin.P_A, Kin.R, Kin.gamma, Kin.omega, Kin.set, Kin.dirs, Kin.coriolis};
   extern __shared__ double sm[];
   double* s_f = sm;                                      // [15][FS] fluxes, then line results
   double* s_carry = sm + C::OFF_C;                       // [2][n*n][5]
@@ -730,7 +738,8 @@ int run_lines(const double* Drow, const EulerConsts& K, int64_t nelem, const int
     HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     kern<<<(unsigned)A.ntiles, C::nn / (n == 8 ? 2 : 1), C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
   } else {
-    auto kern = euler_lines_kernel<n, 1>;
+    const bool fast = n == 8 && K.set == 1 && K.dirs == 7 && !(K.omega > 0.0);
+    auto kern = fast ? euler_lines_kernel<n, 1, true> : euler_lines_kernel<n, 1, false>;
     HV_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     kern<<<(unsigned)A.ntiles, ((C::nn + 31) / 32) * 32, C::SMEM, st>>>(Dt, K, nelem, gid, w3, Mt, q, ldq, A, elem);
   }
