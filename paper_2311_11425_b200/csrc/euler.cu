@@ -602,10 +602,12 @@ __global__ void __launch_bounds__(n * n * n / NPT, (n >= 8 ? 2 : 1)) euler_lines
       }
     }
     __syncthreads();
-    // the next layer's element record (13 metric components, gids, Minv) -> L2, so that its phase-1
-    // loads wait for L2 rather than DRAM
+    // the next layer's element record: the staged rows (grad xi / eta / zeta, Jg) and gids by bulk copy into
+    // the stage, free now that every thread is past its phase-1 reads; the rows phase 1 and 3 load
+    // directly (dPhi_m, M^-1; everything in the unstaged variant) -> L2, so that those loads wait for L2
+    // rather than DRAM
     if constexpr (STG) {
-      if (t0 == 32 && l + 1 < nlay) {   // the stage is free: every thread is past its phase-1 reads
+      if (t0 == 32 && l + 1 < nlay) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue_stage(s_el[l + 1]);
       }
